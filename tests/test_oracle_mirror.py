@@ -1,0 +1,145 @@
+"""Pins for oracle/mirror.py and oracle/predictor.py (CPU)."""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+from oracle import mirror
+from oracle import predictor as P
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def test_get_num_blocks_spec_examples():
+    for l, B, exp in gold("spec_examples.json")["get_num_blocks"]["cases"]:
+        assert mirror.get_num_blocks(l, B) == exp
+
+
+def test_get_num_blocks_brute():
+    for B in (1, 3, 16):
+        for l in range(0, 100):
+            assert mirror.get_num_blocks(l, B) == len(range(0, l, B))
+
+
+def test_allocator_script():
+    g = gold("allocator_script.json")
+    a = mirror.Allocator(g["num_blocks"])
+    for st in g["steps"]:
+        if st["op"] == "alloc":
+            s, ids = a.alloc(st["n"])
+            assert (s, ids) == (st["status"], st["ids"])
+        elif st["op"] == "retain":
+            assert a.retain(st["ids"]) == st["status"]
+        else:
+            assert a.release(st["ids"]) == st["status"]
+        assert a.num_free() == st["free"]
+
+
+def test_allocator_conservation_random():
+    rng = np.random.default_rng(0)
+    a = mirror.Allocator(64)
+    held = []   # one entry per outstanding reference
+    for _ in range(2000):
+        op = rng.integers(0, 3)
+        if op == 0:
+            s, ids = a.alloc(int(rng.integers(0, 9)))
+            if s == 0:
+                held += ids
+        elif op == 1 and held:
+            b = held[int(rng.integers(0, len(held)))]
+            assert a.retain([b]) == 0
+            held.append(b)
+        elif held:
+            b = held.pop(int(rng.integers(0, len(held))))
+            assert a.release([b]) == 0
+        assert a.num_free() + len(set(held)) == 64
+
+
+def test_batch_indices_hand_example():
+    # two requests, B=4: r0 c=5 n=3 table [7,2,9]; r1 c=0 n=2 table [4]; r2 decode sharing [7]
+    bt = [[7, 2, 9], [4, -1, -1], [7, 3, -1]]
+    cu, kv, slot, pg = mirror.batch_indices(bt, [5, 0, 4], [3, 2, 1], [1, 0, 1], 4)
+    assert cu.tolist() == [0, 3, 5, 6]
+    assert kv.tolist() == [8, 2, 5]
+    # p=5,6,7 -> block 2 offs 1,2,3 ; p=0,1 -> block 4 ; p=4 -> block 3 off 0
+    assert slot.tolist() == [2 * 4 + 1, 2 * 4 + 2, 2 * 4 + 3, 16, 17, 12]
+    assert pg.tolist() == [0, -1, 0]
+
+
+def test_validate_rules():
+    B, N = 4, 16
+    ok = dict(block_table=[[0, 1], [0, 2]], c=[4, 5], n=[1, 1], s=[1, 1])
+    assert mirror.validate(B=B, num_blocks=N, **ok) == 0
+    assert mirror.validate([[0, 1], [0, 2]], [4, 5], [0, 1], [1, 1], B, N) == mirror.E_INVALID
+    assert mirror.validate([[0, 1], [0, 2]], [4, 5], [1, 1], [0, 1], B, N) == mirror.E_INVALID
+    assert mirror.validate([[0, 16]], [4], [1], [0], B, N) == mirror.E_INVALID
+    assert mirror.validate([[3, 3]], [4], [1], [0], B, N) == mirror.E_INVALID
+    assert mirror.validate([[0, 1], [0, 2]], [3, 5], [1, 1], [1, 1], B, N, append=True) == mirror.E_SHARED_WRITE
+    assert mirror.validate([[0, 1, 5], [0, 2, 6]], [9, 9], [1, 1], [2, 2], B, N) == mirror.E_INVALID
+    assert mirror.validate([[0, 1]], [4], [1], [0], B, N, H_q=6, H_kv=4) == mirror.E_INVALID
+
+
+def test_featurize_spec_examples():
+    for case in gold("spec_examples.json")["featurize"]["cases"]:
+        f = P.features(case["c"], case["n"])
+        assert f[:6].tolist() == case["expect"]
+
+
+def test_predict_spec_example():
+    g = gold("spec_examples.json")["predict_affine"]
+    w = np.zeros(9)
+    w[0] = g["intercept"]
+    for k, name in enumerate(P.NAMES):
+        w[1 + k] = g["weights"].get(name, 0.0)
+    x = np.array([g["features"].get(nm, 0) for nm in P.NAMES], float)
+    assert abs(P.predict(w, x) - g["expected_ms"]) < 1e-12
+    assert P.predict(np.r_[-5.0, np.zeros(8)], x * 0) == 0.0
+
+
+def test_p2_and_dctx_closed_forms():
+    # single chunk at c=0: P2 = n(n+1)/2 = S_p^2/2 + S_p/2
+    f = P.features([0], [100])
+    assert f[6] == 100 * 101 / 2 == f[2] / 2 + f[0] / 2
+    # decode rows of one group sharing 64 tokens: D_ctx = sum(c+1) - (k-1)*64
+    f = P.features([100, 200, 300], [1, 1, 1], shared_tokens=[64] * 3, group=[0, 0, 0])
+    assert f[7] == 101 + 201 + 301 - 2 * 64
+
+
+def _synthetic(n, rng, w_true, mask, noise=0.0):
+    X = []
+    for _ in range(n):
+        R = int(rng.integers(1, 40))
+        c = rng.integers(0, 4000, R)
+        nn = np.where(rng.random(R) < 0.7, 1, rng.integers(2, 600, R))
+        c = np.where((nn == 1) & (c == 0), 1, c)
+        X.append(P.features(c, nn))
+    X = np.array(X)
+    A, cols = P.design(X, mask)
+    y = A @ np.r_[w_true[0], w_true[1:][cols]]
+    return X, y * (1 + noise * rng.standard_normal(n))
+
+
+def test_fit_recovers_noise_free():
+    rng = np.random.default_rng(1)
+    w_true = np.array([0.02, 1e-4, 0, 2e-9, 0, 3e-3, 1e-3, 5e-8, 4e-6])
+    X, y = _synthetic(500, rng, w_true, P.MASK_GRADED)
+    w = P.fit(X, y, P.MASK_GRADED)
+    _, cols = P.design(X, P.MASK_GRADED)
+    np.testing.assert_allclose(w[[0] + [1 + c for c in cols]], w_true[[0] + [1 + c for c in cols]],
+                               rtol=1e-7)
+    assert P.mape([P.predict(w, x) for x in X], y) < 1e-9
+
+
+def test_fit_noisy_heldout_mape():
+    rng = np.random.default_rng(2)
+    w_true = np.array([0.5, 1e-3, 0, 2e-7, 0, 3e-2, 1e-2, 0, 0])
+    X, y = _synthetic(2000, rng, w_true, P.MASK_EQ2_IDENT, noise=0.01)
+    w = P.fit(X[:1600], y[:1600], P.MASK_EQ2_IDENT)
+    assert P.mape([P.predict(w, x) for x in X[1600:]], y[1600:]) < 0.02

@@ -1,0 +1,454 @@
+"""bench.py -- one hybrid serving iteration's attention on B200 (HyGen hot path).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--extra]
+
+A "step" is one pass of the whole hot path over one batch:
+host plan (validation, indices, prefix tile map) + descriptor H2D + KV append
+(hg_kv_append) + hybrid attention (hg_hybrid_attention), all through the C ABI.
+The N=1 workload is BASELINE.json configs[1] (Llama-2-7B attention shape,
+512-token prefill chunk + 64 decodes at ctx 1-4K: "c1").  With --gpus N > 1
+(torchrun, one rank per GPU) KV heads are sharded across ranks and outputs are
+all-gathered with NCCL (hg_hybrid_attention_tp): total work fixed -> "strong".
+
+--impl reference times the fp64 CPU oracle (oracle/, the only reference this
+paper-only task has) on the host cores, on a bounded sample of the same
+workload, and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "mixed-batch attention tokens/s"
+UNIT = "tokens/s"
+WORKLOAD = "c1"
+WORKLOAD_DESC = ("Llama-2-7B attention shape (32 q/kv heads, head_dim 128, KV block 16): one online 512-token "
+                 "prefill chunk at c=0 + 64 decodes at ctx U[1024,4096] (32 online, 32 offline), bf16")
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling through NVML during the timed region."""
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.dev, self.period = device_index, period_s
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def alg_bytes_splitk(spec):
+    """Algorithmic bytes of the split-K (decode) kernel per launch: the unique KV
+    tokens read by decode rows (4*d*H_kv per token: K+V bf16; a shared prefix
+    handled by the tcgen05 prefix pass is excluded) plus Q read and O written
+    (2*d*H_q each per decode row).  SURVEY.md §8(d) per-unit figures."""
+    d, Hk, Hq, B = spec.d, spec.H_kv, spec.H_q, spec.B
+    kv_tok, rows = 0, 0
+    groups = {}
+    for i, r in enumerate(spec.requests):
+        if r.n != 1:
+            continue
+        rows += 1
+        s = spec.shared_blocks(i)
+        if s:
+            groups.setdefault(r.group, 0)
+            groups[r.group] += 1
+    for i, r in enumerate(spec.requests):
+        if r.n != 1:
+            continue
+        s = spec.shared_blocks(i)
+        pre = s * B if (s and groups.get(r.group, 0) >= 2) else 0
+        kv_tok += r.c + 1 - pre
+    return 4 * d * Hk * kv_tok + 4 * d * Hq * rows
+
+
+def alg_bytes_total(spec):
+    d, Hk, Hq, B = spec.d, spec.H_kv, spec.H_q, spec.B
+    U = sum(r.c + r.n for r in spec.requests)
+    seen = set()
+    for i, r in enumerate(spec.requests):
+        s = spec.shared_blocks(i)
+        if s:
+            if r.group in seen:
+                U -= s * B
+            seen.add(r.group)
+    return 4 * d * Hk * U + 4 * d * Hq * spec.T
+
+
+def alg_flops(spec):
+    return sum(4 * spec.d * spec.H_q * (r.n * r.c + r.n * (r.n + 1) // 2) for r in spec.requests)
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def run_ours(args):
+    import torch
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    from synth.configs import make_config
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    peaks, peak_kind = load_peaks()
+    spec = make_config(WORKLOAD, 0)
+
+    if world > 1:
+        return run_tp(args, spec, rank, world, dev, peaks, peak_kind)
+
+    wl = Workload(spec, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    opts = hg.make_opts(events=ev)
+    for _ in range(args.warmup):
+        wl.step(opts)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sk_ms, tc_ms, cb_ms = [], [], []
+    host_s = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush_l2(flush)                     # L2 flushed outside the timed events
+            starts[k].record(stream)
+            h0 = time.perf_counter()
+            wl.step(opts)
+            host_s.append(time.perf_counter() - h0)
+            ends[k].record(stream)
+            torch.cuda.synchronize()            # per-step kernel events must be read before reuse
+            st = hg.hg_last_plan_stats(wl.pool)
+            if st["splitk_items"]:
+                sk_ms.append(ev[2].elapsed_time(ev[3]))
+            if st["tc_tiles"]:
+                tc_ms.append(ev[0].elapsed_time(ev[1]))
+            if st["combine_rows"]:
+                cb_ms.append(ev[4].elapsed_time(ev[5]))
+        torch.cuda.synchronize()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    ms = total_ms / args.steps
+    stats = hg.hg_last_plan_stats(wl.pool)
+    launches_per_step = stats["kernels"] + 1    # + append
+    T = spec.T
+    value = T * args.steps / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (split-K decode: HBM-bound)
+    sk_avg = statistics.mean(sk_ms) if sk_ms else None
+    bytes_sk = alg_bytes_splitk(spec)
+    achieved = bytes_sk / (sk_avg / 1e3) / 1e9 if sk_avg else None
+    traffic = load_traffic("splitk_kernel", bytes_sk)
+    roofline = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)" if peak_kind == "measured" else "fallback",
+                "unit": "GB/s", "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+                "traffic": traffic, "alg_bytes_per_launch": bytes_sk, "avg_launch_ms": sk_avg,
+                "share_of_step": (sk_avg / ms) if sk_avg else None}
+    # whole-step roofline (all kernels): t_roof = max(bytes/BW, flops/TC)
+    bt, fl = alg_bytes_total(spec), alg_flops(spec)
+    t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
+    e2e = measure_e2e(wl, spec, args, stream)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded counter-based N(0,1)-scale bf16 Q/K/V; fragmented block tables)",
+        "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "tokens_per_step": T, "parallelism": "single GPU",
+                   "l2": "flushed (256 MB write) before every timed step, outside the events; KV working set 2.7 GB > L2"},
+        "roofline": roofline,
+        "step_roofline": {"alg_bytes": bt, "alg_flops": fl, "t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms},
+        "kernel_ms": {"splitk": sk_avg, "tc": statistics.mean(tc_ms) if tc_ms else None,
+                      "combine": statistics.mean(cb_ms) if cb_ms else None},
+        "host_call_ms": statistics.median(host_s) * 1e3,
+        "plan": stats,
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    if args.extra:
+        line["extra"] = extra_configs(args, peaks, dev)
+    line["cpu_baseline"] = cpu_baseline(spec, wl)
+    wl.close()
+    print(json.dumps(line))
+
+
+def load_traffic(kernel, alg_bytes):
+    """dram__bytes_read+write per launch for `kernel` from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        k = d["kernels"][kernel]
+        return {"bytes": k["dram_bytes"], "over_alg": k["dram_bytes"] / alg_bytes, "source": d.get("source", p)}
+    except Exception:
+        return None
+
+
+def measure_e2e(wl, spec, args, stream):
+    """Same metric through hg_hybrid_step_host: pinned host q/k/v in, host O out, copies timed."""
+    import torch
+    import paper_2501_14808_b200 as hg
+    qh = wl.q.cpu().pin_memory()
+    kh = wl.k_new.cpu().pin_memory()
+    vh = wl.v_new.cpu().pin_memory()
+    oh = torch.empty(wl.out.shape, dtype=torch.bfloat16).pin_memory()
+    ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
+                     device=wl.device)
+    for _ in range(args.warmup):
+        hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws, stream)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws, stream)
+    dt = time.perf_counter() - t0
+    h2d = (qh.numel() + kh.numel() + vh.numel()) * 2
+    return {"value": spec.T * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": oh.numel() * 2, "ms_per_step": dt / args.steps * 1e3,
+            "api": "hg_hybrid_step_host (C ABI, host buffers; synchronises each step)"}
+
+
+def cpu_baseline(spec, wl=None, sample_reqs=None):
+    """The fp64 oracle (as it stands) on the host cores, on a bounded sample of the
+    workload: the prefill request plus every 8th decode request; tokens/s is
+    extrapolated by the sample's share of the attention work (key-rows x heads)."""
+    import numpy as np
+    import oracle
+    from oracle.run import fill_pool
+    from synth.layout import make_layout
+    from synth.values import q_values
+    lay = wl.lay if wl is not None else make_layout(spec)
+    if sample_reqs is None:
+        dec = [i for i, r in enumerate(spec.requests) if r.n == 1]
+        pre = [i for i, r in enumerate(spec.requests) if r.n > 1]
+        sample_reqs = sorted(pre + dec[::8])
+    work = lambda idx: sum(r.n * r.c + r.n * (r.n + 1) // 2 for k, r in enumerate(spec.requests) if k in idx)
+    frac = work(set(sample_reqs)) / work(set(range(len(spec.requests))))
+    pool = fill_pool(spec, lay, req_sel=sample_reqs, device="cuda" if wl is not None else "cpu")
+    c = np.array([r.c for r in spec.requests], np.int32)
+    n = np.array([r.n for r in spec.requests], np.int32)
+    q = q_values(spec)
+    t0 = time.perf_counter()
+    pool.attention(lay.block_table, c, n, q, spec.H_q, req_sel=sample_reqs)
+    dt = time.perf_counter() - t0
+    t_full = dt / frac
+    return {"value": spec.T / t_full, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{len(sample_reqs)} of {len(spec.requests)} requests ({frac:.1%} of the attention work), "
+                      f"{dt:.2f} s; full-batch time extrapolated by work share",
+            "oracle_s_sample": dt}
+
+
+def extra_configs(args, peaks, dev):
+    """Other BASELINE.json configs (context; not the headline line)."""
+    import torch
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    from synth.configs import make_config
+    out = {}
+    for name in ("c2", "c3", "p1", "p2"):
+        spec = make_config(name, 0)
+        wl = Workload(spec, device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        opts = hg.make_opts(events=ev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        for _ in range(3):
+            wl.step(opts)
+        ms, ker = [], {"tc": [], "splitk": [], "combine": []}
+        for _ in range(10):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            wl.step(opts)
+            e.record()
+            torch.cuda.synchronize()
+            ms.append(s.elapsed_time(e))
+            st = hg.hg_last_plan_stats(wl.pool)
+            if st["tc_tiles"]:
+                ker["tc"].append(ev[0].elapsed_time(ev[1]))
+            if st["splitk_items"]:
+                ker["splitk"].append(ev[2].elapsed_time(ev[3]))
+            if st["combine_rows"]:
+                ker["combine"].append(ev[4].elapsed_time(ev[5]))
+        m = statistics.median(ms)
+        bt, fl = alg_bytes_total(spec), alg_flops(spec)
+        t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
+        out[name] = {"tokens_per_s": spec.T / (m / 1e3), "ms_per_step": m, "t_roof_ms": t_roof * 1e3,
+                     "step_roof_frac": t_roof * 1e3 / m, "alg_bytes": bt, "alg_flops": fl,
+                     "kernel_ms": {k: (statistics.median(v) if v else None) for k, v in ker.items()},
+                     "plan": hg.hg_last_plan_stats(wl.pool)}
+        wl.close()
+        del wl
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
+    """KV-head sharded attention on `world` GPUs + NCCL all-gather (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    assert spec.H_kv % world == 0
+    Hk, Hq = spec.H_kv // world, spec.H_q // world
+    local = spec.with_(H_kv=Hk, H_q=Hq)
+    # each rank's slice is generated as its own (smaller-head) workload; values are synthetic
+    wl = Workload(local, device=dev)
+    uid = [hg.hg_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = hg.Comm(uid[0], rank, world, dev.index)
+    out = torch.empty((spec.T, spec.H_q, spec.d), dtype=torch.bfloat16, device=dev)
+    ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q), dtype=torch.uint8,
+                     device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        wl.append()
+        hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, out, ws, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([s.elapsed_time(e)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = t.item()
+    if rank == 0:
+        ms = total_ms / args.steps
+        print(json.dumps({
+            "metric": METRIC, "value": spec.T * args.steps / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "parallelism": f"kv-head tp{world} + NCCL all-gather",
+                       "l2": "KV working set 2.7 GB total > L2"},
+            "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 2) * args.steps,
+            "clocks": clk.summary(),
+        }))
+    comm.close()
+    dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The fp64 CPU oracle timed as the reference arm (rank 0 only)."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from synth.configs import make_config
+    spec = make_config(WORKLOAD, 0)
+    base = None
+    times = []
+    for k in range(args.warmup + args.steps):
+        # each step: a bounded sample (the prefill request + 4 decodes, rotating)
+        dec = [i for i, r in enumerate(spec.requests) if r.n == 1]
+        sel = sorted([0] + dec[(4 * k) % len(dec):(4 * k) % len(dec) + 4])
+        cb = cpu_baseline(spec, None, sample_reqs=sel)
+        if k >= args.warmup:
+            times.append(spec.T / cb["value"])
+            base = cb
+    t = sum(times)
+    val = spec.T * len(times) / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t / len(times) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
+                         "sample": "per step: the prefill request + 4 rotating decodes; " + base["sample"]},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--extra", action="store_true", help="also time c2, c3, p1, p2 (context)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,245 @@
+/*
+ * hygen.h -- C ABI of the B200-native hybrid-batch attention library
+ * (HyGen, arXiv 2501.14808: one serving iteration's attention over a paged KV
+ * cache, with the batch-latency predictor that prices it).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (LaTeX source of the paper),
+ * S:n = SPEC.md line n, "§8(x)" = SURVEY.md section.
+ *
+ * Conventions for every entry point
+ *   - Returns hg_status (HG_OK = 0) unless stated; on error a thread-local
+ *     message is available from hg_last_error() and NOTHING has been written
+ *     (no device buffer, no pool metadata): validation precedes any launch.
+ *   - Device pointers are CUDA device addresses on the pool's device; host
+ *     pointers are ordinary (pageable or pinned) memory.  The caller owns all
+ *     device buffers (KV cache, q, out, lse, workspace) and all streams.
+ *   - `stream` is a cudaStream_t passed as void*; kernels are enqueued on it
+ *     and the call returns without synchronising.  A CUDA error raised by an
+ *     earlier launch surfaces as HG_E_CUDA on the next call.
+ *   - Element types: bf16 = IEEE bfloat16 stored as uint16; fp32; int32.
+ *   - Thread safety: one pool per thread at a time (no internal locking).
+ */
+#ifndef HYGEN_H_
+#define HYGEN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HG_API __attribute__((visibility("default")))
+#else
+#define HG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HG_OK = 0,
+    HG_E_INVALID = 1,        /* contract violation in arguments or batch */
+    HG_E_OOM = 2,            /* allocator cannot satisfy the request; message names the free count */
+    HG_E_SHARED_WRITE = 3,   /* append would write into a shared (read-only) prefix block */
+    HG_E_RANK_DEFICIENT = 4, /* predictor design matrix is rank deficient */
+    HG_E_CUDA = 5,           /* a CUDA runtime / driver call failed */
+    HG_E_NCCL = 6,           /* an NCCL call failed or NCCL is unavailable */
+    HG_E_UNSUPPORTED = 7     /* valid request outside what this build implements (e.g. head_dim) */
+} hg_status;
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+HG_API const char *hg_last_error(void);
+
+/* GET_NUM_BLOCKS(l) of Alg. 1: ceil(tokens / block_size),
+ * 0 for tokens <= 0.  Returns -1 if block_size < 1. */
+HG_API int32_t hg_get_num_blocks(int32_t tokens, int32_t block_size);
+
+/* ------------------------------------------------------------------------ */
+/* KV block pool (memory budget m of Alg. 1)        */
+/* ------------------------------------------------------------------------ */
+typedef struct hg_kv_pool hg_kv_pool; /* opaque: allocator metadata + TMA descriptors */
+
+typedef struct {
+    int32_t num_blocks;   /* N_blk >= 1 */
+    int32_t block_size;   /* B tokens per block: 16 (every shipped config; the only size this build accepts) */
+    int32_t num_kv_heads; /* KV heads held by THIS rank (H_kv / G under head sharding) */
+    int32_t head_dim;     /* d: 64 or 128 */
+    int32_t device;       /* CUDA ordinal of k_cache / v_cache */
+    void *k_cache;        /* caller-owned device bf16 [num_blocks][num_kv_heads][block_size][head_dim] */
+    void *v_cache;        /* same layout; 16-byte aligned */
+} hg_kv_pool_desc;
+
+HG_API hg_status hg_kv_pool_create(const hg_kv_pool_desc *desc, hg_kv_pool **out);
+HG_API hg_status hg_kv_pool_destroy(hg_kv_pool *pool);
+
+/* All-or-nothing allocation of n blocks: the n smallest free ids in ascending
+ * order, each with refcount 1 (deterministic, so head-sharded ranks make the
+ * same decisions with no metadata traffic, §8(e)).  HG_E_OOM if fewer than n
+ * are free (message: "need n, free f"). */
+HG_API hg_status hg_kv_alloc(hg_kv_pool *pool, int32_t n, int32_t *out_ids);
+/* refcount += 1 for each id (PSM prefix sharing).  All ids must be
+ * allocated, else HG_E_INVALID and nothing changes. */
+HG_API hg_status hg_kv_retain(hg_kv_pool *pool, const int32_t *ids, int32_t n);
+/* refcount -= 1 for each id (repeats count), freeing at 0.  HG_E_INVALID if
+ * any id would go below 0; nothing changes then. */
+HG_API hg_status hg_kv_release(hg_kv_pool *pool, const int32_t *ids, int32_t n);
+HG_API int32_t hg_kv_num_free(const hg_kv_pool *pool);
+HG_API int32_t hg_kv_refcount(const hg_kv_pool *pool, int32_t id); /* -1 if id out of range */
+
+/* ------------------------------------------------------------------------ */
+/* The batch: B = {(r, l, t_req)} of Alg. 1, extended with the  */
+/* paged-cache state of each request.                                        */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t num_reqs;            /* R >= 0 */
+    int32_t max_blocks_per_req;  /* W: row stride of block_table */
+    const int32_t *block_table;  /* host [R][W]; entries past GET_NUM_BLOCKS(c_i+n_i) ignored (-1 by convention) */
+    const int32_t *cached_len;   /* host [R]: c_i >= 0, tokens already in the cache */
+    const int32_t *new_len;      /* host [R]: n_i >= 1 new tokens this iteration (l of Alg. 1; 1 = decode) */
+    const uint8_t *is_offline;   /* host [R] or NULL: 0 online / 1 offline; no numeric effect (reading R6) */
+    const int32_t *shared_prefix_blocks; /* host [R] or NULL: s_i, block_table[i][0:s_i] are shared read-only
+                                            prefix blocks (PSM); requests with the same first
+                                            shared id must list identical sequences */
+} hg_batch;
+
+/* Write the new tokens' K and V rows into the cache: token j of request i
+ * (batch row t = cu_q[i] + j) goes to position p = c_i + j, i.e. block
+ * block_table[i][p / B], offset p % B, for every KV head.  k_new / v_new:
+ * device bf16 [T][H_kv][d], T = sum n_i.  Bit-exact copy.  HG_E_SHARED_WRITE
+ * if some p < s_i * B. */
+HG_API hg_status hg_kv_append(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
+                       const void *v_new, void *stream);
+
+/* Tuning / test switches for hg_hybrid_attention_ex (zero-initialise for defaults). */
+typedef struct {
+    int32_t split_tokens;       /* >0: fixed split-K chunk (multiple of B) for decode rows, making the
+                                   plan independent of load (bitwise reproducible across G, reading R18);
+                                   0: automatic (sized to fill the SMs) */
+    int32_t disable_prefix_pass;/* 1: no shared-prefix group pass (shared blocks read per request) */
+    int32_t disable_tc;         /* 1: prefill rows also go through the split-K kernel (no tcgen05) */
+    int32_t num_sms;            /* 0: device SM count */
+    void *events[6];            /* profiling: cudaEvent_t (or NULL) recorded on the stream right before /
+                                   after the tcgen05 kernel [0,1], the split-K kernel [2,3] and the
+                                   combine kernel [4,5] (bench.py's per-kernel roofline timing) */
+} hg_attn_opts;
+
+/* Bytes of device workspace hg_hybrid_attention needs for this batch. */
+HG_API hg_status hg_hybrid_attention_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
+                                             int32_t num_q_heads, size_t *bytes);
+
+/* One hybrid iteration's attention.  For request i,
+ * row j, q-head h (KV head g = h / (H_q/H_kv), reading R4):
+ *   O[t][h] = softmax_p( q . K_i(p) / sqrt(d) ) . V_i(p),  p = 0 .. c_i + j
+ * (causal, aligned to absolute positions -- chunked prefill P:63; decode
+ * rows n_i = 1 see c_i + 1 keys; quadratic/linear cost of P:188).
+ *   q   device bf16 [T][H_q][d], rows in request order
+ *   out device bf16 [T][H_q][d]
+ *   lse device fp32 [T][H_q] (natural log-sum-exp of the scaled scores) or NULL
+ * The new tokens' K/V must already be in the cache (hg_kv_append earlier on
+ * the same stream).  Descriptors are staged through pinned host memory and
+ * copied into `workspace` on `stream`. */
+HG_API hg_status hg_hybrid_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
+                              const void *q, void *out, float *lse, void *workspace,
+                              size_t workspace_bytes, void *stream);
+HG_API hg_status hg_hybrid_attention_ex(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
+                                 const void *q, void *out, float *lse, void *workspace,
+                                 size_t workspace_bytes, void *stream, const hg_attn_opts *opts);
+
+/* End-to-end serving step with HOST buffers (the e2e measurement of the
+ * bench): H2D of q/k_new/v_new (host bf16, pinned for async overlap) into the
+ * workspace, hg_kv_append, hg_hybrid_attention, D2H of out.  Synchronises the
+ * stream before returning so out_host is valid. */
+HG_API hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
+                              const void *q_host, const void *k_new_host, const void *v_new_host,
+                              void *out_host, void *workspace, size_t workspace_bytes, void *stream);
+HG_API hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
+                                             int32_t num_q_heads, size_t *bytes);
+
+/* Derived integer outputs, host arrays:
+ *   cu_q [R+1], kv_len [R], slot [T] = block_table[i][p/B]*B + p%B,
+ *   prefix_group [R]: -1 if s_i = 0, else groups numbered by first appearance. */
+HG_API hg_status hg_batch_indices(const hg_kv_pool *pool, const hg_batch *batch, int32_t *cu_q,
+                           int32_t *kv_len, int64_t *slot, int32_t *prefix_group);
+
+/* Plan statistics of the last attention call on this pool (for tests/bench). */
+typedef struct {
+    int32_t tc_tiles;        /* tcgen05 tiles (prefill + prefix group) */
+    int32_t prefix_tiles;    /* of which shared-prefix group tiles */
+    int32_t splitk_items;    /* split-K work items */
+    int32_t combine_rows;    /* (token, KV head) pairs merged by the combine kernel */
+    int32_t kernels;         /* kernels launched by the call */
+    int64_t kv_bytes_unique; /* algorithmic KV bytes: 4*d*H_kv*U */
+    int64_t kv_bytes_read;   /* KV bytes the plan streams from HBM */
+} hg_plan_stats;
+HG_API hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *out);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU: KV-head sharding + all-gather of outputs (§8(e); TP)    */
+/* ------------------------------------------------------------------------ */
+typedef struct hg_comm hg_comm;
+/* Writes a 128-byte NCCL unique id (rank 0 creates it; broadcast it with
+ * torch.distributed).  HG_E_NCCL if libnccl.so.2 cannot be loaded. */
+HG_API hg_status hg_comm_unique_id(void *out_128_bytes);
+HG_API hg_status hg_comm_init(const void *nccl_unique_id, int32_t rank, int32_t world, int32_t device,
+                       hg_comm **out);
+HG_API hg_status hg_comm_destroy(hg_comm *comm);
+/* Rank r holds KV heads [r*H_kv/G, (r+1)*H_kv/G) in `pool` and q-heads
+ * [r*H_q/G, (r+1)*H_q/G) in q_local ([T][H_q/G][d]); every rank receives the
+ * full out_gathered [T][H_q][d].  workspace must hold
+ * hg_hybrid_attention_tp_workspace_size bytes. */
+HG_API hg_status hg_hybrid_attention_tp_workspace_size(const hg_kv_pool *pool, const hg_comm *comm,
+                                                const hg_batch *batch, int32_t num_q_heads_total,
+                                                size_t *bytes);
+HG_API hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
+                                 int32_t num_q_heads_total, const void *q_local, void *out_gathered,
+                                 void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Batch-latency predictor (§4.2 Eq. 1; App. B Eq. 2)  */
+/* ------------------------------------------------------------------------ */
+/* Feature k has weight w[1+k]; w[0] is the intercept. */
+typedef struct {
+    double S_p;   /* 0: total prefill tokens */
+    double S_d;   /* 1: total decode tokens (= N_d: one token per decode) */
+    double S_p2;  /* 2: S_p^2 (Eq. 1) */
+    double S_d2;  /* 3: S_d^2 (Eq. 1 only) */
+    double N_p;   /* 4: prefill requests */
+    double N_d;   /* 5: decode requests */
+    double P2;    /* 6: attended prefill pairs sum n_i (c_i + (n_i+1)/2) (reading R14) */
+    double D_ctx; /* 7: unique KV tokens read by decode rows (reading R15) */
+} hg_features;
+
+#define HG_FEAT_S_P   (1 << 0)
+#define HG_FEAT_S_D   (1 << 1)
+#define HG_FEAT_S_P2  (1 << 2)
+#define HG_FEAT_S_D2  (1 << 3)
+#define HG_FEAT_N_P   (1 << 4)
+#define HG_FEAT_N_D   (1 << 5)
+#define HG_FEAT_P2    (1 << 6)
+#define HG_FEAT_D_CTX (1 << 7)
+/* Eq. 1 with the collinear S_d (= N_d) dropped, and the attention-aware fit. */
+#define HG_MASK_EQ1   (HG_FEAT_S_P | HG_FEAT_S_P2 | HG_FEAT_S_D2 | HG_FEAT_N_P | HG_FEAT_N_D)
+#define HG_MASK_EQ2   (HG_FEAT_S_P | HG_FEAT_S_P2 | HG_FEAT_N_P | HG_FEAT_N_D)
+#define HG_MASK_ATTN  (HG_FEAT_S_P | HG_FEAT_P2 | HG_FEAT_D_CTX | HG_FEAT_N_D | HG_FEAT_N_P)
+
+typedef struct {
+    double w[9];          /* w[0] intercept, w[1+k] feature k (0 for unselected) */
+    int32_t feature_mask; /* HG_FEAT_* bits used by the fit */
+    int32_t n_samples;
+    double train_mape;    /* mean |pred - y| / y on the training set */
+} hg_predictor;
+
+/* Features of a batch (decode row iff n_i == 1 and c_i >= 1, reading R5;
+ * shared prefixes counted once per group in D_ctx). */
+HG_API hg_status hg_batch_features(const hg_batch *batch, int32_t block_size, hg_features *out);
+/* Ordinary least squares of y_ms on [1, selected features] ("linear
+ * regression"), Householder QR in fp64 on column-scaled data.
+ * HG_E_RANK_DEFICIENT if the design has rank < 1 + popcount(mask). */
+HG_API hg_status hg_predictor_fit(const hg_features *X, const double *y_ms, int32_t n, int32_t feature_mask,
+                           hg_predictor *out);
+/* w . [1, x], floored at 0. */
+HG_API double hg_predictor_predict(const hg_predictor *model, const hg_features *x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYGEN_H_ */

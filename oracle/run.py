@@ -17,11 +17,14 @@ from synth.values import KIND_K, KIND_V, kv_values, q_values
 from . import OraclePool
 
 
-def fill_pool(spec, lay, req_sel=None, pool=None):
+def fill_pool(spec, lay, req_sel=None, pool=None, device="cpu"):
     """Oracle pool holding history + the iteration's new tokens.
 
     With ``req_sel`` only those requests (and their shared group prefixes) are
     written: a full-size pool stays lazily mapped except for the sampled blocks.
+    ``device`` only selects where synth evaluates its counter-based generator
+    (bit-identical on CPU and CUDA, tests/test_gpu_parity.py); values are
+    copied to host memory before the oracle sees them.
     """
     pool = pool or OraclePool(lay.num_blocks, spec.H_kv, spec.B, spec.d)
     sel = None if req_sel is None else set(int(i) for i in req_sel)
@@ -33,16 +36,16 @@ def fill_pool(spec, lay, req_sel=None, pool=None):
         ks, vs = [], []
         for k in rows:
             i = st.req[k]
-            ks.append(kv_values(spec, i, st.c[k], st.c[k] + st.n[k], KIND_K))
-            vs.append(kv_values(spec, i, st.c[k], st.c[k] + st.n[k], KIND_V))
+            ks.append(kv_values(spec, i, st.c[k], st.c[k] + st.n[k], KIND_K, device).cpu())
+            vs.append(kv_values(spec, i, st.c[k], st.c[k] + st.n[k], KIND_V, device).cpu())
         pool.append([st.tables[k] for k in rows], [st.c[k] for k in rows],
                      [st.n[k] for k in rows], torch.cat(ks), torch.cat(vs))
     idx = [i for i in range(len(spec.requests)) if sel is None or i in sel]
     if idx:
         ks = torch.cat([kv_values(spec, i, spec.requests[i].c, spec.requests[i].c + spec.requests[i].n,
-                                  KIND_K) for i in idx])
+                                  KIND_K, device).cpu() for i in idx])
         vs = torch.cat([kv_values(spec, i, spec.requests[i].c, spec.requests[i].c + spec.requests[i].n,
-                                  KIND_V) for i in idx])
+                                  KIND_V, device).cpu() for i in idx])
         pool.append(lay.block_table[idx], [spec.requests[i].c for i in idx],
                     [spec.requests[i].n for i in idx], ks, vs)
     return pool
@@ -54,11 +57,11 @@ def _group_needed(spec, i, sel):
         spec.requests[j].group == g and spec.shared_blocks(j) > 0 for j in sel)
 
 
-def run(spec, lay=None, req_sel=None, pool=None):
+def run(spec, lay=None, req_sel=None, pool=None, device="cpu"):
     """fp64 (O [T][H_q][d], LSE [T][H_q]) for the whole batch (rows of
     unselected requests are 0 / nan)."""
     lay = lay or make_layout(spec)
-    pool = fill_pool(spec, lay, req_sel, pool)
+    pool = fill_pool(spec, lay, req_sel, pool, device)
     c = np.array([r.c for r in spec.requests], np.int32)
     n = np.array([r.n for r in spec.requests], np.int32)
     q = q_values(spec)

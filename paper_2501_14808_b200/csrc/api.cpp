@@ -1,0 +1,593 @@
+// api.cpp -- C ABI entry points: KV pool + allocator, append, hybrid attention
+// orchestration (plan -> pinned staging -> H2D -> kernels), e2e host step,
+// batch indices, predictor (Eq. 1 / Eq. 2 linear regression).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <set>
+#include <vector>
+
+#include "hg_internal.h"
+
+using namespace hg;
+
+namespace hg {
+bool make_tensor_maps(hg_kv_pool *pool);  // tc_attn.cu
+}
+
+struct hg_kv_pool {
+    hg_kv_pool_desc desc{};
+    std::vector<int32_t> ref;
+    std::set<int32_t> free_ids;
+    int num_sms = 148;
+    // pinned staging ring for per-call descriptors
+    struct Stage {
+        void *host = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ev = nullptr;
+        bool pending = false;
+    };
+    Stage ring[4];
+    int ring_pos = 0;
+    alignas(64) unsigned char tmap_k[128];
+    alignas(64) unsigned char tmap_v[128];
+    bool tmap_ok = false;
+    hg_plan_stats last{};
+    Plan plan;  // reused storage
+};
+
+namespace hg {
+void *pool_tmap_k(hg_kv_pool *p) { return p->tmap_k; }
+void *pool_tmap_v(hg_kv_pool *p) { return p->tmap_v; }
+const hg_kv_pool_desc &pool_desc(hg_kv_pool *p) { return p->desc; }
+void pool_set_tmap_ok(hg_kv_pool *p, bool ok) { p->tmap_ok = ok; }
+}  // namespace hg
+
+static hg_status cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return HG_OK;
+    return fail(HG_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// Surface errors from earlier asynchronous launches (header contract).
+static hg_status sticky_check() {
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HG_E_CUDA, "earlier CUDA error: %s", cudaGetErrorString(e));
+    }
+    return HG_OK;
+}
+
+// Copy `bytes` of host data to `dst` on `stream` through a pinned staging buffer.
+static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return HG_OK;
+    auto &s = pool->ring[pool->ring_pos];
+    pool->ring_pos = (pool->ring_pos + 1) % 4;
+    if (s.pending) {
+        hg_status r = cuda_check(cudaEventSynchronize(s.ev), "staging event sync");
+        if (r) return r;
+        s.pending = false;
+    }
+    if (s.cap < bytes) {
+        if (s.host) cudaFreeHost(s.host);
+        size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+        hg_status r = cuda_check(cudaHostAlloc(&s.host, cap, cudaHostAllocDefault), "cudaHostAlloc");
+        if (r) { s.host = nullptr; s.cap = 0; return r; }
+        s.cap = cap;
+    }
+    if (!s.ev) {
+        hg_status r = cuda_check(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming), "event create");
+        if (r) return r;
+    }
+    memcpy(s.host, src, bytes);
+    hg_status r = cuda_check(cudaMemcpyAsync(dst, s.host, bytes, cudaMemcpyHostToDevice, st), "H2D descriptors");
+    if (r) return r;
+    r = cuda_check(cudaEventRecord(s.ev, st), "event record");
+    if (r) return r;
+    s.pending = true;
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// pool + allocator
+// ---------------------------------------------------------------------------
+extern "C" hg_status hg_kv_pool_create(const hg_kv_pool_desc *d, hg_kv_pool **out) {
+    if (!d || !out) return fail(HG_E_INVALID, "NULL argument");
+    if (d->num_blocks < 1 || d->num_kv_heads < 1) return fail(HG_E_INVALID, "num_blocks and num_kv_heads must be >= 1");
+    if (d->block_size != kBlock) return fail(HG_E_UNSUPPORTED, "block_size %d (this build: %d)", d->block_size, kBlock);
+    if (d->head_dim != 64 && d->head_dim != 128) return fail(HG_E_UNSUPPORTED, "head_dim %d (64 or 128)", d->head_dim);
+    if (!d->k_cache || !d->v_cache || ((uintptr_t)d->k_cache & 15) || ((uintptr_t)d->v_cache & 15))
+        return fail(HG_E_INVALID, "k_cache / v_cache must be non-NULL and 16-byte aligned");
+    hg_kv_pool *p = new hg_kv_pool();
+    p->desc = *d;
+    p->ref.assign((size_t)d->num_blocks, 0);
+    for (int32_t i = 0; i < d->num_blocks; ++i) p->free_ids.insert(p->free_ids.end(), i);
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device) == cudaSuccess && sms > 0)
+        p->num_sms = sms;
+    else
+        cudaGetLastError();
+    p->tmap_ok = make_tensor_maps(p);
+    *out = p;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
+    if (!p) return HG_OK;
+    for (auto &s : p->ring) {
+        if (s.pending) cudaEventSynchronize(s.ev);
+        if (s.host) cudaFreeHost(s.host);
+        if (s.ev) cudaEventDestroy(s.ev);
+    }
+    delete p;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_kv_alloc(hg_kv_pool *p, int32_t n, int32_t *out_ids) {
+    if (!p || (n > 0 && !out_ids) || n < 0) return fail(HG_E_INVALID, "bad arguments");
+    if ((size_t)n > p->free_ids.size())
+        return fail(HG_E_OOM, "need %d blocks, free %zu", n, p->free_ids.size());
+    auto it = p->free_ids.begin();
+    for (int32_t k = 0; k < n; ++k) {
+        out_ids[k] = *it;
+        p->ref[*it] = 1;
+        it = p->free_ids.erase(it);
+    }
+    return HG_OK;
+}
+
+extern "C" hg_status hg_kv_retain(hg_kv_pool *p, const int32_t *ids, int32_t n) {
+    if (!p || n < 0 || (n > 0 && !ids)) return fail(HG_E_INVALID, "bad arguments");
+    for (int32_t k = 0; k < n; ++k)
+        if (ids[k] < 0 || ids[k] >= p->desc.num_blocks || p->ref[ids[k]] == 0)
+            return fail(HG_E_INVALID, "retain of unallocated block %d", ids[k]);
+    for (int32_t k = 0; k < n; ++k) p->ref[ids[k]]++;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_kv_release(hg_kv_pool *p, const int32_t *ids, int32_t n) {
+    if (!p || n < 0 || (n > 0 && !ids)) return fail(HG_E_INVALID, "bad arguments");
+    std::vector<std::pair<int32_t, int32_t>> need;
+    for (int32_t k = 0; k < n; ++k) {
+        if (ids[k] < 0 || ids[k] >= p->desc.num_blocks) return fail(HG_E_INVALID, "release of block %d out of range", ids[k]);
+        need.push_back({ids[k], 1});
+    }
+    std::sort(need.begin(), need.end());
+    for (size_t a = 0; a < need.size();) {
+        size_t b = a;
+        int cnt = 0;
+        while (b < need.size() && need[b].first == need[a].first) cnt += need[b++].second;
+        if (p->ref[need[a].first] < cnt) return fail(HG_E_INVALID, "release of block %d below refcount 0", need[a].first);
+        a = b;
+    }
+    for (int32_t k = 0; k < n; ++k)
+        if (--p->ref[ids[k]] == 0) p->free_ids.insert(ids[k]);
+    return HG_OK;
+}
+
+extern "C" int32_t hg_kv_num_free(const hg_kv_pool *p) { return p ? (int32_t)p->free_ids.size() : 0; }
+
+extern "C" int32_t hg_kv_refcount(const hg_kv_pool *p, int32_t id) {
+    if (!p || id < 0 || id >= p->desc.num_blocks) return -1;
+    return p->ref[id];
+}
+
+// ---------------------------------------------------------------------------
+// a.1 indices
+// ---------------------------------------------------------------------------
+extern "C" hg_status hg_batch_indices(const hg_kv_pool *pool, const hg_batch *batch, int32_t *cu_q,
+                                      int32_t *kv_len, int64_t *slot, int32_t *prefix_group) {
+    if (!pool) return fail(HG_E_INVALID, "pool is NULL");
+    BatchView v;
+    hg_status s = view_batch(batch, &v);
+    if (s) return s;
+    s = validate(v, pool->desc.block_size, pool->desc.num_blocks, -1, 0, false);
+    if (s) return s;
+    const int B = pool->desc.block_size;
+    int64_t t = 0;
+    if (cu_q) cu_q[0] = 0;
+    for (int i = 0; i < v.R; ++i) {
+        if (cu_q) cu_q[i + 1] = cu_q[i] + v.n[i];
+        if (kv_len) kv_len[i] = v.c[i] + v.n[i];
+        for (int j = 0; j < v.n[i]; ++j, ++t) {
+            int64_t pos = (int64_t)v.c[i] + j;
+            if (slot) slot[t] = (int64_t)v.bt[(int64_t)i * v.W + pos / B] * B + pos % B;
+        }
+    }
+    if (prefix_group) {
+        std::vector<int32_t> g;
+        prefix_groups(v, &g);
+        memcpy(prefix_group, g.data(), sizeof(int32_t) * (size_t)v.R);
+    }
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// a.3 append
+// ---------------------------------------------------------------------------
+static hg_status append_impl(hg_kv_pool *pool, const BatchView &v, const void *k_new, const void *v_new,
+                             void *slot_dev, cudaStream_t st) {
+    const int B = pool->desc.block_size;
+    int64_t T = 0;
+    for (int i = 0; i < v.R; ++i) T += v.n[i];
+    if (T == 0) return HG_OK;
+    std::vector<int64_t> slot((size_t)T);
+    int64_t t = 0;
+    for (int i = 0; i < v.R; ++i)
+        for (int j = 0; j < v.n[i]; ++j, ++t) {
+            int64_t pos = (int64_t)v.c[i] + j;
+            slot[t] = (int64_t)v.bt[(int64_t)i * v.W + pos / B] * B + pos % B;
+        }
+    hg_status s = stage_h2d(pool, slot_dev, slot.data(), sizeof(int64_t) * (size_t)T, st);
+    if (s) return s;
+    return launch_append((const uint16_t *)k_new, (const uint16_t *)v_new, (uint16_t *)pool->desc.k_cache,
+                         (uint16_t *)pool->desc.v_cache, (const int64_t *)slot_dev, (int)T,
+                         pool->desc.num_kv_heads, pool->desc.head_dim, st);
+}
+
+// Small device scratch for append slots (pool-independent, grows on demand).
+static thread_local void *g_slot_dev = nullptr;
+static thread_local size_t g_slot_cap = 0;
+
+extern "C" hg_status hg_kv_append(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
+                                  const void *v_new, void *stream) {
+    if (!pool) return fail(HG_E_INVALID, "pool is NULL");
+    BatchView v;
+    hg_status s = view_batch(batch, &v);
+    if (s) return s;
+    s = validate(v, pool->desc.block_size, pool->desc.num_blocks, -1, 0, true);
+    if (s) return s;
+    s = sticky_check();
+    if (s) return s;
+    int64_t T = 0;
+    for (int i = 0; i < v.R; ++i) T += v.n[i];
+    if (T == 0) return HG_OK;
+    if (!k_new || !v_new) return fail(HG_E_INVALID, "k_new / v_new NULL");
+    size_t need = sizeof(int64_t) * (size_t)T;
+    if (g_slot_cap < need) {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (g_slot_dev) {
+            cudaStreamSynchronize(st);
+            cudaFree(g_slot_dev);
+        }
+        size_t cap = std::max<size_t>(need * 2, 1 << 16);
+        s = cuda_check(cudaMalloc(&g_slot_dev, cap), "cudaMalloc(slots)");
+        if (s) { g_slot_dev = nullptr; g_slot_cap = 0; return s; }
+        g_slot_cap = cap;
+    }
+    return append_impl(pool, v, k_new, v_new, g_slot_dev, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------
+// a.1-a.7 hybrid attention
+// ---------------------------------------------------------------------------
+static PlanOpts plan_opts(const hg_kv_pool *pool, const hg_attn_opts *o) {
+    PlanOpts po;
+    po.num_sms = pool->num_sms;
+    if (o) {
+        po.split_tokens = o->split_tokens;
+        po.prefix_pass = !o->disable_prefix_pass;
+        po.use_tc = !o->disable_tc;
+        if (o->num_sms > 0) po.num_sms = o->num_sms;
+    }
+    return po;
+}
+
+static hg_status plan_call(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const hg_attn_opts *o,
+                           BatchView *v, Plan *plan) {
+    hg_status s = view_batch(batch, v);
+    if (s) return s;
+    s = validate(*v, pool->desc.block_size, pool->desc.num_blocks, H_q, pool->desc.num_kv_heads, false);
+    if (s) return s;
+    PlanOpts po = plan_opts(pool, o);
+    if (!pool->tmap_ok) po.use_tc = false;
+    return build_plan(*v, H_q, pool->desc.num_kv_heads, pool->desc.head_dim, po, plan);
+}
+
+extern "C" hg_status hg_hybrid_attention_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
+                                                        int32_t num_q_heads, size_t *bytes) {
+    if (!pool || !bytes) return fail(HG_E_INVALID, "NULL argument");
+    BatchView v;
+    Plan plan;
+    hg_status s = plan_call(const_cast<hg_kv_pool *>(pool), batch, num_q_heads, nullptr, &v, &plan);
+    if (s) return s;
+    *bytes = plan.total_bytes;
+    return HG_OK;
+}
+
+static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, void *out,
+                                float *lse, void *ws, size_t ws_bytes, cudaStream_t st, const hg_attn_opts *o) {
+    BatchView v;
+    Plan &plan = pool->plan;
+    hg_status s = plan_call(pool, batch, H_q, o, &v, &plan);
+    if (s) return s;
+    s = sticky_check();
+    if (s) return s;
+    if (plan.T == 0) {
+        pool->last = hg_plan_stats{};
+        return HG_OK;
+    }
+    if (!q || !out) return fail(HG_E_INVALID, "q / out NULL");
+    if (!ws || ws_bytes < plan.total_bytes)
+        return fail(HG_E_INVALID, "workspace %zu bytes < required %zu", ws_bytes, plan.total_bytes);
+    // one image of all descriptors -> one pinned H2D copy
+    static thread_local std::vector<uint8_t> img;
+    img.assign(plan.desc_bytes, 0);
+    auto put = [&](size_t off, const void *src, size_t n) { if (n) memcpy(img.data() + off, src, n); };
+    put(plan.off_reqs, plan.reqs.data(), sizeof(ReqDev) * plan.reqs.size());
+    put(plan.off_bt, plan.bt_flat.data(), sizeof(int32_t) * plan.bt_flat.size());
+    put(plan.off_sk, plan.sk.data(), sizeof(SkItem) * plan.sk.size());
+    put(plan.off_tc, plan.tc.data(), sizeof(TcItem) * plan.tc.size());
+    put(plan.off_rows, plan.tc_rows.data(), sizeof(TcRow) * plan.tc_rows.size());
+    put(plan.off_cbase, plan.comb_base.data(), sizeof(int32_t) * plan.comb_base.size());
+    put(plan.off_comb, plan.comb.data(), sizeof(CombItem) * plan.comb.size());
+    s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
+    if (s) return s;
+    uint8_t *w = (uint8_t *)ws;
+    AttnParams p{};
+    p.k_cache = (const uint16_t *)pool->desc.k_cache;
+    p.v_cache = (const uint16_t *)pool->desc.v_cache;
+    p.q = (const uint16_t *)q;
+    p.out = (uint16_t *)out;
+    p.lse = lse;
+    p.reqs = (const ReqDev *)(w + plan.off_reqs);
+    p.bt_flat = (const int32_t *)(w + plan.off_bt);
+    p.sk = (const SkItem *)(w + plan.off_sk);
+    p.tc = (const TcItem *)(w + plan.off_tc);
+    p.tc_rows = (const TcRow *)(w + plan.off_rows);
+    p.comb_base = (const int32_t *)(w + plan.off_cbase);
+    p.comb = (const CombItem *)(w + plan.off_comb);
+    p.part_o = (float *)(w + plan.off_part_o);
+    p.part_lse = (float *)(w + plan.off_part_lse);
+    p.H_q = H_q;
+    p.H_kv = pool->desc.num_kv_heads;
+    p.G_q = H_q / p.H_kv;
+    p.d = pool->desc.head_dim;
+    p.n_sk = (int32_t)plan.sk.size();
+    p.n_tc = (int32_t)plan.tc.size();
+    p.n_comb = (int32_t)plan.comb.size();
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.d));
+    int kernels = 0;
+    auto rec = [&](int k) {
+        if (o && o->events[k]) cudaEventRecord((cudaEvent_t)o->events[k], st);
+    };
+    if (p.n_tc) {
+        rec(0);
+        s = launch_tc(p, pool->tmap_k, pool->tmap_v, st);
+        if (s) return s;
+        rec(1);
+        ++kernels;
+    }
+    if (p.n_sk) {
+        rec(2);
+        s = launch_splitk(p, st);
+        if (s) return s;
+        rec(3);
+        ++kernels;
+    }
+    if (p.n_comb) {
+        rec(4);
+        s = launch_combine(p, st);
+        if (s) return s;
+        rec(5);
+        ++kernels;
+    }
+    hg_plan_stats &ls = pool->last;
+    ls.tc_tiles = p.n_tc;
+    ls.prefix_tiles = plan.prefix_tiles;
+    ls.splitk_items = p.n_sk;
+    ls.combine_rows = p.n_comb;
+    ls.kernels = kernels;
+    ls.kv_bytes_unique = plan.kv_bytes_unique;
+    ls.kv_bytes_read = plan.kv_bytes_read;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_hybrid_attention_ex(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
+                                            const void *q, void *out, float *lse, void *workspace,
+                                            size_t workspace_bytes, void *stream, const hg_attn_opts *opts) {
+    if (!pool) return fail(HG_E_INVALID, "pool is NULL");
+    return attention_impl(pool, batch, num_q_heads, q, out, lse, workspace, workspace_bytes,
+                          (cudaStream_t)stream, opts);
+}
+
+extern "C" hg_status hg_hybrid_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
+                                         const void *q, void *out, float *lse, void *workspace,
+                                         size_t workspace_bytes, void *stream) {
+    return hg_hybrid_attention_ex(pool, batch, num_q_heads, q, out, lse, workspace, workspace_bytes, stream,
+                                  nullptr);
+}
+
+extern "C" hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *out) {
+    if (!pool || !out) return fail(HG_E_INVALID, "NULL argument");
+    *out = pool->last;
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// e2e step with host buffers
+// ---------------------------------------------------------------------------
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+extern "C" hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
+                                                        int32_t H_q, size_t *bytes) {
+    size_t attn = 0;
+    hg_status s = hg_hybrid_attention_workspace_size(pool, batch, H_q, &attn);
+    if (s) return s;
+    int64_t T = 0;
+    for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
+    const size_t d = pool->desc.head_dim, Hk = pool->desc.num_kv_heads;
+    *bytes = al256(attn) + 2 * al256(T * H_q * d * 2) + 2 * al256(T * Hk * d * 2) + al256(T * 8);
+    return HG_OK;
+}
+
+extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q,
+                                         const void *q_host, const void *k_new_host, const void *v_new_host,
+                                         void *out_host, void *workspace, size_t workspace_bytes, void *stream) {
+    if (!pool) return fail(HG_E_INVALID, "pool is NULL");
+    hg_status s = sticky_check();
+    if (s) return s;
+    size_t need = 0;
+    s = hg_hybrid_step_host_workspace_size(pool, batch, H_q, &need);
+    if (s) return s;
+    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    BatchView v;
+    s = view_batch(batch, &v);
+    if (s) return s;
+    s = validate(v, pool->desc.block_size, pool->desc.num_blocks, H_q, pool->desc.num_kv_heads, true);
+    if (s) return s;
+    int64_t T = 0;
+    for (int i = 0; i < v.R; ++i) T += v.n[i];
+    if (T == 0) return HG_OK;
+    size_t attn = 0;
+    s = hg_hybrid_attention_workspace_size(pool, batch, H_q, &attn);
+    if (s) return s;
+    const size_t d = pool->desc.head_dim, Hk = pool->desc.num_kv_heads;
+    uint8_t *w = (uint8_t *)workspace;
+    size_t off = al256(attn);
+    void *q_d = w + off;   off += al256(T * H_q * d * 2);
+    void *o_d = w + off;   off += al256(T * H_q * d * 2);
+    void *k_d = w + off;   off += al256(T * Hk * d * 2);
+    void *v_d = w + off;   off += al256(T * Hk * d * 2);
+    void *slot_d = w + off;
+    cudaStream_t st = (cudaStream_t)stream;
+    s = cuda_check(cudaMemcpyAsync(q_d, q_host, T * H_q * d * 2, cudaMemcpyHostToDevice, st), "H2D q");
+    if (s) return s;
+    s = cuda_check(cudaMemcpyAsync(k_d, k_new_host, T * Hk * d * 2, cudaMemcpyHostToDevice, st), "H2D k");
+    if (s) return s;
+    s = cuda_check(cudaMemcpyAsync(v_d, v_new_host, T * Hk * d * 2, cudaMemcpyHostToDevice, st), "H2D v");
+    if (s) return s;
+    s = append_impl(pool, v, k_d, v_d, slot_d, st);
+    if (s) return s;
+    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, workspace, attn, st, nullptr);
+    if (s) return s;
+    s = cuda_check(cudaMemcpyAsync(out_host, o_d, T * H_q * d * 2, cudaMemcpyDeviceToHost, st), "D2H out");
+    if (s) return s;
+    return cuda_check(cudaStreamSynchronize(st), "stream sync");
+}
+
+// ---------------------------------------------------------------------------
+// a.9 predictor: features, OLS (Householder QR), predict
+// ---------------------------------------------------------------------------
+extern "C" hg_status hg_batch_features(const hg_batch *batch, int32_t block_size, hg_features *out) {
+    if (!out || block_size < 1) return fail(HG_E_INVALID, "bad arguments");
+    BatchView v;
+    hg_status s = view_batch(batch, &v);
+    if (s) return s;
+    hg_features f{};
+    // groups of physically shared prefixes: key = first shared id (validated identical sequences)
+    std::vector<std::pair<int32_t, int32_t>> seen;  // (first id, shared tokens) of decode groups
+    for (int i = 0; i < v.R; ++i) {
+        const int64_t c = v.c[i], n = v.n[i];
+        if (n == 1 && c >= 1) {
+            f.N_d += 1;
+            f.S_d += 1;
+            f.D_ctx += (double)(c + 1);
+            if (v.s[i] > 0) {
+                const int32_t id0 = v.bt[(int64_t)i * v.W];
+                bool dup = false;
+                for (auto &e : seen)
+                    if (e.first == id0) { dup = true; break; }
+                if (dup) f.D_ctx -= (double)v.s[i] * block_size;
+                else seen.push_back({id0, v.s[i] * block_size});
+            }
+        } else {
+            f.N_p += 1;
+            f.S_p += (double)n;
+            f.P2 += (double)n * ((double)c + (double)(n + 1) / 2.0);
+        }
+    }
+    f.S_p2 = f.S_p * f.S_p;
+    f.S_d2 = f.S_d * f.S_d;
+    *out = f;
+    return HG_OK;
+}
+
+static void feat_vec(const hg_features &f, double x[8]) {
+    x[0] = f.S_p; x[1] = f.S_d; x[2] = f.S_p2; x[3] = f.S_d2;
+    x[4] = f.N_p; x[5] = f.N_d; x[6] = f.P2; x[7] = f.D_ctx;
+}
+
+extern "C" hg_status hg_predictor_fit(const hg_features *X, const double *y, int32_t n, int32_t mask,
+                                      hg_predictor *out) {
+    if (!X || !y || !out || n < 1 || (mask & ~0xFF)) return fail(HG_E_INVALID, "bad arguments");
+    int cols[8], k = 0;
+    for (int b = 0; b < 8; ++b)
+        if (mask >> b & 1) cols[k++] = b;
+    const int p = k + 1;
+    if (n < p) return fail(HG_E_RANK_DEFICIENT, "%d samples < %d parameters", n, p);
+    // A = [1, x_cols] scaled column-wise by max |.| (conditioning), column-major
+    std::vector<double> A((size_t)n * p), b(y, y + n), scale(p, 1.0);
+    for (int i = 0; i < n; ++i) {
+        double x[8];
+        feat_vec(X[i], x);
+        A[i] = 1.0;
+        for (int j = 0; j < k; ++j) A[(size_t)(j + 1) * n + i] = x[cols[j]];
+    }
+    for (int j = 0; j < p; ++j) {
+        double m = 0;
+        for (int i = 0; i < n; ++i) m = std::max(m, std::fabs(A[(size_t)j * n + i]));
+        if (m == 0) return fail(HG_E_RANK_DEFICIENT, "feature column %d is identically zero", j);
+        scale[j] = m;
+        for (int i = 0; i < n; ++i) A[(size_t)j * n + i] /= m;
+    }
+    // Householder QR, applying reflections to b
+    std::vector<double> diag(p);
+    double rmax = 0;
+    for (int j = 0; j < p; ++j) {
+        double *aj = &A[(size_t)j * n];
+        double norm = 0;
+        for (int i = j; i < n; ++i) norm += aj[i] * aj[i];
+        norm = std::sqrt(norm);
+        double alpha = aj[j] > 0 ? -norm : norm;
+        diag[j] = alpha;
+        rmax = std::max(rmax, std::fabs(alpha));
+        if (std::fabs(alpha) <= 1e-12 * std::max(rmax, 1.0))
+            return fail(HG_E_RANK_DEFICIENT, "design matrix is rank deficient at column %d (mask 0x%x)", j, mask);
+        aj[j] -= alpha;  // v = a - alpha e_j
+        double vnorm2 = 0;
+        for (int i = j; i < n; ++i) vnorm2 += aj[i] * aj[i];
+        auto reflect = [&](double *c) {
+            double dot = 0;
+            for (int i = j; i < n; ++i) dot += aj[i] * c[i];
+            double f = 2.0 * dot / vnorm2;
+            for (int i = j; i < n; ++i) c[i] -= f * aj[i];
+        };
+        for (int jj = j + 1; jj < p; ++jj) reflect(&A[(size_t)jj * n]);
+        reflect(b.data());
+    }
+    // back substitution R w = Q^T b (R upper: diag[j] on the diagonal, A above)
+    std::vector<double> w(p);
+    for (int j = p - 1; j >= 0; --j) {
+        double acc = b[j];
+        for (int jj = j + 1; jj < p; ++jj) acc -= A[(size_t)jj * n + j] * w[jj];
+        w[j] = acc / diag[j];
+    }
+    hg_predictor m{};
+    m.w[0] = w[0] / scale[0];
+    for (int j = 0; j < k; ++j) m.w[1 + cols[j]] = w[j + 1] / scale[j + 1];
+    m.feature_mask = mask;
+    m.n_samples = n;
+    double err = 0;
+    for (int i = 0; i < n; ++i) err += std::fabs(hg_predictor_predict(&m, &X[i]) - y[i]) / y[i];
+    m.train_mape = err / n;
+    *out = m;
+    return HG_OK;
+}
+
+extern "C" double hg_predictor_predict(const hg_predictor *m, const hg_features *f) {
+    if (!m || !f) return 0.0;
+    double x[8];
+    feat_vec(*f, x);
+    double acc = m->w[0];
+    for (int k = 0; k < 8; ++k) acc += m->w[1 + k] * x[k];
+    return acc > 0 ? acc : 0.0;
+}
+
+namespace hg {
+int pool_num_kv_heads(const hg_kv_pool *p) { return p->desc.num_kv_heads; }
+int pool_head_dim(const hg_kv_pool *p) { return p->desc.head_dim; }
+}  // namespace hg

@@ -1,0 +1,140 @@
+// comm.cpp -- multi-GPU step of the hot path:
+// rank r owns KV heads [r*H_kv/G, (r+1)*H_kv/G) and their q-heads, runs the
+// single-GPU path on its slice, then the outputs are all-gathered over NVLink
+// with NCCL (tensor-parallel attention; the paper runs TP=2).
+//
+// NCCL is loaded with dlopen (libnccl.so.2, the copy torch ships) so the
+// library has no link-time NCCL dependency; only the ABI below is used.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstring>
+
+#include "hg_internal.h"
+
+namespace {
+typedef int nccl_result;
+typedef void *nccl_comm;
+struct nccl_uid { char internal[128]; };
+enum { kNcclBf16 = 9 };
+
+struct NcclApi {
+    bool loaded = false;
+    nccl_result (*GetUniqueId)(nccl_uid *) = nullptr;
+    nccl_result (*CommInitRank)(nccl_comm *, int, nccl_uid, int) = nullptr;
+    nccl_result (*CommDestroy)(nccl_comm) = nullptr;
+    nccl_result (*AllGather)(const void *, void *, size_t, int, nccl_comm, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(nccl_result) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+    if (g_nccl.loaded) return true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        const char *p = getenv("HG_NCCL_PATH");
+        if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) return false;
+    g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+    g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    g_nccl.loaded = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather;
+    return g_nccl.loaded;
+}
+}  // namespace
+
+struct hg_comm {
+    nccl_comm comm = nullptr;
+    int rank = 0, world = 1, device = 0;
+};
+
+using namespace hg;
+
+namespace hg {
+hg_status launch_gather_transpose(const uint16_t *src, uint16_t *dst, int G, int T, int row_elems, void *stream);
+int pool_num_kv_heads(const hg_kv_pool *p);
+int pool_head_dim(const hg_kv_pool *p);
+}  // namespace hg
+
+extern "C" hg_status hg_comm_unique_id(void *out) {
+    if (!out) return fail(HG_E_INVALID, "NULL argument");
+    if (!load_nccl()) return fail(HG_E_NCCL, "libnccl.so.2 not loadable (set HG_NCCL_PATH)");
+    nccl_uid id;
+    nccl_result r = g_nccl.GetUniqueId(&id);
+    if (r) return fail(HG_E_NCCL, "ncclGetUniqueId: %d", r);
+    memcpy(out, id.internal, 128);
+    return HG_OK;
+}
+
+extern "C" hg_status hg_comm_init(const void *uid, int32_t rank, int32_t world, int32_t device, hg_comm **out) {
+    if (!uid || !out || world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "bad arguments");
+    if (!load_nccl()) return fail(HG_E_NCCL, "libnccl.so.2 not loadable (set HG_NCCL_PATH)");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(HG_E_CUDA, "cudaSetDevice(%d)", device);
+    nccl_uid id;
+    memcpy(id.internal, uid, 128);
+    hg_comm *c = new hg_comm();
+    nccl_result r = g_nccl.CommInitRank(&c->comm, world, id, rank);
+    if (r) {
+        delete c;
+        return fail(HG_E_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+    }
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    *out = c;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_comm_destroy(hg_comm *c) {
+    if (!c) return HG_OK;
+    if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+    delete c;
+    return HG_OK;
+}
+
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+extern "C" hg_status hg_hybrid_attention_tp_workspace_size(const hg_kv_pool *pool, const hg_comm *comm,
+                                                           const hg_batch *batch, int32_t H_q, size_t *bytes) {
+    if (!pool || !comm || !batch || !bytes) return fail(HG_E_INVALID, "NULL argument");
+    if (H_q % comm->world) return fail(HG_E_INVALID, "num_q_heads %d not divisible by world %d", H_q, comm->world);
+    size_t attn = 0;
+    hg_status s = hg_hybrid_attention_workspace_size(pool, batch, H_q / comm->world, &attn);
+    if (s) return s;
+    int64_t T = 0;
+    for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
+    *bytes = al256(attn) + al256((size_t)T * H_q * pool_head_dim(pool) * 2);
+    return HG_OK;
+}
+
+extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
+                                            const void *q_local, void *out_gathered, void *workspace,
+                                            size_t workspace_bytes, void *stream) {
+    if (!pool || !comm || !batch) return fail(HG_E_INVALID, "NULL argument");
+    size_t need = 0;
+    hg_status s = hg_hybrid_attention_tp_workspace_size(pool, comm, batch, H_q, &need);
+    if (s) return s;
+    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    const int G = comm->world, Hl = H_q / G, d = pool_head_dim(pool);
+    int64_t T = 0;
+    for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
+    size_t attn = 0;
+    s = hg_hybrid_attention_workspace_size(pool, batch, Hl, &attn);
+    if (s) return s;
+    uint8_t *w = (uint8_t *)workspace;
+    uint16_t *gather = (uint16_t *)(w + al256(attn));  // [G][T][Hl][d], rank-major (NCCL layout)
+    const size_t count = (size_t)T * Hl * d;
+    uint16_t *mine = gather + (size_t)comm->rank * count;
+    s = hg_hybrid_attention(pool, batch, Hl, q_local, mine, nullptr, workspace, attn, stream);
+    if (s) return s;
+    if (T == 0) return HG_OK;
+    if (G > 1) {
+        nccl_result r = g_nccl.AllGather(mine, gather, count, kNcclBf16, comm->comm, (cudaStream_t)stream);
+        if (r) return fail(HG_E_NCCL, "ncclAllGather: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+    }
+    // [G][T][Hl*d] -> [T][G*Hl*d]
+    return launch_gather_transpose(gather, (uint16_t *)out_gathered, G, (int)T, Hl * d, stream);
+}

@@ -1,0 +1,146 @@
+// hg_internal.h -- structures shared by the host planner (host.cpp / api.cpp)
+// and the sm_100a kernels (kernels.cu, tc_attn.cu).  Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "hygen.h"
+
+namespace hg {
+
+constexpr int kBlock = 16;        // KV block size B handled by the kernels
+constexpr int kSkRows = 16;       // query rows per split-K item (one m16 MMA tile)
+constexpr int kTcRows = 128;      // query rows per tcgen05 tile (UMMA M)
+constexpr int kTcKeys = 128;      // keys per tcgen05 KV tile (UMMA N of S = Q K^T)
+
+// Per-request record in the device descriptor.
+struct ReqDev {
+    int32_t c;       // cached length c_i
+    int32_t n;       // new tokens n_i
+    int32_t cu_q;    // first batch row of the request
+    int32_t bt_off;  // offset of the request's block ids in bt_flat
+};
+
+// Split-K item (sm_100a mma.sync path, kernels.cu): up to 16 stacked query rows
+// (token j0 + r / G_q, head g*G_q + r % G_q) of one request against keys
+// [k0, k1) further capped per row by causality (key <= c + j).
+struct SkItem {
+    int32_t req;
+    int32_t g;
+    int32_t j0;
+    int32_t nt;     // token rows in the item (nt * G_q <= 16)
+    int32_t k0;     // multiple of kBlock
+    int32_t k1;
+    int32_t part;   // partial index for rows that are combined
+    int32_t pad;
+};
+
+// tcgen05 tile (tc_attn.cu): 128 stacked rows sharing KV head g and a key
+// range [k0, k1) of ONE block table (the request's, or the group prefix's).
+// Rows are listed in tc_rows[row0 .. row0 + nrows).
+struct TcItem {
+    int32_t bt_off;  // block table (bt_flat offset) the keys are read through
+    int32_t g;
+    int32_t k0;      // multiple of kTcKeys
+    int32_t k1;
+    int32_t row0;
+    int32_t nrows;   // <= 128
+    int32_t part;    // partial index (-1: rows written directly)
+    int32_t pad;
+};
+
+// One stacked query row of a tcgen05 tile.
+struct TcRow {
+    int32_t t;       // batch token
+    int32_t h;       // q head
+    int32_t lim;     // exclusive key limit (causal: c + j + 1; prefix: k1)
+    int32_t pad;
+};
+
+// (token, KV head) pair whose rows are merged from several partials.
+struct CombItem {
+    int32_t t;
+    int32_t g;
+    int32_t base;    // first partial slot; slot = base + part * G_q + (h % G_q)
+    int32_t nparts;
+};
+
+// Device-side view of one attention call.
+struct AttnParams {
+    const uint16_t *k_cache;
+    const uint16_t *v_cache;
+    const uint16_t *q;
+    uint16_t *out;
+    float *lse;
+    const ReqDev *reqs;
+    const int32_t *bt_flat;
+    const SkItem *sk;
+    const TcItem *tc;
+    const TcRow *tc_rows;
+    const int32_t *comb_base;  // [T * H_kv]: first partial slot of (t, g) or -1 (direct write)
+    const CombItem *comb;
+    float *part_o;             // [slots][d] normalised partial outputs
+    float *part_lse;           // [slots] log2-domain LSE of each partial (-inf: empty)
+    int32_t H_q, H_kv, G_q, d;
+    int32_t n_sk, n_tc, n_comb;
+    float scale_log2;          // log2(e) / sqrt(d)
+};
+
+// Host-side plan (a.1 + a.4): built per call, staged to the device.
+struct Plan {
+    int R = 0, T = 0, W = 0;
+    std::vector<ReqDev> reqs;
+    std::vector<int32_t> bt_flat;
+    std::vector<SkItem> sk;
+    std::vector<TcItem> tc;
+    std::vector<TcRow> tc_rows;
+    std::vector<int32_t> comb_base;
+    std::vector<CombItem> comb;
+    int64_t n_slots = 0;
+    int32_t prefix_tiles = 0;
+    int64_t kv_bytes_unique = 0;
+    int64_t kv_bytes_read = 0;
+    // device layout (byte offsets inside the workspace)
+    size_t off_reqs = 0, off_bt = 0, off_sk = 0, off_tc = 0, off_rows = 0, off_cbase = 0,
+           off_comb = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
+};
+
+// ---- host helpers (host.cpp) ------------------------------------------------
+void set_error(const char *fmt, ...);
+hg_status fail(hg_status s, const char *fmt, ...);
+
+struct BatchView {
+    int R, W;
+    const int32_t *bt, *c, *n, *s;
+    std::vector<int32_t> s_store;  // zeros when shared_prefix_blocks == NULL
+};
+hg_status view_batch(const hg_batch *b, BatchView *v);
+// Validation rules of SURVEY §8(b); num_q_heads < 0 skips the head check.
+hg_status validate(const BatchView &v, int block_size, int num_blocks, int num_q_heads, int H_kv,
+                   bool append);
+void prefix_groups(const BatchView &v, std::vector<int32_t> *group);
+
+struct KernelEvents {
+    void *ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+struct PlanOpts {
+    int split_tokens = 0;
+    bool prefix_pass = true;
+    bool use_tc = true;
+    int num_sms = 148;
+};
+hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpts &o, Plan *p);
+
+// ---- kernel launchers (kernels.cu / tc_attn.cu) -----------------------------
+hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache,
+                        uint16_t *v_cache, const int64_t *slot, int T, int H_kv, int d,
+                        void *stream);
+hg_status launch_splitk(const AttnParams &p, void *stream);
+hg_status launch_combine(const AttnParams &p, void *stream);
+hg_status launch_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v, void *stream);
+int tc_supported(int d);
+
+}  // namespace hg

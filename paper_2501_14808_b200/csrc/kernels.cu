@@ -1,0 +1,455 @@
+// kernels.cu -- sm_100a kernels of the HBM-bound half of the hot path:
+//   append_kernel   a.3  paged KV write (16-byte vector copies)
+//   splitk_kernel   a.6  split-K attention for decode rows (and small row groups):
+//                        per (request, KV head, key range) item, up to 16 stacked
+//                        query rows (token x q-head of one GQA group) against
+//                        paged KV blocks streamed by cp.async with 16-byte
+//                        coalesced loads; QK^T and PV on mma.sync m16n8k16
+//                        (bf16 in, fp32 accumulate) because GQA decode is
+//                        G_q FLOP/B and CUDA-core FMA cannot keep up with HBM
+//                        at G_q >= 4; warp-shuffle online
+//                        softmax; 4 warps split the item's blocks and merge
+//                        through shared memory.
+//   combine_kernel  a.7  log-sum-exp merge of split / prefix partials.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "hg_internal.h"
+
+namespace hg {
+
+// ----------------------------------------------------------------------------
+// a.3 append: K[slot] = K_new[t], V[slot] = V_new[t] for every KV head.
+// ----------------------------------------------------------------------------
+__global__ void append_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
+                              uint4 *__restrict__ k_cache, uint4 *__restrict__ v_cache,
+                              const int64_t *__restrict__ slot, int T, int H_kv, int chunks_per_row) {
+    // one 16-byte chunk of K and of V per thread; rows = (t, g)
+    const int64_t total = (int64_t)T * H_kv * chunks_per_row;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = idx / chunks_per_row;
+        const int ch = (int)(idx % chunks_per_row);
+        const int64_t t = row / H_kv;
+        const int g = (int)(row % H_kv);
+        const int64_t s = slot[t];
+        const int64_t blk = s / kBlock, off = s % kBlock;
+        const int64_t dst = ((blk * H_kv + g) * kBlock + off) * chunks_per_row + ch;
+        k_cache[dst] = k_new[idx];
+        v_cache[dst] = v_new[idx];
+    }
+}
+
+hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache,
+                        uint16_t *v_cache, const int64_t *slot, int T, int H_kv, int d, void *stream) {
+    if (T == 0) return HG_OK;
+    const int cpr = d / 8;
+    const int64_t total = (int64_t)T * H_kv * cpr;
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+    append_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+        (const uint4 *)k_new, (const uint4 *)v_new, (uint4 *)k_cache, (uint4 *)v_cache, slot, T, H_kv, cpr);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
+}
+
+// ----------------------------------------------------------------------------
+// PTX helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+// D = A * B + D, m16n8k16, bf16 inputs, fp32 accumulators
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&v);
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Byte offset of 16-byte chunk `ch` of row `row` in a [rows][D] bf16 tile whose
+// chunks are XOR-swizzled by (row & 7): ldmatrix of 8 rows at one chunk index
+// then touches 8 distinct bank groups.
+template <int D>
+__device__ __forceinline__ uint32_t swz(int row, int ch) {
+    return (uint32_t)(row * D * 2 + ((ch ^ (row & 7)) << 4));
+}
+
+// ----------------------------------------------------------------------------
+// a.6 split-K attention item kernel
+// ----------------------------------------------------------------------------
+constexpr int kSkWarps = 4;
+constexpr int kSkStages = 2;
+
+template <int D>
+struct SkSmem {
+    static constexpr int kTile = kBlock * D * 2;            // one K (or V) block tile, bytes
+    static constexpr int kStage = 2 * kTile;                 // K + V
+    static constexpr int kWarp = kSkStages * kStage;
+    static constexpr int kQ = kSkRows * D * 2;
+    static constexpr int kMerge = kSkWarps * (kSkRows * D + 2 * kSkRows) * 4;
+    static constexpr int kMain = kSkWarps * kWarp;
+    static constexpr int kBytes = kQ + (kMain > kMerge ? kMain : kMerge);
+};
+
+template <int D>
+__global__ void __launch_bounds__(kSkWarps * 32)
+splitk_kernel(const AttnParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int NCH = D / 8;   // 16-byte chunks per row
+    constexpr int NKS = D / 16;  // k-steps over the head dim
+    constexpr int NNT = D / 8;   // n-tiles over the head dim (PV)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const SkItem it = p.sk[blockIdx.x];
+    const ReqDev rq = p.reqs[it.req];
+    const int G = p.G_q;
+    const int nrows = it.nt * G;
+    uint8_t *sQ = smem;
+    uint8_t *sKV = smem + SkSmem<D>::kQ;
+
+    // ---- Q tile (16 rows, zero padded) -> smem (swizzled) --------------------
+    for (int idx = threadIdx.x; idx < kSkRows * NCH; idx += blockDim.x) {
+        const int r = idx / NCH, ch = idx % NCH;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (r < nrows) {
+            const int t = rq.cu_q + it.j0 + r / G;
+            const int h = it.g * G + r % G;
+            val = *reinterpret_cast<const uint4 *>(p.q + ((int64_t)t * p.H_q + h) * D + ch * 8);
+        }
+        *reinterpret_cast<uint4 *>(sQ + swz<D>(r, ch)) = val;
+    }
+    // per-row causal limit (exclusive), rows this lane owns: r0 = lane/4, r1 = r0 + 8
+    const int ra = lane >> 2, rb = ra + 8;
+    auto row_lim = [&](int r) -> int {
+        if (r >= nrows) return 0;
+        const int lim = rq.c + it.j0 + r / G + 1;
+        return lim < it.k1 ? lim : it.k1;
+    };
+    const int lim_a = row_lim(ra), lim_b = row_lim(rb);
+
+    // ---- this warp's blocks ----------------------------------------------------
+    const int kb0 = it.k0 / kBlock;
+    const int kb_end = (it.k1 + kBlock - 1) / kBlock;
+    const int nblk_w = (kb_end - kb0 - warp + kSkWarps - 1) / kSkWarps;  // may be <= 0
+    const int32_t *bt = p.bt_flat + rq.bt_off;
+    uint8_t *sW = sKV + warp * SkSmem<D>::kWarp;
+    const uint32_t sW_u = smem_u32(sW);
+    const int64_t head_stride = (int64_t)kBlock * D;            // elements per (block, head)
+    auto issue = [&](int bi, int stage) {
+        const int kb = kb0 + warp + bi * kSkWarps;
+        const int64_t base = ((int64_t)bt[kb] * p.H_kv + it.g) * head_stride;
+        const uint16_t *gk = p.k_cache + base;
+        const uint16_t *gv = p.v_cache + base;
+        const uint32_t dk = sW_u + stage * SkSmem<D>::kStage;
+        const uint32_t dv = dk + SkSmem<D>::kTile;
+#pragma unroll
+        for (int i = 0; i < kBlock * NCH / 32; ++i) {
+            const int id = lane + 32 * i;
+            const int r = id / NCH, ch = id % NCH;
+            cp_async16(dk + swz<D>(r, ch), gk + r * D + ch * 8);
+            cp_async16(dv + swz<D>(r, ch), gv + r * D + ch * 8);
+        }
+    };
+    if (nblk_w > 0) issue(0, 0);
+    cp_async_commit();
+    __syncthreads();  // Q tile visible
+
+    // Q A-fragments (all warps hold the same 16 x D tile)
+    uint32_t qa[NKS][4];
+    {
+        const uint32_t sQ_u = smem_u32(sQ);
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+            const int r = lane & 15;
+            const int ch = 2 * ks + (lane >> 4);
+            ldsm_x4(sQ_u + swz<D>(r, ch), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+        }
+    }
+
+    float o[NNT][4];
+#pragma unroll
+    for (int nt = 0; nt < NNT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    float m_a = -CUDART_INF_F, m_b = -CUDART_INF_F;  // running max (log2 domain)
+    float l_a = 0.f, l_b = 0.f;                      // per-lane partial sums
+
+    for (int bi = 0; bi < nblk_w; ++bi) {
+        const int stage = bi & 1;
+        if (bi + 1 < nblk_w) issue(bi + 1, stage ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const uint32_t sk = sW_u + stage * SkSmem<D>::kStage;
+        const uint32_t sv = sk + SkSmem<D>::kTile;
+        // ---- S = Q K^T (16 rows x 16 keys) ----
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+            uint32_t b0, b1, b2, b3;
+            const int key = (lane & 7) + ((lane >> 4) << 3);
+            const int ch = 2 * ks + ((lane >> 3) & 1);
+            ldsm_x4(sk + swz<D>(key, ch), b0, b1, b2, b3);
+            mma_bf16(s0, qa[ks], b0, b1);
+            mma_bf16(s1, qa[ks], b2, b3);
+        }
+        // ---- mask + online softmax (rows ra, rb; cols 2*(lane&3)+{0,1} (+8)) ----
+        const int kbase = (kb0 + warp + bi * kSkWarps) * kBlock;
+        const int c0 = kbase + 2 * (lane & 3);
+        float x[8];
+        x[0] = (c0 < lim_a) ? s0[0] * p.scale_log2 : -CUDART_INF_F;
+        x[1] = (c0 + 1 < lim_a) ? s0[1] * p.scale_log2 : -CUDART_INF_F;
+        x[2] = (c0 < lim_b) ? s0[2] * p.scale_log2 : -CUDART_INF_F;
+        x[3] = (c0 + 1 < lim_b) ? s0[3] * p.scale_log2 : -CUDART_INF_F;
+        x[4] = (c0 + 8 < lim_a) ? s1[0] * p.scale_log2 : -CUDART_INF_F;
+        x[5] = (c0 + 9 < lim_a) ? s1[1] * p.scale_log2 : -CUDART_INF_F;
+        x[6] = (c0 + 8 < lim_b) ? s1[2] * p.scale_log2 : -CUDART_INF_F;
+        x[7] = (c0 + 9 < lim_b) ? s1[3] * p.scale_log2 : -CUDART_INF_F;
+        float mxa = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[4], x[5]));
+        float mxb = fmaxf(fmaxf(x[2], x[3]), fmaxf(x[6], x[7]));
+        mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 1));
+        mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 2));
+        mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 1));
+        mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 2));
+        const float mna = fmaxf(m_a, mxa), mnb = fmaxf(m_b, mxb);
+        const float refa = (mna == -CUDART_INF_F) ? 0.f : mna;
+        const float refb = (mnb == -CUDART_INF_F) ? 0.f : mnb;
+        const float alpha_a = fast_exp2(m_a - refa), alpha_b = fast_exp2(m_b - refb);
+        m_a = mna;
+        m_b = mnb;
+        float pr[8];
+        pr[0] = fast_exp2(x[0] - refa); pr[1] = fast_exp2(x[1] - refa);
+        pr[2] = fast_exp2(x[2] - refb); pr[3] = fast_exp2(x[3] - refb);
+        pr[4] = fast_exp2(x[4] - refa); pr[5] = fast_exp2(x[5] - refa);
+        pr[6] = fast_exp2(x[6] - refb); pr[7] = fast_exp2(x[7] - refb);
+        l_a = l_a * alpha_a + (pr[0] + pr[1] + pr[4] + pr[5]);
+        l_b = l_b * alpha_b + (pr[2] + pr[3] + pr[6] + pr[7]);
+        if (__any_sync(0xffffffffu, alpha_a != 1.f || alpha_b != 1.f)) {
+#pragma unroll
+            for (int nt = 0; nt < NNT; ++nt) {
+                o[nt][0] *= alpha_a; o[nt][1] *= alpha_a;
+                o[nt][2] *= alpha_b; o[nt][3] *= alpha_b;
+            }
+        }
+        // P as the A operand (16 x 16 keys): a0=(ra, k0..1) a1=(rb, k0..1) a2=(ra, k8..9) a3=(rb, k8..9)
+        uint32_t pa[4];
+        pa[0] = pack_bf16(pr[0], pr[1]);
+        pa[1] = pack_bf16(pr[2], pr[3]);
+        pa[2] = pack_bf16(pr[4], pr[5]);
+        pa[3] = pack_bf16(pr[6], pr[7]);
+        // ---- O += P V ----
+#pragma unroll
+        for (int c2 = 0; c2 < NNT / 2; ++c2) {
+            uint32_t b0, b1, b2, b3;
+            const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
+            const int ch = 2 * c2 + (lane >> 4);
+            ldsm_x4_t(sv + swz<D>(key, ch), b0, b1, b2, b3);
+            mma_bf16(o[2 * c2], pa, b0, b1);
+            mma_bf16(o[2 * c2 + 1], pa, b2, b3);
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+    // ---- reduce l over the quad, then merge the 4 warps through smem ----------
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+    __syncthreads();  // all warps done with their KV stages
+    float *mo = reinterpret_cast<float *>(sKV);                     // [warp][16][D]
+    float *mml = mo + kSkWarps * kSkRows * D;                       // [warp][16][2]
+    {
+        float *ow = mo + warp * kSkRows * D;
+        const int cc = 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < NNT; ++nt) {
+            ow[ra * D + nt * 8 + cc] = o[nt][0];
+            ow[ra * D + nt * 8 + cc + 1] = o[nt][1];
+            ow[rb * D + nt * 8 + cc] = o[nt][2];
+            ow[rb * D + nt * 8 + cc + 1] = o[nt][3];
+        }
+        if ((lane & 3) == 0) {
+            mml[(warp * kSkRows + ra) * 2 + 0] = m_a;
+            mml[(warp * kSkRows + ra) * 2 + 1] = l_a;
+            mml[(warp * kSkRows + rb) * 2 + 0] = m_b;
+            mml[(warp * kSkRows + rb) * 2 + 1] = l_b;
+        }
+    }
+    __syncthreads();
+    // 128 threads: thread -> (row r = tid / 8, dim chunk of D/8 elements)
+    {
+        const int r = threadIdx.x >> 3;
+        const int part8 = threadIdx.x & 7;
+        if (r < nrows) {
+            float M = -CUDART_INF_F;
+#pragma unroll
+            for (int w = 0; w < kSkWarps; ++w) M = fmaxf(M, mml[(w * kSkRows + r) * 2]);
+            const float ref = (M == -CUDART_INF_F) ? 0.f : M;
+            float f[kSkWarps], L = 0.f;
+#pragma unroll
+            for (int w = 0; w < kSkWarps; ++w) {
+                f[w] = fast_exp2(mml[(w * kSkRows + r) * 2] - ref);
+                L += f[w] * mml[(w * kSkRows + r) * 2 + 1];
+            }
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+            const int t = rq.cu_q + it.j0 + r / G;
+            const int h = it.g * G + r % G;
+            const int base = (it.part >= 0) ? p.comb_base[(int64_t)t * p.H_kv + it.g] : -1;
+            constexpr int PER = D / 8;
+            float acc[PER];
+#pragma unroll
+            for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int w = 0; w < kSkWarps; ++w) {
+                const float fw = f[w] * inv;
+                const float *src = mo + (w * kSkRows + r) * D + part8 * PER;
+#pragma unroll
+                for (int e = 0; e < PER; ++e) acc[e] += fw * src[e];
+            }
+            const float lse2 = (L > 0.f) ? ref + __log2f(L) : -CUDART_INF_F;
+            if (base < 0) {
+                uint16_t *dst = p.out + ((int64_t)t * p.H_q + h) * D + part8 * PER;
+#pragma unroll
+                for (int e = 0; e < PER; e += 8) {
+                    uint4 v;
+                    v.x = pack_bf16(acc[e + 0], acc[e + 1]);
+                    v.y = pack_bf16(acc[e + 2], acc[e + 3]);
+                    v.z = pack_bf16(acc[e + 4], acc[e + 5]);
+                    v.w = pack_bf16(acc[e + 6], acc[e + 7]);
+                    *reinterpret_cast<uint4 *>(dst + e) = v;
+                }
+                if (p.lse && part8 == 0) p.lse[(int64_t)t * p.H_q + h] = lse2 * 0.69314718055994531f;
+            } else {
+                const int64_t slot = base + (int64_t)it.part * G + (r % G);
+                float *dst = p.part_o + slot * D + part8 * PER;
+#pragma unroll
+                for (int e = 0; e < PER; e += 4)
+                    *reinterpret_cast<float4 *>(dst + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+                if (part8 == 0) p.part_lse[slot] = lse2;
+            }
+        }
+    }
+}
+
+template <int D>
+static hg_status launch_splitk_d(const AttnParams &p, cudaStream_t st) {
+    constexpr int bytes = SkSmem<D>::kBytes;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(splitk_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        attr = true;
+    }
+    splitk_kernel<D><<<p.n_sk, kSkWarps * 32, bytes, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "split-K launch: %s", cudaGetErrorString(e));
+}
+
+hg_status launch_splitk(const AttnParams &p, void *stream) {
+    if (p.n_sk == 0) return HG_OK;
+    if (p.d == 128) return launch_splitk_d<128>(p, (cudaStream_t)stream);
+    if (p.d == 64) return launch_splitk_d<64>(p, (cudaStream_t)stream);
+    return fail(HG_E_UNSUPPORTED, "head_dim %d", p.d);
+}
+
+// ----------------------------------------------------------------------------
+// a.7 combine: O = sum_s 2^{lse_s - LSE} o_s, LSE = log2 sum_s 2^{lse_s}
+// one warp per (token, KV head, q-head-in-group)
+// ----------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int G = p.G_q;
+    if (wid >= p.n_comb * G) return;
+    const CombItem ci = p.comb[wid / G];
+    const int hl = wid % G;
+    float M = -CUDART_INF_F;
+    for (int s = 0; s < ci.nparts; ++s) M = fmaxf(M, p.part_lse[ci.base + s * G + hl]);
+    const float ref = (M == -CUDART_INF_F) ? 0.f : M;
+    float L = 0.f;
+    for (int s = 0; s < ci.nparts; ++s) L += fast_exp2(p.part_lse[ci.base + s * G + hl] - ref);
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    constexpr int PER = D / 32;
+    float acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    for (int s = 0; s < ci.nparts; ++s) {
+        const int64_t slot = ci.base + (int64_t)s * G + hl;
+        const float w = fast_exp2(p.part_lse[slot] - ref) * inv;
+        const float *src = p.part_o + slot * D + lane * PER;
+#pragma unroll
+        for (int e = 0; e < PER; e += 2) {
+            float2 v = *reinterpret_cast<const float2 *>(src + e);
+            acc[e] += w * v.x;
+            acc[e + 1] += w * v.y;
+        }
+    }
+    const int h = ci.g * G + hl;
+    uint16_t *dst = p.out + ((int64_t)ci.t * p.H_q + h) * D + lane * PER;
+#pragma unroll
+    for (int e = 0; e < PER; e += 2) *reinterpret_cast<uint32_t *>(dst + e) = pack_bf16(acc[e], acc[e + 1]);
+    if (p.lse && lane == 0)
+        p.lse[(int64_t)ci.t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
+}
+
+hg_status launch_combine(const AttnParams &p, void *stream) {
+    if (p.n_comb == 0) return HG_OK;
+    const int64_t warps = (int64_t)p.n_comb * p.G_q;
+    const int blocks = (int)((warps * 32 + 255) / 256);
+    if (p.d == 128) combine_kernel<128><<<blocks, 256, 0, (cudaStream_t)stream>>>(p);
+    else if (p.d == 64) combine_kernel<64><<<blocks, 256, 0, (cudaStream_t)stream>>>(p);
+    else return fail(HG_E_UNSUPPORTED, "head_dim %d", p.d);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "combine launch: %s", cudaGetErrorString(e));
+}
+
+}  // namespace hg
+
+namespace hg {
+// [G][T][E] -> [T][G][E] (E = H_q/G * d bf16 elements), 16-byte chunks.
+__global__ void gather_transpose_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int G, int T,
+                                        int chunks) {
+    const int64_t total = (int64_t)G * T * chunks;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % chunks);
+        const int64_t rt = i / chunks;
+        const int t = (int)(rt % T);
+        const int r = (int)(rt / T);
+        dst[((int64_t)t * G + r) * chunks + c] = src[i];
+    }
+}
+
+hg_status launch_gather_transpose(const uint16_t *src, uint16_t *dst, int G, int T, int row_elems, void *stream) {
+    const int chunks = row_elems / 8;
+    const int64_t total = (int64_t)G * T * chunks;
+    if (total == 0) return HG_OK;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    gather_transpose_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)src, (uint4 *)dst, G, T, chunks);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "transpose launch: %s", cudaGetErrorString(e));
+}
+}  // namespace hg

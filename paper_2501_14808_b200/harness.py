@@ -1,0 +1,92 @@
+"""Load a synthetic workload (synth.BatchSpec) into a device KV pool through the
+C ABI, and run the iteration.  Used by tests/ (GPU parity) and bench.py.
+
+Everything numeric happens in libhygen.so: the history is written with
+hg_kv_append, the iteration with hg_kv_append + hg_hybrid_attention.  Token
+values come from synth's counter-based generator evaluated on the device.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import paper_2501_14808_b200 as hg
+from synth.layout import Layout, history_steps, make_layout
+from synth.values import KIND_K, KIND_V, kv_values, q_values
+
+
+class Workload:
+    def __init__(self, spec, lay: Layout = None, device="cuda", populate=True, append_chunk_tokens=1 << 16):
+        self.spec = spec
+        self.lay = lay or make_layout(spec)
+        self.device = torch.device(device)
+        N, H, d = self.lay.num_blocks, spec.H_kv, spec.d
+        self.k_cache = torch.zeros((N, H, spec.B, d), dtype=torch.bfloat16, device=self.device)
+        self.v_cache = torch.zeros((N, H, spec.B, d), dtype=torch.bfloat16, device=self.device)
+        self.pool = hg.KVPool(self.k_cache, self.v_cache, N, spec.B, H, d,
+                              self.device.index if self.device.index is not None else torch.cuda.current_device())
+        c = [r.c for r in spec.requests]
+        n = [r.n for r in spec.requests]
+        self.batch = hg.Batch(self.lay.block_table, c, n, [int(r.offline) for r in spec.requests], self.lay.shared)
+        self.q = q_values(spec, device=self.device)
+        self.k_new = self._kv_new(KIND_K)
+        self.v_new = self._kv_new(KIND_V)
+        T = spec.T
+        self.out = torch.empty((T, spec.H_q, d), dtype=torch.bfloat16, device=self.device)
+        self.lse = torch.empty((T, spec.H_q), dtype=torch.float32, device=self.device)
+        self.ws = None
+        self.chunk = append_chunk_tokens
+        if populate:
+            self.populate()
+
+    def _kv_new(self, kind):
+        parts = [kv_values(self.spec, i, r.c, r.c + r.n, kind, device=self.device)
+                 for i, r in enumerate(self.spec.requests)]
+        if not parts:
+            return torch.empty((0, self.spec.H_kv, self.spec.d), dtype=torch.bfloat16, device=self.device)
+        return torch.cat(parts)
+
+    def populate(self):
+        """History appends: every request's first c_i tokens (group prefixes once)."""
+        spec = self.spec
+        for st in history_steps(spec, self.lay):
+            rows = list(range(len(st.c)))
+            start = 0
+            while start < len(rows):
+                tok, end = 0, start
+                while end < len(rows) and (end == start or tok + st.n[rows[end]] <= self.chunk):
+                    tok += st.n[rows[end]]
+                    end += 1
+                sel = rows[start:end]
+                ks = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_K, device=self.device)
+                                for k in sel])
+                vs = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_V, device=self.device)
+                                for k in sel])
+                # pseudo rows writing a group prefix have s = 0; private history starts at s*B
+                shared = [0 if st.c[k] == 0 else spec.shared_blocks(st.req[k]) for k in sel]
+                b = hg.Batch(np.array([st.tables[k] for k in sel], np.int32), [st.c[k] for k in sel],
+                             [st.n[k] for k in sel], None, shared)
+                hg.hg_kv_append(self.pool, b, ks, vs)
+                start = end
+        torch.cuda.synchronize(self.device)
+
+    def workspace(self, opts=None):
+        need = hg.hg_hybrid_attention_workspace_size(self.pool, self.batch, self.spec.H_q)
+        need = max(need, 1 << 20) * 2   # plans with opts may differ a little; keep headroom
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self.ws
+
+    def append(self, stream=None):
+        hg.hg_kv_append(self.pool, self.batch, self.k_new, self.v_new, stream)
+
+    def attention(self, opts=None, lse=True, stream=None):
+        hg.hg_hybrid_attention(self.pool, self.batch, self.spec.H_q, self.q, self.out,
+                               self.lse if lse else None, self.workspace(opts), stream, opts)
+
+    def step(self, opts=None, stream=None):
+        self.append(stream)
+        self.attention(opts, stream=stream)
+
+    def close(self):
+        self.pool.close()

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances (north_star, BASELINE.json): rel-L2 <= 5e-3
+and max-abs <= 2e-2 over the output tensor; LSE within 1e-3 absolute; the
+paged cache after append bit-exact; indices bit-exact (tests/test_host_lib.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+REL_L2, MAX_ABS, LSE_ABS = 5e-3, 2e-2, 1e-3
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    _cuda()
+    import paper_2501_14808_b200 as hg
+    hg.lib()   # raises if the extension is missing: no fallback
+    yield
+
+
+def rows_of(spec, i):
+    s = sum(r.n for r in spec.requests[:i])
+    return slice(s, s + spec.requests[i].n)
+
+
+def compare(spec, wl, req_sel=None, check_lse=True, tag=""):
+    from oracle.run import run
+    o_ref, lse_ref = run(spec, wl.lay, req_sel=req_sel, device="cuda")
+    out = wl.out.float().cpu().double().numpy()
+    lse = wl.lse.cpu().double().numpy()
+    sel = range(len(spec.requests)) if req_sel is None else req_sel
+    idx = np.concatenate([np.arange(rows_of(spec, i).start, rows_of(spec, i).stop) for i in sel])
+    a, b = out[idx], o_ref[idx]
+    rel = np.linalg.norm(a - b) / np.linalg.norm(b)
+    mx = np.abs(a - b).max()
+    worst = max(np.linalg.norm(out[rows_of(spec, i)] - o_ref[rows_of(spec, i)]) /
+                np.linalg.norm(o_ref[rows_of(spec, i)]) for i in sel)
+    print(f"{spec.name}{tag}: rel-L2 {rel:.3e} max-abs {mx:.3e} worst-request rel-L2 {worst:.3e}")
+    assert rel <= REL_L2 and mx <= MAX_ABS, (rel, mx)
+    if check_lse:
+        dl = np.abs(lse[idx] - lse_ref[idx]).max()
+        assert dl <= LSE_ABS, dl
+    return rel, mx
+
+
+def make(spec, **kw):
+    from paper_2501_14808_b200.harness import Workload
+    return Workload(spec, **kw)
+
+
+def test_values_generator_cpu_gpu_bit_identical():
+    from synth.values import gen_block
+    pos = torch.arange(0, 3000)
+    a = gen_block(3, 1, 77, pos, 4, 128, scale=4.0)
+    b = gen_block(3, 1, 77, pos.cuda(), 4, 128, scale=4.0).cpu()
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+@pytest.mark.parametrize("name", ["toy_a", "toy_b"])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("q_scale", [1.0, 4.0])
+def test_toy(name, seed, q_scale):
+    from synth.configs import make_config
+    spec = make_config(name, seed, q_scale)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    compare(spec, wl)
+
+
+@pytest.mark.parametrize("name", ["toy_a", "toy_b"])
+def test_append_bit_exact(name):
+    from oracle.run import fill_pool
+    from synth.configs import make_config
+    spec = make_config(name, 0)
+    wl = make(spec)
+    wl.append()
+    torch.cuda.synchronize()
+    pool = fill_pool(spec, wl.lay)
+    k = wl.k_cache.cpu().view(torch.int16).numpy().view(np.uint16)
+    v = wl.v_cache.cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(k, pool.K) and np.array_equal(v, pool.V)
+
+
+def test_tag_flip_bit_identical():
+    from synth.configs import make_config
+    spec = make_config("toy_b", 1)
+    wl = make(spec)
+    wl.step()
+    a = wl.out.clone()
+    flipped = spec.with_(requests=[r.__class__(**{**r.__dict__, "offline": not r.offline}) for r in spec.requests])
+    wl2 = make(flipped, lay=wl.lay)
+    wl2.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int16), wl2.out.view(torch.int16))
+
+
+def test_block_permutation_within_tolerance():
+    from synth.configs import make_fuzz
+    from synth.layout import make_layout
+    spec = make_fuzz(7)
+    wl1 = make(spec, lay=make_layout(spec, seed=1))
+    wl2 = make(spec, lay=make_layout(spec, seed=2))
+    wl1.step()
+    wl2.step()
+    torch.cuda.synchronize()
+    a, b = wl1.out.double(), wl2.out.double()
+    assert (a - b).abs().max().item() <= MAX_ABS
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_fuzz(seed):
+    from synth.configs import make_fuzz
+    spec = make_fuzz(seed)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    compare(spec, wl)
+
+
+@pytest.mark.parametrize("variant", ["default", "no_tc", "split64", "no_prefix"])
+@pytest.mark.parametrize("seed", range(8))
+def test_plan_variants(variant, seed):
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_fuzz
+    spec = make_fuzz(100 + seed)
+    opts = {"default": None, "no_tc": hg.make_opts(disable_tc=True), "split64": hg.make_opts(split_tokens=64),
+            "no_prefix": hg.make_opts(disable_prefix_pass=True)}[variant]
+    wl = make(spec)
+    wl.append()
+    wl.attention(opts)
+    torch.cuda.synchronize()
+    compare(spec, wl, tag=f"[{variant}]")
+
+
+def test_shared_vs_private_copies():
+    from synth.configs import make_config
+    spec = make_config("toy_a", 2)
+    priv = spec.with_(requests=[r.__class__(**{**r.__dict__, "share": False}) for r in spec.requests])
+    a, b = make(spec), make(priv)
+    a.step()
+    b.step()
+    torch.cuda.synchronize()
+    assert (a.out.double() - b.out.double()).abs().max().item() <= MAX_ABS
+    compare(spec, a)
+    compare(priv, b)
+
+
+def _sample(spec, k=6):
+    """Requests checked at full size: every prefill request, plus decodes spread over the batch."""
+    pre = [i for i, r in enumerate(spec.requests) if r.n > 1]
+    dec = [i for i, r in enumerate(spec.requests) if r.n == 1]
+    step = max(1, len(dec) // k)
+    return sorted(set(pre + dec[::step][:k] + dec[-1:]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c1_long", "c2", "c2_g8", "c2_none", "c3", "p1", "p2"])
+def test_full_size_sampled(name):
+    from synth.configs import make_config
+    spec = make_config(name, 0)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    sel = _sample(spec) if name not in ("p1", "p2") else [0] if name == "p2" else [0, 3]
+    compare(spec, wl, req_sel=sel)
+    wl.close()
+
+
+@pytest.mark.parametrize("q_scale", [8.0])
+@pytest.mark.parametrize("name", ["p1"])
+def test_peaked(name, q_scale):
+    from synth.configs import make_config
+    spec = make_config(name, 0, q_scale)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    compare(spec, wl, req_sel=[1])
+
+
+def test_empty_batch():
+    import paper_2501_14808_b200 as hg
+    from synth.configs import BatchSpec
+    spec = BatchSpec("empty", 2, 2, 64, 16, 0, [])
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    assert hg.hg_last_plan_stats(wl.pool)["kernels"] == 0
+
+
+def test_error_leaves_outputs_untouched():
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_config
+    spec = make_config("toy_a", 0)
+    wl = make(spec)
+    wl.out.fill_(7.0)
+    bad = hg.Batch(wl.lay.block_table, [0, 32, 32], [16, 1, 1], None, [0, 1, 2])
+    k_before = wl.k_cache.clone()
+    st = hg.status_of(hg.hg_hybrid_attention, wl.pool, bad, spec.H_q, wl.q, wl.out, None, wl.workspace())
+    assert st == hg.HG_E_INVALID
+    st = hg.status_of(hg.hg_kv_append, wl.pool, hg.Batch(wl.lay.block_table[1:], [3, 32], [1, 1], None, [1, 1]),
+                      wl.k_new[:2], wl.v_new[:2])
+    assert st == hg.HG_E_SHARED_WRITE
+    small = torch.empty(16, dtype=torch.uint8, device="cuda")
+    st = hg.status_of(hg.hg_hybrid_attention, wl.pool, wl.batch, spec.H_q, wl.q, wl.out, None, small)
+    assert st == hg.HG_E_INVALID
+    torch.cuda.synchronize()
+    assert torch.all(wl.out == 7.0) and torch.equal(k_before, wl.k_cache)
+
+
+def test_e2e_host_step_matches_device_path():
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_config
+    spec = make_config("toy_b", 0)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    qh, kh, vh = (x.cpu().pin_memory() for x in (wl.q, wl.k_new, wl.v_new))
+    oh = torch.empty(wl.out.shape, dtype=torch.bfloat16).pin_memory()
+    ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
+                     device="cuda")
+    hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
+    assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16))

@@ -171,33 +171,31 @@ def run_ours(args):
     wl = Workload(spec, device=dev)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-    opts = hg.make_opts(events=ev)
     for _ in range(args.warmup):
-        wl.step(opts)
+        wl.step()
     torch.cuda.synchronize()
+    # one set of kernel events per step, created before the timed region, so steps
+    # are issued back to back: the host plans step k+1 while the GPU runs step k
+    # (the serving-engine overlap); per-step GPU time is read after the loop.
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    kopts = [hg.make_opts(events=e) for e in kev]
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    sk_ms, tc_ms, cb_ms = [], [], []
     host_s = []
+    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
         for k in range(args.steps):
-            flush_l2(flush)                     # L2 flushed outside the timed events
+            flush_l2(flush)                     # L2 flushed between steps, outside the timed events
             starts[k].record(stream)
             h0 = time.perf_counter()
-            wl.step(opts)
+            wl.step(kopts[k])
             host_s.append(time.perf_counter() - h0)
             ends[k].record(stream)
-            torch.cuda.synchronize()            # per-step kernel events must be read before reuse
-            st = hg.hg_last_plan_stats(wl.pool)
-            if st["splitk_items"]:
-                sk_ms.append(ev[2].elapsed_time(ev[3]))
-            if st["tc_tiles"]:
-                tc_ms.append(ev[0].elapsed_time(ev[1]))
-            if st["combine_rows"]:
-                cb_ms.append(ev[4].elapsed_time(ev[5]))
         torch.cuda.synchronize()
+    st = hg.hg_last_plan_stats(wl.pool)
+    sk_ms = [e[2].elapsed_time(e[3]) for e in kev] if st["splitk_items"] else []
+    tc_ms = [e[0].elapsed_time(e[1]) for e in kev] if st["tc_tiles"] else []
+    cb_ms = [e[4].elapsed_time(e[5]) for e in kev] if st["combine_rows"] else []
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
     ms = total_ms / args.steps
@@ -219,7 +217,7 @@ def run_ours(args):
     # whole-step roofline (all kernels): t_roof = max(bytes/BW, flops/TC)
     bt, fl = alg_bytes_total(spec), alg_flops(spec)
     t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
-    e2e = measure_e2e(wl, spec, args, stream)
+    e2e = None if args.profile else measure_e2e(wl, spec, args, stream)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -238,7 +236,7 @@ def run_ours(args):
     }
     if args.extra:
         line["extra"] = extra_configs(args, peaks, dev)
-    line["cpu_baseline"] = cpu_baseline(spec, wl)
+    line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
 
@@ -318,27 +316,25 @@ def extra_configs(args, peaks, dev):
     for name in ("c2", "c3", "p1", "p2"):
         spec = make_config(name, 0)
         wl = Workload(spec, device=dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        opts = hg.make_opts(events=ev)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         for _ in range(3):
-            wl.step(opts)
-        ms, ker = [], {"tc": [], "splitk": [], "combine": []}
-        for _ in range(10):
+            wl.step()
+        n = 10
+        kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n)]
+        kopts = [hg.make_opts(events=e) for e in kev]
+        se = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        torch.cuda.synchronize()
+        for k in range(n):
             flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            wl.step(opts)
-            e.record()
-            torch.cuda.synchronize()
-            ms.append(s.elapsed_time(e))
-            st = hg.hg_last_plan_stats(wl.pool)
-            if st["tc_tiles"]:
-                ker["tc"].append(ev[0].elapsed_time(ev[1]))
-            if st["splitk_items"]:
-                ker["splitk"].append(ev[2].elapsed_time(ev[3]))
-            if st["combine_rows"]:
-                ker["combine"].append(ev[4].elapsed_time(ev[5]))
+            se[k][0].record()
+            wl.step(kopts[k])
+            se[k][1].record()
+        torch.cuda.synchronize()
+        ms = [s.elapsed_time(e) for s, e in se]
+        st = hg.hg_last_plan_stats(wl.pool)
+        ker = {"tc": [e[0].elapsed_time(e[1]) for e in kev] if st["tc_tiles"] else [],
+               "splitk": [e[2].elapsed_time(e[3]) for e in kev] if st["splitk_items"] else [],
+               "combine": [e[4].elapsed_time(e[5]) for e in kev] if st["combine_rows"] else []}
         m = statistics.median(ms)
         bt, fl = alg_bytes_total(spec), alg_flops(spec)
         t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
@@ -442,6 +438,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--extra", action="store_true", help="also time c2, c3, p1, p2 (context)")
+    ap.add_argument("--profile", action="store_true", help="timed steps only (no e2e / cpu baseline): for ncu")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

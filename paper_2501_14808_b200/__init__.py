@@ -236,6 +236,8 @@ def make_opts(split_tokens=0, disable_prefix_pass=False, disable_tc=False, num_s
     o = hg_attn_opts(split_tokens, int(disable_prefix_pass), int(disable_tc), num_sms)
     if events is not None:
         for k, ev in enumerate(events):
+            if ev is not None:
+                ev.record()   # torch creates CUDA events lazily: force creation (and mark recorded)
             o.events[k] = None if ev is None else ev.cuda_event
     return o
 
@@ -336,11 +338,17 @@ def hg_batch_features(batch: Batch, block_size: int = 16) -> hg_features:
     return f
 
 
-def hg_predictor_fit(X: Sequence[hg_features], y_ms, feature_mask: int) -> hg_predictor:
-    arr = (hg_features * len(X))(*X)
+def hg_predictor_fit(X, y_ms, feature_mask: int) -> hg_predictor:
+    """X: sequence of hg_features, or a float64 array [n][8] (the same memory layout, passed zero-copy)."""
+    if isinstance(X, np.ndarray):
+        arr = np.ascontiguousarray(X, np.float64).reshape(-1, 8)
+        ptr, n = _ptr(arr), arr.shape[0]
+    else:
+        arr = (hg_features * len(X))(*X)
+        ptr, n = ctypes.addressof(arr), len(X)
     y = np.ascontiguousarray(y_ms, np.float64)
     m = hg_predictor()
-    _check(lib().hg_predictor_fit(arr, _ptr(y), len(X), feature_mask, ctypes.byref(m)))
+    _check(lib().hg_predictor_fit(ptr, _ptr(y), n, feature_mask, ctypes.byref(m)))
     return m
 
 

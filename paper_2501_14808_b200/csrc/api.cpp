@@ -321,7 +321,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_bt, plan.bt_flat.data(), sizeof(int32_t) * plan.bt_flat.size());
     put(plan.off_sk, plan.sk.data(), sizeof(SkItem) * plan.sk.size());
     put(plan.off_tc, plan.tc.data(), sizeof(TcItem) * plan.tc.size());
-    put(plan.off_rows, plan.tc_rows.data(), sizeof(TcRow) * plan.tc_rows.size());
+    put(plan.off_rows, plan.tc_tok.data(), sizeof(int32_t) * plan.tc_tok.size());
     put(plan.off_cbase, plan.comb_base.data(), sizeof(int32_t) * plan.comb_base.size());
     put(plan.off_comb, plan.comb.data(), sizeof(CombItem) * plan.comb.size());
     s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
@@ -337,7 +337,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.bt_flat = (const int32_t *)(w + plan.off_bt);
     p.sk = (const SkItem *)(w + plan.off_sk);
     p.tc = (const TcItem *)(w + plan.off_tc);
-    p.tc_rows = (const TcRow *)(w + plan.off_rows);
+    p.tc_tok = (const int32_t *)(w + plan.off_rows);
     p.comb_base = (const int32_t *)(w + plan.off_cbase);
     p.comb = (const CombItem *)(w + plan.off_comb);
     p.part_o = (float *)(w + plan.off_part_o);

@@ -37,26 +37,23 @@ struct SkItem {
     int32_t pad;
 };
 
-// tcgen05 tile (tc_attn.cu): 128 stacked rows sharing KV head g and a key
-// range [k0, k1) of ONE block table (the request's, or the group prefix's).
-// Rows are listed in tc_rows[row0 .. row0 + nrows).
+// tcgen05 tile (tc_attn.cu): up to 128 stacked query rows sharing KV head g
+// and a key range [k0, k1) of ONE block table (the request's, or the group
+// prefix's).  Stacked row r has index x = hl0 + r, token slot j = x / G_q and
+// q head g*G_q + x % G_q:
+//   mode 0 (prefill chunk): token t = t0 + j, causal limit pos0 + j + 1
+//   mode 1 (prefix group):  token t = tc_tok[t0 + j] (member decode rows), limit k1
 struct TcItem {
     int32_t bt_off;  // block table (bt_flat offset) the keys are read through
     int32_t g;
     int32_t k0;      // multiple of kTcKeys
     int32_t k1;
-    int32_t row0;
+    int32_t mode;
+    int32_t t0;
     int32_t nrows;   // <= 128
     int32_t part;    // partial index (-1: rows written directly)
-    int32_t pad;
-};
-
-// One stacked query row of a tcgen05 tile.
-struct TcRow {
-    int32_t t;       // batch token
-    int32_t h;       // q head
-    int32_t lim;     // exclusive key limit (causal: c + j + 1; prefix: k1)
-    int32_t pad;
+    int32_t pos0;    // mode 0: absolute position of token t0
+    int32_t hl0;     // q-head-in-group of stacked row 0
 };
 
 // (token, KV head) pair whose rows are merged from several partials.
@@ -78,7 +75,7 @@ struct AttnParams {
     const int32_t *bt_flat;
     const SkItem *sk;
     const TcItem *tc;
-    const TcRow *tc_rows;
+    const int32_t *tc_tok;     // member tokens of prefix-group tiles
     const int32_t *comb_base;  // [T * H_kv]: first partial slot of (t, g) or -1 (direct write)
     const CombItem *comb;
     float *part_o;             // [slots][d] normalised partial outputs
@@ -95,7 +92,9 @@ struct Plan {
     std::vector<int32_t> bt_flat;
     std::vector<SkItem> sk;
     std::vector<TcItem> tc;
-    std::vector<TcRow> tc_rows;
+    std::vector<int32_t> tc_tok;
+    std::vector<SkItem> sk_tmp;
+    std::vector<TcItem> tc_tmp;
     std::vector<int32_t> comb_base;
     std::vector<CombItem> comb;
     int64_t n_slots = 0;

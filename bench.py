@@ -236,6 +236,8 @@ def run_ours(args):
     }
     if args.extra:
         line["extra"] = extra_configs(args, peaks, dev)
+    if not args.profile and not args.no_predictor:
+        line["predictor"] = predictor_sweep(dev, iters=args.sweep_iters)
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -276,7 +278,7 @@ def measure_e2e(wl, spec, args, stream):
             "api": "hg_hybrid_step_host (C ABI, host buffers; synchronises each step)"}
 
 
-def cpu_baseline(spec, wl=None, sample_reqs=None):
+def cpu_baseline(spec, wl=None, sample_reqs=None, min_s=10.0):
     """The fp64 oracle (as it stands) on the host cores, on a bounded sample of the
     workload: the prefill request plus every 8th decode request; tokens/s is
     extrapolated by the sample's share of the attention work (key-rows x heads)."""
@@ -296,14 +298,18 @@ def cpu_baseline(spec, wl=None, sample_reqs=None):
     c = np.array([r.c for r in spec.requests], np.int32)
     n = np.array([r.n for r in spec.requests], np.int32)
     q = q_values(spec)
-    t0 = time.perf_counter()
-    pool.attention(lay.block_table, c, n, q, spec.H_q, req_sel=sample_reqs)
-    dt = time.perf_counter() - t0
+    passes, t0 = 0, time.perf_counter()
+    while True:       # repeat the sample for ~min_s of CPU work (bounded: a few minutes at most)
+        pool.attention(lay.block_table, c, n, q, spec.H_q, req_sel=sample_reqs)
+        passes += 1
+        if time.perf_counter() - t0 >= min_s:
+            break
+    dt = (time.perf_counter() - t0) / passes
     t_full = dt / frac
     return {"value": spec.T / t_full, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{len(sample_reqs)} of {len(spec.requests)} requests ({frac:.1%} of the attention work), "
-                      f"{dt:.2f} s; full-batch time extrapolated by work share",
-            "oracle_s_sample": dt}
+            "sample": f"{len(sample_reqs)} of {len(spec.requests)} requests ({frac:.1%} of the attention work) x "
+                      f"{passes} passes, {dt:.3f} s per pass; full-batch time extrapolated by work share",
+            "oracle_s_per_pass": dt}
 
 
 def extra_configs(args, peaks, dev):
@@ -346,6 +352,88 @@ def extra_configs(args, peaks, dev):
         del wl
         torch.cuda.empty_cache()
     return out
+
+
+def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
+    """C4: time hg_hybrid_attention on the bursty-trace batches, fit the paper's
+    linear-regression predictor on a random 80%, report held-out MAPE.
+
+    Target y = GPU time of the call's kernels (first kernel start -> last
+    kernel end, library-recorded events), median of `reps`, L2 flushed before
+    each rep.  K/V content is random (timing does not depend on values)."""
+    import numpy as np
+    import torch
+    import paper_2501_14808_b200 as hg
+    from synth.layout import make_layout
+    from synth.trace import sweep
+    H = {"llama3-8b": (32, 8, 128), "llama2-7b": (32, 32, 128)}[shape]
+    t0 = time.perf_counter()
+    specs = sweep(seed=seed, iters=iters, H_q=H[0], H_kv=H[1], d=H[2])
+    need = max(sum(-(-(r.c + r.n) // 16) for r in s.requests) for s in specs)
+    N = int(need * 1.25) + 64
+    kc = torch.randn((N, H[1], 16, H[2]), device=dev).to(torch.bfloat16)
+    vc = torch.randn((N, H[1], 16, H[2]), device=dev).to(torch.bfloat16)
+    pool = hg.KVPool(kc, vc, N, 16, H[1], H[2], dev.index)
+    maxT = max(s.T for s in specs)
+    q = torch.randn((maxT, H[0], H[2]), device=dev).to(torch.bfloat16)
+    kn = torch.randn((maxT, H[1], H[2]), device=dev).to(torch.bfloat16)
+    vn = torch.randn((maxT, H[1], H[2]), device=dev).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ws = None
+    X, y, T, pre = [], [], [], []
+    for k, spec in enumerate(specs):
+        lay = make_layout(spec, seed=k, num_blocks=N)
+        b = hg.Batch(lay.block_table, [r.c for r in spec.requests], [r.n for r in spec.requests],
+                     [int(r.offline) for r in spec.requests], lay.shared)
+        need_ws = hg.hg_hybrid_attention_workspace_size(pool, b, H[0])
+        if ws is None or ws.numel() < need_ws:
+            ws = torch.empty(need_ws * 2, dtype=torch.uint8, device=dev)
+        hg.hg_kv_append(pool, b, kn, vn)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(reps)]
+        ops = [hg.make_opts(events=e) for e in evs]
+        for r in range(reps):
+            flush.zero_()
+            hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, ops[r])
+        torch.cuda.synchronize()
+        st = hg.hg_last_plan_stats(pool)
+        first = 0 if st["tc_tiles"] else 2 if st["splitk_items"] else 4
+        last = 5 if st["combine_rows"] else 3 if st["splitk_items"] else 1
+        y.append(statistics.median(e[first].elapsed_time(e[last]) for e in evs))
+        X.append(hg.hg_batch_features(b).as_array())
+        T.append(spec.T)
+        sp = sum(r.n for r in spec.requests if not (r.n == 1 and r.c >= 1))
+        pre.append(sp / spec.T)
+    pool.close()
+    X, y = np.array(X), np.array(y)
+    rng = np.random.default_rng(1)
+    perm = rng.permutation(len(y))
+    ntr = int(0.8 * len(y))
+    tr, te = perm[:ntr], perm[ntr:]
+    res = {"batches": len(y), "shape": shape, "reps": reps, "target": "GPU ms of the call's kernels (median)",
+           "sweep_s": time.perf_counter() - t0}
+    for name, mask in (("attn (S_p, P2, D_ctx, N_d, N_p)", hg.HG_MASK_ATTN), ("paper Eq.2 (S_p, S_p^2, N_p, N_d)", hg.HG_MASK_EQ2),
+                       ("paper Eq.1 (S_p, S_p^2, S_d^2, N_p, N_d)", hg.HG_MASK_EQ1)):
+        t1 = time.perf_counter()
+        m = hg.hg_predictor_fit(X[tr], y[tr], mask)
+        fit_ms = (time.perf_counter() - t1) * 1e3
+        yh = np.array([hg.hg_predictor_predict(m, hg.features_from_array(x)) for x in X[te]])
+        t2 = time.perf_counter()
+        for x in X[te]:
+            hg.hg_predictor_predict(m, hg.features_from_array(x))
+        pred_us = (time.perf_counter() - t2) / len(te) * 1e6
+        res[name] = {"mape_heldout": float(np.mean(np.abs(yh - y[te]) / y[te])), "train_mape": m.train_mape,
+                     "fit_ms": fit_ms, "predict_us_python": pred_us, "w": list(m.w)}
+    # tokens/s versus mix (share of prefill tokens in the batch)
+    pre = np.array(pre)
+    mix = {}
+    for lo, hi in ((0, 0.05), (0.05, 0.5), (0.5, 0.9), (0.9, 1.01)):
+        sel = (pre >= lo) & (pre < hi)
+        if sel.any():
+            mix[f"prefill_share[{lo},{hi})"] = {"batches": int(sel.sum()),
+                                                 "tokens_per_s": float(np.sum(np.array(T)[sel]) / (np.sum(y[sel]) / 1e3))}
+    res["tokens_per_s_vs_mix"] = mix
+    return res
 
 
 def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
@@ -414,7 +502,7 @@ def run_reference(args):
         # each step: a bounded sample (the prefill request + 4 decodes, rotating)
         dec = [i for i, r in enumerate(spec.requests) if r.n == 1]
         sel = sorted([0] + dec[(4 * k) % len(dec):(4 * k) % len(dec) + 4])
-        cb = cpu_baseline(spec, None, sample_reqs=sel)
+        cb = cpu_baseline(spec, None, sample_reqs=sel, min_s=0.0)
         if k >= args.warmup:
             times.append(spec.T / cb["value"])
             base = cb
@@ -439,6 +527,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--extra", action="store_true", help="also time c2, c3, p1, p2 (context)")
     ap.add_argument("--profile", action="store_true", help="timed steps only (no e2e / cpu baseline): for ncu")
+    ap.add_argument("--no-predictor", action="store_true", help="skip the C4 sweep + predictor fit")
+    ap.add_argument("--sweep-iters", type=int, default=64, help="C4 iterations per (rho, chunk) point")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -30,7 +30,8 @@ struct hg_kv_pool {
         cudaEvent_t ev = nullptr;
         bool pending = false;
     };
-    Stage ring[4];
+    static constexpr int kRing = 8;  // descriptor copies in flight: the host may plan ~4 calls ahead
+    Stage ring[kRing];
     int ring_pos = 0;
     alignas(64) unsigned char tmap_k[128];
     alignas(64) unsigned char tmap_v[128];
@@ -65,7 +66,7 @@ static hg_status sticky_check() {
 static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return HG_OK;
     auto &s = pool->ring[pool->ring_pos];
-    pool->ring_pos = (pool->ring_pos + 1) % 4;
+    pool->ring_pos = (pool->ring_pos + 1) % hg_kv_pool::kRing;
     if (s.pending) {
         hg_status r = cuda_check(cudaEventSynchronize(s.ev), "staging event sync");
         if (r) return r;

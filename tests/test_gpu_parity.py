@@ -227,3 +227,23 @@ def test_e2e_host_step_matches_device_path():
                      device="cuda")
     hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
     assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16))
+
+
+def test_tp_path_world1_matches_single_gpu():
+    """hg_hybrid_attention_tp on a 1-rank NCCL communicator (the only GPU count
+    gpurun offers): the sharded path's workspace layout + transpose kernel."""
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_config
+    spec = make_config("toy_b", 0)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    uid = hg.hg_comm_unique_id()
+    comm = hg.Comm(uid, 0, 1, torch.cuda.current_device())
+    out = torch.empty_like(wl.out)
+    ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q),
+                     dtype=torch.uint8, device="cuda")
+    hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, out, ws)
+    torch.cuda.synchronize()
+    comm.close()
+    assert torch.equal(out.view(torch.int16), wl.out.view(torch.int16))

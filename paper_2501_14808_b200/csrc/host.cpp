@@ -177,6 +177,36 @@ static void lpt_sort(std::vector<Item> &v, std::vector<Item> &tmp) {
     v.swap(tmp);
 }
 
+// tcgen05 tiles: keep the tiles that read the same KV stream (same block table
+// and KV head) adjacent, so the CTAs of one wave share K/V through L2, longest
+// stream first and longest tile first within a stream (LPT at stream grain).
+static void stream_sort(std::vector<TcItem> &v, std::vector<TcItem> &tmp) {
+    const size_t n = v.size();
+    if (n < 2) return;
+    struct Seg { size_t b, e; int32_t len; };
+    std::vector<Seg> segs;
+    for (size_t a = 0; a < n;) {
+        size_t b = a;
+        int32_t mx = 0;
+        while (b < n && v[b].bt_off == v[a].bt_off && v[b].g == v[a].g) {
+            mx = std::max(mx, v[b].k1 - v[b].k0);
+            ++b;
+        }
+        segs.push_back({a, b, mx});
+        a = b;
+    }
+    std::stable_sort(segs.begin(), segs.end(), [](const Seg &x, const Seg &y) { return x.len > y.len; });
+    tmp.clear();
+    tmp.reserve(n);
+    for (const Seg &s : segs) {
+        const size_t first = tmp.size();
+        tmp.insert(tmp.end(), v.begin() + s.b, v.begin() + s.e);
+        std::stable_sort(tmp.begin() + first, tmp.end(),
+                         [](const TcItem &x, const TcItem &y) { return (x.k1 - x.k0) > (y.k1 - y.k0); });
+    }
+    v.swap(tmp);
+}
+
 hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpts &o, Plan *p) {
     const int G = H_q / H_kv;
     const int B = kBlock;
@@ -326,7 +356,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     }
     p->kv_bytes_read = kv_tok_read * 4ll * d;
     lpt_sort(p->sk, p->sk_tmp);
-    lpt_sort(p->tc, p->tc_tmp);
+    stream_sort(p->tc, p->tc_tmp);
 
     // ---- workspace layout ----------------------------------------------------
     size_t off = 0;

@@ -243,6 +243,17 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     auto in_prefix_pass = [&](int i) {
         return o.prefix_pass && tc_ok && group[i] >= 0 && v.n[i] == 1 && gcount[group[i]] >= 2;
     };
+    // rows per tcgen05 CTA: 256 (two Q tiles sharing K/V, half the L2 traffic per
+    // FLOP) when that still gives every SM a CTA, else 128 (more CTAs)
+    int ipr = kTcRows;
+    if (tc_ok) {
+        int64_t n256 = 0;
+        for (int i = 0; i < v.R; ++i)
+            if (v.n[i] > 1) n256 += (int64_t)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows);
+        for (int gi = 0; gi < ng; ++gi)
+            if (gcount[gi] >= 2 && o.prefix_pass) n256 += (int64_t)H_kv * ceil_div((int64_t)gcount[gi] * G, 2 * kTcRows);
+        if (n256 >= o.num_sms) ipr = 2 * kTcRows;
+    }
     // algorithmic unique KV tokens U: shared prefix counted once per group
     {
         int64_t U = 0;
@@ -264,8 +275,8 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             if (v.n[i] <= 1) continue;
             const int rows = v.n[i] * G;
             for (int g = 0; g < H_kv; ++g) {
-                for (int r0 = 0; r0 < rows; r0 += kTcRows) {
-                    const int nr = std::min(kTcRows, rows - r0);
+                for (int r0 = 0; r0 < rows; r0 += ipr) {
+                    const int nr = std::min(ipr, rows - r0);
                     const int j0 = r0 / G, j_last = (r0 + nr - 1) / G;
                     TcItem it{p->reqs[i].bt_off, g, 0, v.c[i] + j_last + 1, 0, p->reqs[i].cu_q + j0, nr, -1,
                               v.c[i] + j0, r0 - j0 * G};
@@ -343,8 +354,8 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             const int P = v.s[rep[gi]] * B;
             const int rows = nm * G;
             for (int g = 0; g < H_kv; ++g) {
-                for (int r0 = 0; r0 < rows; r0 += kTcRows) {
-                    const int nr = std::min(kTcRows, rows - r0);
+                for (int r0 = 0; r0 < rows; r0 += ipr) {
+                    const int nr = std::min(ipr, rows - r0);
                     const int m0 = r0 / G;
                     TcItem it{p->reqs[rep[gi]].bt_off, g, 0, P, 1, base_off + first[gi] + m0, nr, 0, 0, r0 - m0 * G};
                     kv_tok_read += P;

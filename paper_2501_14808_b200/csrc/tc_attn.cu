@@ -1,22 +1,24 @@
 // tc_attn.cu -- tcgen05 / TMEM / TMA flash-attention tiles for sm_100a.
 //
-// One CTA computes one TcItem: 128 stacked query rows (token x q-head of one
-// GQA group, or the decode rows of every member of a shared-prefix group, the
-// Hydragen-style stacking of SURVEY §8(a) a.4) against the keys [k0, k1) of one
-// block table, in KV tiles of 128 keys:
+// One CTA computes one TcItem: up to 256 stacked query rows (token x q-head of
+// one GQA group, or the decode rows of every member of a shared-prefix group:
+// the Hydragen-style stacking of SURVEY §8(a) a.4), as two 128-row Q tiles,
+// against the keys [k0, k1) of one block table, in KV tiles of 128 keys:
 //
 //   S   = Q K^T        tcgen05.mma kind::f16, M=128 N=128 K=16 x (D/16), A/B from
 //                      smem (K-major, 128B swizzle), fp32 accumulator in TMEM
 //   P   = exp2(S*c - m) softmax warps: tcgen05.ld S row -> registers, online
-//                      max with lazy (threshold 2^8) rescaling, P -> smem bf16
-//   O  += P V          tcgen05.mma M=128 N=D K=16 x 8, A=P (K-major), B=V
-//                      (MN-major, 128B swizzle), fp32 accumulator in TMEM
+//                      max with lazy (threshold 2^8) rescaling, exp2 on MUFU with
+//                      1/4 on the FMA pipe (polynomial), P -> TMEM (bf16 pairs)
+//   O  += P V          tcgen05.mma M=128 N=D K=16 x 8, A=P from TMEM, B=V from
+//                      smem (MN-major, 128B swizzle), fp32 accumulator in TMEM
 //
 // K/V tiles are staged by TMA from the paged pool: each 16-token block of one
 // KV head is a [16][64] box per 64-column half (2 KB), eight blocks per tile,
-// double buffered.  Warp roles (192 threads): warps 0-3 softmax / epilogue
-// (thread i <-> TMEM lane i <-> tile row i), warp 4 TMA producer, warp 5 MMA
-// issuer + TMEM allocator.  Synchronisation is mbarrier-only.
+// double buffered, shared by both Q tiles.  Warp roles (320 threads): warps
+// 0-3 / 4-7 softmax + epilogue of Q tile 0 / 1 (thread <-> TMEM lane <-> row),
+// warp 8 TMA producer, warp 9 MMA issuer + TMEM allocator (all 512 columns).
+// Synchronisation is mbarrier-only.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -172,26 +174,59 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // warps 0-3 / 4-7 softmax of Q tile 0 / 1, warp 8 TMA, warp 9 MMA
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values stay <= 2^8 between rescales
 
+// 2^x on the FMA/ALU pipes (offloads the MUFU unit): x = n + f, n = rint(x)
+// by the 1.5*2^23 magic add, f in [-0.5, 0.5], 2^f by a degree-3 polynomial
+// (max rel. error 1.4e-4, far below bf16's 3.9e-3 rounding of P).
+__device__ __forceinline__ float exp2_poly(float x) {
+    x = fmaxf(x, -126.0f);
+    const float t = x + 12582912.0f;
+    const float f = x - (t - 12582912.0f);
+    const int n = __float_as_int(t) - 0x4B400000;
+    float q = fmaf(0.05502927f, f, 0.24225698f);
+    q = fmaf(q, f, 0.69325305f);
+    q = fmaf(q, f, 0.99995134f);
+    return __int_as_float(__float_as_int(q) + (n << 23));
+}
+
+// Two 128-row Q tiles per CTA (FA4-style ping-pong) share every K/V tile, so a
+// KV byte staged from L2 feeds 256 query rows; P never leaves TMEM: softmax
+// overwrites S's first 64 columns with packed bf16 P and PV is a TS-MMA (A from
+// TMEM).  tcgen05 ops issued by one thread complete in order and a commit
+// covers all prior ops, so "S(j+1) full" also means "PV(j) done": the S-free
+// and O-stable handshakes of a one-tile design disappear.
 template <int D>
 struct TcSmem {
     static constexpr int NH = D / 64;                  // 64-column (128 B) halves of a row
     static constexpr int kHalf = kTcRows * 128;        // one [128][64] bf16 half tile = 16 KB
-    static constexpr int kQ = NH * kHalf;
+    static constexpr int kQ = NH * kHalf;              // one 128-row Q tile
     static constexpr int kKV = NH * kHalf;             // one K (or V) tile of 128 keys
-    static constexpr int kP = 2 * kHalf;               // P: 128 rows x 128 keys
-    static constexpr int oQ = 0;
-    static constexpr int oK = oQ + kQ;                 // 2 stages
+    static constexpr int oQ = 0;                       // 2 Q tiles
+    static constexpr int oK = oQ + 2 * kQ;             // 2 stages
     static constexpr int oV = oK + 2 * kKV;            // 2 stages
-    static constexpr int oP = oV + 2 * kKV;
-    static constexpr int oBar = oP + kP;
+    static constexpr int oBar = oV + 2 * kKV;
     static constexpr int kBytes = oBar + 256 + 1024;   // barriers + alignment slack
 };
 
-enum { BAR_KFULL = 0, BAR_VFULL = 2, BAR_KVEMPTY = 4, BAR_SFULL = 6, BAR_SFREE = 7, BAR_PFULL = 8, BAR_ODONE = 9,
-       BAR_QREADY = 10, BAR_N = 11 };
+enum { BAR_KFULL = 0, BAR_VFULL = 2, BAR_KVEMPTY = 4, BAR_SFULL = 6, BAR_PFULL = 8, BAR_ODONE = 10, BAR_QREADY = 11,
+       BAR_N = 12 };
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
 
 template <int D>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -202,7 +237,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = su32(smem);
-    const uint32_t sQ = sbase + L::oQ, sK = sbase + L::oK, sV = sbase + L::oV, sP = sbase + L::oP;
+    const uint32_t sQ = sbase + L::oQ, sK = sbase + L::oK, sV = sbase + L::oV;
     const uint32_t bars = sbase + L::oBar;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::oBar + BAR_N * 8);
     auto bar = [&](int i) { return bars + 8u * i; };
@@ -210,32 +245,30 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const TcItem it = p.tc[blockIdx.x];
     const int nkt = (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys;
+    const int ntiles = it.nrows > kTcRows ? 2 : 1;
 
     if (threadIdx.x == 0) {
-        mbar_init(bar(BAR_KFULL), 1);
-        mbar_init(bar(BAR_KFULL + 1), 1);
-        mbar_init(bar(BAR_VFULL), 1);
-        mbar_init(bar(BAR_VFULL + 1), 1);
-        mbar_init(bar(BAR_KVEMPTY), 1);
-        mbar_init(bar(BAR_KVEMPTY + 1), 1);
-        mbar_init(bar(BAR_SFULL), 1);
-        mbar_init(bar(BAR_SFREE), 128);
-        mbar_init(bar(BAR_PFULL), 128);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar(BAR_KFULL + i), 1);
+            mbar_init(bar(BAR_VFULL + i), 1);
+            mbar_init(bar(BAR_KVEMPTY + i), 1);
+            mbar_init(bar(BAR_SFULL + i), 1);
+            mbar_init(bar(BAR_PFULL + i), 128);
+        }
         mbar_init(bar(BAR_ODONE), 1);
-        mbar_init(bar(BAR_QREADY), 128);
+        mbar_init(bar(BAR_QREADY), 256);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (warp == 5) {  // TMEM: S [0,128) + O [128, 128+D) fp32 columns
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(su32(tmem_slot)));
+    if (warp == 9) {  // TMEM: tile t: S/P at [256 t, 256 t + 128), O at [256 t + 128, 256 t + 128 + D)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + 128;
 
-    if (warp == 4) {
+    if (warp == 8) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             const int32_t *bt = p.bt_flat + it.bt_off;
@@ -245,72 +278,77 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 const int s = j & 1;
                 if (j >= 2) mbar_wait(bar(BAR_KVEMPTY + s), ((j - 2) >> 1) & 1);
                 const uint32_t dk = sK + s * L::kKV, dv = sV + s * L::kKV;
-                mbar_expect_tx(bar(BAR_KFULL + s), L::kKV);
-#pragma unroll 1
+                int rows[8];
+#pragma unroll
                 for (int b = 0; b < 8; ++b) {
                     int kb = kb0 + j * 8 + b;
                     kb = kb <= kb_last ? kb : kb0;  // rows past k1 are masked; keep the data finite
-                    const int row = (bt[kb] * p.H_kv + it.g) * kBlock;
+                    rows[b] = (bt[kb] * p.H_kv + it.g) * kBlock;
+                }
+                mbar_expect_tx(bar(BAR_KFULL + s), L::kKV);
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
 #pragma unroll
                     for (int h = 0; h < NH; ++h)
-                        tma_load_2d(dk + h * L::kHalf + b * (kBlock * 128), &tmap_k, h * 64, row, bar(BAR_KFULL + s));
-                }
+                        tma_load_2d(dk + h * L::kHalf + b * (kBlock * 128), &tmap_k, h * 64, rows[b], bar(BAR_KFULL + s));
                 mbar_expect_tx(bar(BAR_VFULL + s), L::kKV);
-#pragma unroll 1
-                for (int b = 0; b < 8; ++b) {
-                    int kb = kb0 + j * 8 + b;
-                    kb = kb <= kb_last ? kb : kb0;
-                    const int row = (bt[kb] * p.H_kv + it.g) * kBlock;
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
 #pragma unroll
                     for (int h = 0; h < NH; ++h)
-                        tma_load_2d(dv + h * L::kHalf + b * (kBlock * 128), &tmap_v, h * 64, row, bar(BAR_VFULL + s));
-                }
+                        tma_load_2d(dv + h * L::kHalf + b * (kBlock * 128), &tmap_v, h * 64, rows[b], bar(BAR_VFULL + s));
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ===================== MMA issuer =====================
         if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A, B K-major
-            constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);    // O += P V: A K-major, B (V) MN-major
+            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A, B K-major (smem)
+            constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);    // O += P V: A (P) in TMEM, B (V) MN-major
             mbar_wait(bar(BAR_QREADY), 0);
-            auto issue_qk = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(bar(BAR_KFULL + s), (j >> 1) & 1);
-                if (j > 0) mbar_wait(bar(BAR_SFREE), (j - 1) & 1);
-                tc_fence_after();
+            auto issue_qk = [&](int t, int j) {
+                const uint32_t tS = tmem + 256 * t, q = sQ + t * L::kQ, k = sK + (j & 1) * L::kKV;
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = (ks / 4) * L::kHalf + (ks % 4) * 32;
-                    umma_bf16(tS, smem_desc(sQ + off, 16, 1024), smem_desc(sK + s * L::kKV + off, 16, 1024), idS,
-                              ks > 0);
+                    umma_bf16(tS, smem_desc(q + off, 16, 1024), smem_desc(k + off, 16, 1024), idS, ks > 0);
                 }
-                umma_commit(bar(BAR_SFULL));
+                umma_commit(bar(BAR_SFULL + t));
             };
-            issue_qk(0);
+            mbar_wait(bar(BAR_KFULL), 0);
+            tc_fence_after();
+            for (int t = 0; t < ntiles; ++t) issue_qk(t, 0);
             for (int j = 0; j < nkt; ++j) {
-                if (j + 1 < nkt) issue_qk(j + 1);
                 const int s = j & 1;
-                mbar_wait(bar(BAR_PFULL), j & 1);
-                mbar_wait(bar(BAR_VFULL + s), (j >> 1) & 1);
-                tc_fence_after();
+                for (int t = 0; t < ntiles; ++t) {
+                    mbar_wait(bar(BAR_PFULL + t), j & 1);
+                    if (t == 0) mbar_wait(bar(BAR_VFULL + s), (j >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t tS = tmem + 256 * t, tO = tS + 128;
 #pragma unroll
-                for (int ks = 0; ks < kTcKeys / 16; ++ks) {
-                    const uint32_t aoff = (ks / 4) * L::kHalf + (ks % 4) * 32;   // P: K-major, keys along K
-                    const uint32_t boff = ks * 2048;                             // V: 16 keys = 2 x 8-row groups
-                    umma_bf16(tO, smem_desc(sP + aoff, 16, 1024), smem_desc(sV + s * L::kKV + boff, L::kHalf, 1024),
-                              idO, (j > 0 || ks > 0));
+                    for (int ks = 0; ks < kTcKeys / 16; ++ks)   // P: 16 keys = 8 packed columns per k-step
+                        umma_bf16_ts(tO, tS + ks * 8, smem_desc(sV + s * L::kKV + ks * 2048, L::kHalf, 1024), idO,
+                                     (j > 0 || ks > 0));
+                    if (j + 1 < nkt) {
+                        if (t == 0) {
+                            mbar_wait(bar(BAR_KFULL + (s ^ 1)), ((j + 1) >> 1) & 1);
+                            tc_fence_after();
+                        }
+                        issue_qk(t, j + 1);   // in-order after PV(t, j): overwrites S/P of tile t safely
+                    }
                 }
                 umma_commit(bar(BAR_KVEMPTY + s));
-                umma_commit(bar(BAR_ODONE));
             }
+            umma_commit(bar(BAR_ODONE));
         }
     } else {
-        // ===================== softmax / correction / epilogue (warps 0-3) =====================
-        const int r = threadIdx.x;  // tile row == TMEM lane
-        const bool valid = r < it.nrows;
+        // ===================== softmax / correction / epilogue (warps 0-7) =====================
+        const int t = warp >> 2;             // Q tile of this warpgroup
+        const int r = threadIdx.x & 127;     // row in the tile == TMEM lane
+        const int rr = t * kTcRows + r;      // stacked row of the item
+        const bool valid = rr < it.nrows;
         struct { int t, h, lim; } row{0, 0, 0};
         if (valid) {
-            const int x = it.hl0 + r, j = x / p.G_q;
+            const int x = it.hl0 + rr, j = x / p.G_q;
             row.h = it.g * p.G_q + (x - j * p.G_q);
             if (it.mode == 0) {
                 row.t = it.t0 + j;
@@ -321,126 +359,128 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             }
         }
         // Q row -> smem, K-major 128B swizzle: half h, row r at h*16K + r*128, chunk c at (c ^ (r&7))*16
-        {
+        if (t < ntiles) {
             const uint4 *src = reinterpret_cast<const uint4 *>(p.q + ((int64_t)row.t * p.H_q + row.h) * D);
+            const uint32_t qb = sQ + t * L::kQ + r * 128;
 #pragma unroll
             for (int c = 0; c < D / 8; ++c) {
-                uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
-                const int h = c >> 3, cc = c & 7;
-                *reinterpret_cast<uint4 *>(smem + L::oQ + h * L::kHalf + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
+                const uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
+                sts128(qb + (c >> 3) * L::kHalf + (((c & 7) ^ (r & 7)) << 4), v);
             }
             fence_async_smem();
-            mbar_arrive(bar(BAR_QREADY));
         }
-        const int lim = valid ? row.lim : 0;
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-        float m_used = -CUDART_INF_F;  // reference max (log2 domain) of the exponentials
-        float l_sum = 0.f;
-        for (int j = 0; j < nkt; ++j) {
-            mbar_wait(bar(BAR_SFULL), j & 1);
-            tc_fence_after();
-            uint32_t sr[128];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) TMEM_LD32(tS + lane_base + c * 32, (&sr[c * 32]));
-            tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(bar(BAR_SFREE));
-            const int kbase = it.k0 + j * kTcKeys;
-            float mt = -CUDART_INF_F;
-#pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                float x = (kbase + c < lim) ? __uint_as_float(sr[c]) * p.scale_log2 : -CUDART_INF_F;
-                sr[c] = __float_as_uint(x);
-                mt = fmaxf(mt, x);
-            }
-            // lazy rescaling: move the reference only when the row max grew by > 2^8
-            const bool bump = mt > m_used + kRescaleThreshold;
-            float alpha = 1.f;
-            if (bump) {
-                alpha = (m_used == -CUDART_INF_F) ? 0.f : ex2(m_used - mt);
-                m_used = mt;
-            }
-            const float ref = (m_used == -CUDART_INF_F) ? 0.f : m_used;
-            float ls = 0.f;
-            uint32_t pk[64];
-#pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                const float a = ex2(__uint_as_float(sr[2 * c]) - ref);
-                const float b = ex2(__uint_as_float(sr[2 * c + 1]) - ref);
-                ls += a + b;
-                pk[c] = pack2(a, b);
-            }
-            l_sum = l_sum * alpha + ls;
-            if (j > 0) {
-                mbar_wait(bar(BAR_ODONE), (j - 1) & 1);  // PV_{j-1} done: P smem free, O stable
+        mbar_arrive(bar(BAR_QREADY));
+        if (t < ntiles) {
+            const int lim = valid ? row.lim : 0;
+            const float sc = p.scale_log2;
+            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+            const uint32_t tS = tmem + 256 * t + lane_base, tO = tS + 128;
+            float m_used = -CUDART_INF_F;  // reference max (log2 domain) of the exponentials
+            float l_sum = 0.f;
+            for (int j = 0; j < nkt; ++j) {
+                mbar_wait(bar(BAR_SFULL + t), j & 1);   // QK(t, j) and everything before it (PV(t, j-1)) done
                 tc_fence_after();
-            }
-            // P row -> smem (K-major 128B swizzle; keys 0-63 in half 0, 64-127 in half 1)
+                uint32_t sr[128];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const int h = c >> 3, cc = c & 7;
-                *reinterpret_cast<uint4 *>(smem + L::oP + h * L::kHalf + r * 128 + ((cc ^ (r & 7)) << 4)) =
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            }
-            fence_async_smem();
-            if (j > 0 && __any_sync(0xffffffffu, bump)) {
-                uint32_t orr[32];
-#pragma unroll 1
-                for (int c = 0; c < D / 32; ++c) {
-                    TMEM_LD32(tO + lane_base + c * 32, orr);
-                    tmem_wait_ld();
+                for (int c = 0; c < 4; ++c) TMEM_LD32(tS + c * 32, (&sr[c * 32]));
+                tmem_wait_ld();
+                const int kbase = it.k0 + j * kTcKeys;
+                if (kbase + kTcKeys > lim) {  // diagonal / tail tile: mask keys >= lim
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
-                    TMEM_ST32(tO + lane_base + c * 32, orr);
+                    for (int c = 0; c < 128; ++c)
+                        if (kbase + c >= lim) sr[c] = __float_as_uint(-CUDART_INF_F);
                 }
-                tmem_wait_st();
-            }
-            tc_fence_before();
-            mbar_arrive(bar(BAR_PFULL));
-        }
-        // ---- epilogue ----
-        mbar_wait(bar(BAR_ODONE), (nkt - 1) & 1);
-        tc_fence_after();
-        const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-        const float lse2 = l_sum > 0.f ? m_used + __log2f(l_sum) : -CUDART_INF_F;
-        const int G = p.G_q;
-        const int base = (valid && it.part >= 0) ? p.comb_base[(int64_t)row.t * p.H_kv + it.g] : -1;
+                float mx[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mx[e] = __uint_as_float(sr[e]);
+#pragma unroll
+                for (int c = 8; c < 128; ++c) mx[c & 7] = fmaxf(mx[c & 7], __uint_as_float(sr[c]));
+                const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                const float mt = mraw * sc;   // scale > 0: max commutes with scaling
+                // lazy rescaling: move the reference only when the row max grew by > 2^8
+                const bool bump = mt > m_used + kRescaleThreshold;
+                float alpha = 1.f;
+                if (bump) {
+                    alpha = (m_used == -CUDART_INF_F) ? 0.f : ex2(m_used - mt);
+                    m_used = mt;
+                }
+                if (j > 0 && __any_sync(0xffffffffu, bump)) {  // O(t) is stable: PV(t, j-1) completed
+                    uint32_t orr[32];
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-            uint32_t orr[32];
-            TMEM_LD32(tO + lane_base + c * 32, orr);
-            tmem_wait_ld();
-            if (!valid) continue;
-            if (it.part < 0) {
-                uint4 *dst = reinterpret_cast<uint4 *>(p.out + ((int64_t)row.t * p.H_q + row.h) * D + c * 32);
+                    for (int c = 0; c < D / 32; ++c) {
+                        TMEM_LD32(tO + c * 32, orr);
+                        tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    dst[e] = make_uint4(pack2(__uint_as_float(orr[8 * e + 0]) * inv, __uint_as_float(orr[8 * e + 1]) * inv),
-                                        pack2(__uint_as_float(orr[8 * e + 2]) * inv, __uint_as_float(orr[8 * e + 3]) * inv),
-                                        pack2(__uint_as_float(orr[8 * e + 4]) * inv, __uint_as_float(orr[8 * e + 5]) * inv),
-                                        pack2(__uint_as_float(orr[8 * e + 6]) * inv, __uint_as_float(orr[8 * e + 7]) * inv));
-            } else {
-                const int64_t slot = base + (int64_t)it.part * G + (row.h % G);
-                float4 *dst = reinterpret_cast<float4 *>(p.part_o + slot * D + c * 32);
+                        for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+                        TMEM_ST32(tO + c * 32, orr);
+                    }
+                }
+                const float nref = (m_used == -CUDART_INF_F) ? 0.f : -m_used;
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+                uint32_t pk[64];
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    dst[e] = make_float4(__uint_as_float(orr[4 * e]) * inv, __uint_as_float(orr[4 * e + 1]) * inv,
-                                         __uint_as_float(orr[4 * e + 2]) * inv, __uint_as_float(orr[4 * e + 3]) * inv);
+                for (int c = 0; c < 64; ++c) {
+                    const float x0 = fmaf(__uint_as_float(sr[2 * c]), sc, nref);
+                    const float x1 = fmaf(__uint_as_float(sr[2 * c + 1]), sc, nref);
+                    // one pair in four on the FMA pipe, three on MUFU (offload, FA4-style)
+                    const float a = ((c & 3) == 3) ? exp2_poly(x0) : ex2(x0);
+                    const float b = ((c & 3) == 3) ? exp2_poly(x1) : ex2(x1);
+                    ls[c & 3] += a + b;
+                    pk[c] = pack2(a, b);
+                }
+                l_sum = l_sum * alpha + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
+                // P (bf16 pairs) over S's first 64 columns of this lane
+                TMEM_ST32(tS, pk);
+                TMEM_ST32(tS + 32, (&pk[32]));
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(bar(BAR_PFULL + t));
             }
-        }
-        if (valid) {
-            if (it.part < 0) {
-                if (p.lse) p.lse[(int64_t)row.t * p.H_q + row.h] = lse2 * 0.69314718055994531f;
-            } else {
-                p.part_lse[base + (int64_t)it.part * G + (row.h % G)] = lse2;
+            // ---- epilogue ----
+            mbar_wait(bar(BAR_ODONE), 0);
+            tc_fence_after();
+            const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+            const float lse2 = l_sum > 0.f ? m_used + __log2f(l_sum) : -CUDART_INF_F;
+            const int G = p.G_q;
+            const int base = (valid && it.part >= 0) ? p.comb_base[(int64_t)row.t * p.H_kv + it.g] : -1;
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t orr[32];
+                TMEM_LD32(tO + c * 32, orr);
+                tmem_wait_ld();
+                if (!valid) continue;
+                if (it.part < 0) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(p.out + ((int64_t)row.t * p.H_q + row.h) * D + c * 32);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        dst[e] = make_uint4(pack2(__uint_as_float(orr[8 * e + 0]) * inv, __uint_as_float(orr[8 * e + 1]) * inv),
+                                            pack2(__uint_as_float(orr[8 * e + 2]) * inv, __uint_as_float(orr[8 * e + 3]) * inv),
+                                            pack2(__uint_as_float(orr[8 * e + 4]) * inv, __uint_as_float(orr[8 * e + 5]) * inv),
+                                            pack2(__uint_as_float(orr[8 * e + 6]) * inv, __uint_as_float(orr[8 * e + 7]) * inv));
+                } else {
+                    const int64_t slot = base + (int64_t)it.part * G + (row.h % G);
+                    float4 *dst = reinterpret_cast<float4 *>(p.part_o + slot * D + c * 32);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        dst[e] = make_float4(__uint_as_float(orr[4 * e]) * inv, __uint_as_float(orr[4 * e + 1]) * inv,
+                                             __uint_as_float(orr[4 * e + 2]) * inv, __uint_as_float(orr[4 * e + 3]) * inv);
+                }
+            }
+            if (valid) {
+                if (it.part < 0) {
+                    if (p.lse) p.lse[(int64_t)row.t * p.H_q + row.h] = lse2 * 0.69314718055994531f;
+                } else {
+                    p.part_lse[base + (int64_t)it.part * G + (row.h % G)] = lse2;
+                }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
     }
 }
 

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 120 python -m pytest tests/test_gpu_parity.py -q -x -k "toy" > gpurun_out/t0.log 2>&1
+echo t0=$? >> gpurun_out/status.txt
+timeout 200 python tools/trace_tc.py p2 > gpurun_out/trace.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "fuzz or full_size or peaked or variants or shared or tp" > gpurun_out/t.log 2>&1
+echo t=$? >> gpurun_out/status.txt
+for c in p2 p1 c1 c3; do timeout 120 python tools/run_config.py $c --time --steps 3 >> gpurun_out/time.log 2>&1; done

@@ -120,6 +120,8 @@ typedef struct {
     void *events[6];            /* profiling: cudaEvent_t (or NULL) recorded on the stream right before /
                                    after the tcgen05 kernel [0,1], the split-K kernel [2,3] and the
                                    combine kernel [4,5] (bench.py's per-kernel roofline timing) */
+    void *debug_trace;          /* NULL, or device int64[4096]: clock64 stamps of tcgen05 CTA 0's pipeline
+                                   events (kernel development aid; see tc_attn.cu) */
 } hg_attn_opts;
 
 /* Bytes of device workspace hg_hybrid_attention needs for this batch. */

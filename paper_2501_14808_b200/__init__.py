@@ -49,7 +49,7 @@ class hg_batch(ctypes.Structure):
 
 class hg_attn_opts(ctypes.Structure):
     _fields_ = [("split_tokens", i32), ("disable_prefix_pass", i32), ("disable_tc", i32), ("num_sms", i32),
-                ("events", P * 6)]
+                ("events", P * 6), ("debug_trace", P)]
 
 
 class hg_plan_stats(ctypes.Structure):

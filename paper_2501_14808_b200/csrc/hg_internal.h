@@ -83,6 +83,7 @@ struct AttnParams {
     int32_t H_q, H_kv, G_q, d;
     int32_t n_sk, n_tc, n_comb;
     float scale_log2;          // log2(e) / sqrt(d)
+    long long *trace;          // debug: per-event clock64 stamps of tcgen05 CTA 0 (NULL: off)
 };
 
 // Host-side plan (a.1 + a.4): built per call, staged to the device.

@@ -15,9 +15,10 @@
 //
 // K/V tiles are staged by TMA from the paged pool: each 16-token block of one
 // KV head is a [16][64] box per 64-column half (2 KB), eight blocks per tile,
-// double buffered, shared by both Q tiles.  Warp roles (320 threads): warps
-// 0-3 / 4-7 softmax + epilogue of Q tile 0 / 1 (thread <-> TMEM lane <-> row),
-// warp 8 TMA producer, warp 9 MMA issuer + TMEM allocator (all 512 columns).
+// double buffered, shared by both Q tiles.  Warp roles (384 threads): warps
+// 0-3 / 4-7 softmax + epilogue of Q tile 0 / 1 (thread <-> TMEM lane <-> row,
+// 224 registers via setmaxnreg), warp 8 TMA producer, warp 9 MMA issuer + TMEM
+// allocator (all 512 columns), warps 10-11 idle (56 registers).
 // Synchronisation is mbarrier-only.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -174,7 +175,7 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-constexpr int kTcThreads = 320;  // warps 0-3 / 4-7 softmax of Q tile 0 / 1, warp 8 TMA, warp 9 MMA
+constexpr int kTcThreads = 384;  // WG0/WG1: softmax of Q tile 0/1; WG2: warp 8 TMA, warp 9 MMA, 10-11 idle
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values stay <= 2^8 between rescales
 
 // 2^x on the FMA/ALU pipes (offloads the MUFU unit): x = n + f, n = rint(x)
@@ -191,6 +192,46 @@ __device__ __forceinline__ float exp2_poly(float x) {
     return __int_as_float(__float_as_int(q) + (n << 23));
 }
 
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2): two lanes of the softmax per instruction.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// exp2_poly on a pair: 2 FMNMX + 3 FADD2/FFMA2 + 3 FFMA2 + 2 IMAD for two values.
+// The exponent add folds (bits(t) - 0x4B400000) << 23 into bits(t) << 23 (the
+// constant vanishes mod 2^32).
+__device__ __forceinline__ void exp2_poly2(uint64_t x2, float &a, float &b) {
+    float x0, x1;
+    f2unpack(x2, x0, x1);
+    x2 = f2pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+    const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+    const uint64_t t = fadd2(x2, magic);
+    const uint64_t r = fadd2(t, f2pack(-12582912.0f, -12582912.0f));
+    const uint64_t f = ffma2(r, f2pack(-1.0f, -1.0f), x2);
+    uint64_t q = ffma2(f2pack(0.05502927f, 0.05502927f), f, f2pack(0.24225698f, 0.24225698f));
+    q = ffma2(q, f, f2pack(0.69325305f, 0.69325305f));
+    q = ffma2(q, f, f2pack(0.99995134f, 0.99995134f));
+    float q0, q1, t0, t1;
+    f2unpack(q, q0, q1);
+    f2unpack(t, t0, t1);
+    a = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+    b = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
+
 // Two 128-row Q tiles per CTA (FA4-style ping-pong) share every K/V tile, so a
 // KV byte staged from L2 feeds 256 query rows; P never leaves TMEM: softmax
 // overwrites S's first 64 columns with packed bf16 P and PV is a TS-MMA (A from
@@ -203,15 +244,17 @@ struct TcSmem {
     static constexpr int kHalf = kTcRows * 128;        // one [128][64] bf16 half tile = 16 KB
     static constexpr int kQ = NH * kHalf;              // one 128-row Q tile
     static constexpr int kKV = NH * kHalf;             // one K (or V) tile of 128 keys
+    static constexpr int kKStages = 3;                 // K ring: freed as soon as both QKs read it
+    static constexpr int kVStages = 2;                 // V ring: freed after both PVs
     static constexpr int oQ = 0;                       // 2 Q tiles
-    static constexpr int oK = oQ + 2 * kQ;             // 2 stages
-    static constexpr int oV = oK + 2 * kKV;            // 2 stages
-    static constexpr int oBar = oV + 2 * kKV;
+    static constexpr int oK = oQ + 2 * kQ;
+    static constexpr int oV = oK + kKStages * kKV;
+    static constexpr int oBar = oV + kVStages * kKV;
     static constexpr int kBytes = oBar + 256 + 1024;   // barriers + alignment slack
 };
 
-enum { BAR_KFULL = 0, BAR_VFULL = 2, BAR_KVEMPTY = 4, BAR_SFULL = 6, BAR_PFULL = 8, BAR_ODONE = 10, BAR_QREADY = 11,
-       BAR_N = 12 };
+enum { BAR_KFULL = 0, BAR_KEMPTY = 3, BAR_VFULL = 6, BAR_VEMPTY = 8, BAR_SFULL = 10, BAR_PFULL = 12, BAR_ODONE = 14,
+       BAR_QREADY = 15, BAR_N = 16 };
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -246,12 +289,16 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     const TcItem it = p.tc[blockIdx.x];
     const int nkt = (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys;
     const int ntiles = it.nrows > kTcRows ? 2 : 1;
+    long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;   // debug timeline (NULL: off)
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < L::kKStages; ++i) {
             mbar_init(bar(BAR_KFULL + i), 1);
+            mbar_init(bar(BAR_KEMPTY + i), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(bar(BAR_VFULL + i), 1);
-            mbar_init(bar(BAR_KVEMPTY + i), 1);
+            mbar_init(bar(BAR_VEMPTY + i), 1);
             mbar_init(bar(BAR_SFULL + i), 1);
             mbar_init(bar(BAR_PFULL + i), 128);
         }
@@ -268,35 +315,48 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // register rebalance between warpgroups (setmaxnreg at the head of each role):
+    // producers need few registers, a softmax thread holds a 128-column S row
+    if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (warp == 8) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             const int32_t *bt = p.bt_flat + it.bt_off;
             const int kb0 = it.k0 / kBlock;
             const int kb_last = (it.k1 - 1) / kBlock;
-            for (int j = 0; j < nkt; ++j) {
-                const int s = j & 1;
-                if (j >= 2) mbar_wait(bar(BAR_KVEMPTY + s), ((j - 2) >> 1) & 1);
-                const uint32_t dk = sK + s * L::kKV, dv = sV + s * L::kKV;
-                int rows[8];
+            auto rows_of = [&](int j, int *rows) {
 #pragma unroll
                 for (int b = 0; b < 8; ++b) {
                     int kb = kb0 + j * 8 + b;
                     kb = kb <= kb_last ? kb : kb0;  // rows past k1 are masked; keep the data finite
                     rows[b] = (bt[kb] * p.H_kv + it.g) * kBlock;
                 }
-                mbar_expect_tx(bar(BAR_KFULL + s), L::kKV);
+            };
+            auto load = [&](const CUtensorMap *tm, uint32_t dst, uint32_t fb, const int *rows) {
+                mbar_expect_tx(fb, L::kKV);
 #pragma unroll
                 for (int b = 0; b < 8; ++b)
 #pragma unroll
                     for (int h = 0; h < NH; ++h)
-                        tma_load_2d(dk + h * L::kHalf + b * (kBlock * 128), &tmap_k, h * 64, rows[b], bar(BAR_KFULL + s));
-                mbar_expect_tx(bar(BAR_VFULL + s), L::kKV);
-#pragma unroll
-                for (int b = 0; b < 8; ++b)
-#pragma unroll
-                    for (int h = 0; h < NH; ++h)
-                        tma_load_2d(dv + h * L::kHalf + b * (kBlock * 128), &tmap_v, h * 64, rows[b], bar(BAR_VFULL + s));
+                        tma_load_2d(dst + h * L::kHalf + b * (kBlock * 128), tm, h * 64, rows[b], fb);
+            };
+            // K runs one tile ahead of V: K0, K1, V0, K2, V1, ...
+            for (int j = 0; j <= nkt; ++j) {
+                if (j < nkt) {
+                    const int ks = j % L::kKStages;
+                    if (j >= L::kKStages) mbar_wait(bar(BAR_KEMPTY + ks), ((j / L::kKStages) - 1) & 1);
+                    if (tr && j < 64) tr[1024 + 2 * j] = clock64();
+                    int rows[8];
+                    rows_of(j, rows);
+                    load(&tmap_k, sK + ks * L::kKV, bar(BAR_KFULL + ks), rows);
+                }
+                if (j >= 1) {
+                    const int jv = j - 1, vs = jv & 1;
+                    if (jv >= 2) mbar_wait(bar(BAR_VEMPTY + vs), ((jv >> 1) - 1) & 1);
+                    int rows[8];
+                    rows_of(jv, rows);
+                    load(&tmap_v, sV + vs * L::kKV, bar(BAR_VFULL + vs), rows);
+                }
             }
         }
     } else if (warp == 9) {
@@ -306,13 +366,14 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);    // O += P V: A (P) in TMEM, B (V) MN-major
             mbar_wait(bar(BAR_QREADY), 0);
             auto issue_qk = [&](int t, int j) {
-                const uint32_t tS = tmem + 256 * t, q = sQ + t * L::kQ, k = sK + (j & 1) * L::kKV;
+                const uint32_t tS = tmem + 256 * t, q = sQ + t * L::kQ, k = sK + (j % L::kKStages) * L::kKV;
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = (ks / 4) * L::kHalf + (ks % 4) * 32;
                     umma_bf16(tS, smem_desc(q + off, 16, 1024), smem_desc(k + off, 16, 1024), idS, ks > 0);
                 }
                 umma_commit(bar(BAR_SFULL + t));
+                if (t == ntiles - 1) umma_commit(bar(BAR_KEMPTY + j % L::kKStages));  // both QKs read K(j)
             };
             mbar_wait(bar(BAR_KFULL), 0);
             tc_fence_after();
@@ -321,6 +382,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 const int s = j & 1;
                 for (int t = 0; t < ntiles; ++t) {
                     mbar_wait(bar(BAR_PFULL + t), j & 1);
+                    if (tr && j < 64) tr[8 * j + 2 * t] = clock64();
                     if (t == 0) mbar_wait(bar(BAR_VFULL + s), (j >> 1) & 1);
                     tc_fence_after();
                     const uint32_t tS = tmem + 256 * t, tO = tS + 128;
@@ -330,18 +392,20 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                                      (j > 0 || ks > 0));
                     if (j + 1 < nkt) {
                         if (t == 0) {
-                            mbar_wait(bar(BAR_KFULL + (s ^ 1)), ((j + 1) >> 1) & 1);
+                            mbar_wait(bar(BAR_KFULL + (j + 1) % L::kKStages), ((j + 1) / L::kKStages) & 1);
                             tc_fence_after();
                         }
                         issue_qk(t, j + 1);   // in-order after PV(t, j): overwrites S/P of tile t safely
                     }
+                    if (tr && j < 64) tr[8 * j + 2 * t + 1] = clock64();
                 }
-                umma_commit(bar(BAR_KVEMPTY + s));
+                umma_commit(bar(BAR_VEMPTY + s));   // both PVs read V(j)
             }
             umma_commit(bar(BAR_ODONE));
         }
-    } else {
+    } else if (warp < 8) {
         // ===================== softmax / correction / epilogue (warps 0-7) =====================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
         const int t = warp >> 2;             // Q tile of this warpgroup
         const int r = threadIdx.x & 127;     // row in the tile == TMEM lane
         const int rr = t * kTcRows + r;      // stacked row of the item
@@ -379,6 +443,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             float l_sum = 0.f;
             for (int j = 0; j < nkt; ++j) {
                 mbar_wait(bar(BAR_SFULL + t), j & 1);   // QK(t, j) and everything before it (PV(t, j-1)) done
+                if (tr && r == 0 && j < 64) tr[512 + 256 * t + 2 * j] = clock64();
                 tc_fence_after();
                 uint32_t sr[128];
 #pragma unroll
@@ -417,25 +482,37 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     }
                 }
                 const float nref = (m_used == -CUDART_INF_F) ? 0.f : -m_used;
-                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(nref, nref);
+                uint64_t ls2[2] = {0ull, 0ull};
                 uint32_t pk[64];
 #pragma unroll
                 for (int c = 0; c < 64; ++c) {
-                    const float x0 = fmaf(__uint_as_float(sr[2 * c]), sc, nref);
-                    const float x1 = fmaf(__uint_as_float(sr[2 * c + 1]), sc, nref);
-                    // one pair in four on the FMA pipe, three on MUFU (offload, FA4-style)
-                    const float a = ((c & 3) == 3) ? exp2_poly(x0) : ex2(x0);
-                    const float b = ((c & 3) == 3) ? exp2_poly(x1) : ex2(x1);
-                    ls[c & 3] += a + b;
+                    const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
+                                              nref2);
+                    float a, b;
+                    if ((c & 3) == 3) {   // one pair in four on the FMA pipe, three on MUFU (FA4-style offload)
+                        exp2_poly2(x2, a, b);
+                    } else {
+                        float x0, x1;
+                        f2unpack(x2, x0, x1);
+                        a = ex2(x0);
+                        b = ex2(x1);
+                    }
+                    const uint64_t ab = f2pack(a, b);
+                    ls2[c & 1] = fadd2(ls2[c & 1], ab);
                     pk[c] = pack2(a, b);
                 }
-                l_sum = l_sum * alpha + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
+                float l0, l1, l2, l3;
+                f2unpack(ls2[0], l0, l1);
+                f2unpack(ls2[1], l2, l3);
+                l_sum = l_sum * alpha + ((l0 + l1) + (l2 + l3));
                 // P (bf16 pairs) over S's first 64 columns of this lane
                 TMEM_ST32(tS, pk);
                 TMEM_ST32(tS + 32, (&pk[32]));
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(bar(BAR_PFULL + t));
+                if (tr && r == 0 && j < 64) tr[512 + 256 * t + 2 * j + 1] = clock64();
             }
             // ---- epilogue ----
             mbar_wait(bar(BAR_ODONE), 0);

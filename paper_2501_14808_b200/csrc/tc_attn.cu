@@ -137,6 +137,17 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
         "}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "elect.sync _|P, 0xffffffff;\n"
+        "selp.b32 %0, 1, 0, P;\n"
+        "}\n"
+        : "=r"(p));
+    return p != 0;
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                  : "memory");
@@ -254,7 +265,7 @@ struct TcSmem {
 };
 
 enum { BAR_KFULL = 0, BAR_KEMPTY = 3, BAR_VFULL = 6, BAR_VEMPTY = 8, BAR_SFULL = 10, BAR_PFULL = 12, BAR_ODONE = 14,
-       BAR_QREADY = 15, BAR_N = 16 };
+       BAR_QREADY = 15, BAR_PHALF = 16, BAR_N = 18 };
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -301,6 +312,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             mbar_init(bar(BAR_VEMPTY + i), 1);
             mbar_init(bar(BAR_SFULL + i), 1);
             mbar_init(bar(BAR_PFULL + i), 128);
+            mbar_init(bar(BAR_PHALF + i), 128);
         }
         mbar_init(bar(BAR_ODONE), 1);
         mbar_init(bar(BAR_QREADY), 256);
@@ -361,48 +373,74 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         }
     } else if (warp == 9) {
         // ===================== MMA issuer =====================
-        if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A, B K-major (smem)
-            constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);    // O += P V: A (P) in TMEM, B (V) MN-major
-            mbar_wait(bar(BAR_QREADY), 0);
-            auto issue_qk = [&](int t, int j) {
-                const uint32_t tS = tmem + 256 * t, q = sQ + t * L::kQ, k = sK + (j % L::kKStages) * L::kKV;
+        // The whole warp runs the control flow (warp-uniform: descriptors live in
+        // uniform registers, no per-MMA register->uniform moves); one elected lane
+        // issues each tcgen05 instruction.  Descriptors are built once and advanced
+        // by compile-time offsets (start address field counts 16-byte units).
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A, B K-major (smem)
+        constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);    // O += P V: A (P) in TMEM, B (V) MN-major
+        const uint64_t dQ0 = smem_desc(sQ, 16, 1024);
+        const uint64_t dK0 = smem_desc(sK, 16, 1024);
+        const uint64_t dV0 = smem_desc(sV, L::kHalf, 1024);
+        mbar_wait(bar(BAR_QREADY), 0);
+        auto issue_qk = [&](int t, int j) {
+            const uint32_t tS = tmem + 256 * t;
+            const uint64_t dq = dQ0 + (uint64_t)((t * L::kQ) >> 4);
+            const uint64_t dk = dK0 + (uint64_t)(((j % L::kKStages) * L::kKV) >> 4);
+            if (elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t off = (ks / 4) * L::kHalf + (ks % 4) * 32;
-                    umma_bf16(tS, smem_desc(q + off, 16, 1024), smem_desc(k + off, 16, 1024), idS, ks > 0);
+                    constexpr int kh = L::kHalf;
+                    const uint32_t off = ((ks / 4) * kh + (ks % 4) * 32) >> 4;
+                    umma_bf16(tS, dq + off, dk + off, idS, ks > 0);
                 }
                 umma_commit(bar(BAR_SFULL + t));
                 if (t == ntiles - 1) umma_commit(bar(BAR_KEMPTY + j % L::kKStages));  // both QKs read K(j)
-            };
-            mbar_wait(bar(BAR_KFULL), 0);
-            tc_fence_after();
-            for (int t = 0; t < ntiles; ++t) issue_qk(t, 0);
-            for (int j = 0; j < nkt; ++j) {
-                const int s = j & 1;
-                for (int t = 0; t < ntiles; ++t) {
-                    mbar_wait(bar(BAR_PFULL + t), j & 1);
-                    if (tr && j < 64) tr[8 * j + 2 * t] = clock64();
-                    if (t == 0) mbar_wait(bar(BAR_VFULL + s), (j >> 1) & 1);
-                    tc_fence_after();
-                    const uint32_t tS = tmem + 256 * t, tO = tS + 128;
-#pragma unroll
-                    for (int ks = 0; ks < kTcKeys / 16; ++ks)   // P: 16 keys = 8 packed columns per k-step
-                        umma_bf16_ts(tO, tS + ks * 8, smem_desc(sV + s * L::kKV + ks * 2048, L::kHalf, 1024), idO,
-                                     (j > 0 || ks > 0));
-                    if (j + 1 < nkt) {
-                        if (t == 0) {
-                            mbar_wait(bar(BAR_KFULL + (j + 1) % L::kKStages), ((j + 1) / L::kKStages) & 1);
-                            tc_fence_after();
-                        }
-                        issue_qk(t, j + 1);   // in-order after PV(t, j): overwrites S/P of tile t safely
-                    }
-                    if (tr && j < 64) tr[8 * j + 2 * t + 1] = clock64();
-                }
-                umma_commit(bar(BAR_VEMPTY + s));   // both PVs read V(j)
             }
-            umma_commit(bar(BAR_ODONE));
+            __syncwarp();
+        };
+        mbar_wait(bar(BAR_KFULL), 0);
+        tc_fence_after();
+        for (int t = 0; t < ntiles; ++t) issue_qk(t, 0);
+        for (int j = 0; j < nkt; ++j) {
+            const int s = j & 1;
+            const uint64_t dv = dV0 + (uint64_t)((s * L::kKV) >> 4);
+            for (int t = 0; t < ntiles; ++t) {
+                // PV in two halves: keys 0-63 as soon as the softmax has written them
+                mbar_wait(bar(BAR_PHALF + t), j & 1);
+                if (tr && j < 64 && lane == 0) tr[8 * j + 2 * t] = clock64();
+                if (t == 0) mbar_wait(bar(BAR_VFULL + s), (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t tS = tmem + 256 * t, tO = tS + 128;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    if (half == 1) {
+                        mbar_wait(bar(BAR_PFULL + t), j & 1);
+                        tc_fence_after();
+                    }
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < kTcKeys / 32; ++kk) {   // P: 16 keys = 8 packed columns per k-step
+                            const int ks = half * (kTcKeys / 32) + kk;
+                            umma_bf16_ts(tO, tS + ks * 8, dv + (uint64_t)((ks * 2048) >> 4), idO, (j > 0 || ks > 0));
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (j + 1 < nkt) {
+                    if (t == 0) {
+                        mbar_wait(bar(BAR_KFULL + (j + 1) % L::kKStages), ((j + 1) / L::kKStages) & 1);
+                        tc_fence_after();
+                    }
+                    issue_qk(t, j + 1);   // in-order after PV(t, j): overwrites S/P of tile t safely
+                }
+                if (tr && j < 64 && lane == 0) tr[8 * j + 2 * t + 1] = clock64();
+            }
+            if (elect_one()) umma_commit(bar(BAR_VEMPTY + s));   // both PVs read V(j)
+            __syncwarp();
         }
+        if (elect_one()) umma_commit(bar(BAR_ODONE));
+        __syncwarp();
     } else if (warp < 8) {
         // ===================== softmax / correction / epilogue (warps 0-7) =====================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
@@ -487,6 +525,12 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 uint32_t pk[64];
 #pragma unroll
                 for (int c = 0; c < 64; ++c) {
+                    if (c == 32) {   // first half of P (keys 0-63) -> TMEM: the MMA can start PV on it
+                        TMEM_ST32(tS, pk);
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(bar(BAR_PHALF + t));
+                    }
                     const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
                                               nref2);
                     float a, b;
@@ -506,8 +550,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 f2unpack(ls2[0], l0, l1);
                 f2unpack(ls2[1], l2, l3);
                 l_sum = l_sum * alpha + ((l0 + l1) + (l2 + l3));
-                // P (bf16 pairs) over S's first 64 columns of this lane
-                TMEM_ST32(tS, pk);
+                // second half of P (bf16 pairs, keys 64-127) over S's columns 32-63 of this lane
                 TMEM_ST32(tS + 32, (&pk[32]));
                 tmem_wait_st();
                 tc_fence_before();

@@ -330,8 +330,9 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     // register rebalance between warpgroups (setmaxnreg at the head of each role):
     // producers need few registers, a softmax thread holds a 128-column S row
     if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-    if (warp == 8) {
-        // ===================== TMA producer =====================
+    if (warp == 8 || warp == 10) {
+        // ===================== TMA producers: warp 8 streams K, warp 10 streams V =====================
+        // (separate threads so a V slot that is still busy never delays the next K load)
         if (lane == 0) {
             const int32_t *bt = p.bt_flat + it.bt_off;
             const int kb0 = it.k0 / kBlock;
@@ -352,9 +353,8 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     for (int h = 0; h < NH; ++h)
                         tma_load_2d(dst + h * L::kHalf + b * (kBlock * 128), tm, h * 64, rows[b], fb);
             };
-            // K runs one tile ahead of V: K0, K1, V0, K2, V1, ...
-            for (int j = 0; j <= nkt; ++j) {
-                if (j < nkt) {
+            if (warp == 8) {
+                for (int j = 0; j < nkt; ++j) {
                     const int ks = j % L::kKStages;
                     if (j >= L::kKStages) mbar_wait(bar(BAR_KEMPTY + ks), ((j / L::kKStages) - 1) & 1);
                     if (tr && j < 64) tr[1024 + 2 * j] = clock64();
@@ -362,8 +362,9 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     rows_of(j, rows);
                     load(&tmap_k, sK + ks * L::kKV, bar(BAR_KFULL + ks), rows);
                 }
-                if (j >= 1) {
-                    const int jv = j - 1, vs = jv & 1;
+            } else {
+                for (int jv = 0; jv < nkt; ++jv) {
+                    const int vs = jv & 1;
                     if (jv >= 2) mbar_wait(bar(BAR_VEMPTY + vs), ((jv >> 1) - 1) & 1);
                     int rows[8];
                     rows_of(jv, rows);

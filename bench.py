@@ -52,7 +52,7 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi style clock / throttle sampling through NVML during the timed region."""
 
-    def __init__(self, device_index: int, period_s: float = 0.02):
+    def __init__(self, device_index: int, period_s: float = 0.002):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.dev, self.period = device_index, period_s
         self._stop = threading.Event()
@@ -344,10 +344,23 @@ def extra_configs(args, peaks, dev):
         m = statistics.median(ms)
         bt, fl = alg_bytes_total(spec), alg_flops(spec)
         t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
+        kms = {k: (statistics.median(v) if v else None) for k, v in ker.items()}
         out[name] = {"tokens_per_s": spec.T / (m / 1e3), "ms_per_step": m, "t_roof_ms": t_roof * 1e3,
                      "step_roof_frac": t_roof * 1e3 / m, "alg_bytes": bt, "alg_flops": fl,
-                     "kernel_ms": {k: (statistics.median(v) if v else None) for k, v in ker.items()},
-                     "plan": hg.hg_last_plan_stats(wl.pool)}
+                     "kernel_ms": kms, "plan": hg.hg_last_plan_stats(wl.pool)}
+        if name.startswith("p") and kms["tc"]:
+            # tensor-bound: the tcgen05 kernel does all the work; algorithmic (causal) FLOPs
+            ach = fl / (kms["tc"] / 1e3) / 1e12
+            out[name]["roofline"] = {"bound": "tensor", "kernel": "tc_attn_kernel<128>", "achieved": ach,
+                                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                                     "frac": ach / peaks["bf16_tflops"],
+                                     "peak_kind": "measured burst (MEASURED_PEAKS.json bf16_tflops, cuBLAS)"}
+        elif kms["splitk"]:
+            b_sk = alg_bytes_splitk(spec)
+            ach = b_sk / (kms["splitk"] / 1e3) / 1e9
+            out[name]["roofline"] = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": ach,
+                                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                                     "alg_bytes_per_launch": b_sk}
         wl.close()
         del wl
         torch.cuda.empty_cache()
@@ -525,7 +538,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", action="store_true", help="also time c2, c3, p1, p2 (context)")
+    ap.add_argument("--no-extra", dest="extra", action="store_false",
+                    help="skip the other configs (c2, c3, p1, p2) reported beside the headline")
     ap.add_argument("--profile", action="store_true", help="timed steps only (no e2e / cpu baseline): for ncu")
     ap.add_argument("--no-predictor", action="store_true", help="skip the C4 sweep + predictor fit")
     ap.add_argument("--sweep-iters", type=int, default=64, help="C4 iterations per (rho, chunk) point")

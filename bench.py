@@ -3,8 +3,8 @@
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--extra]
 
 A "step" is one pass of the whole hot path over one batch:
-host plan (validation, indices, prefix tile map) + descriptor H2D + KV append
-(hg_kv_append) + hybrid attention (hg_hybrid_attention), all through the C ABI.
+host plan (validation, indices, prefix tile map) + one descriptor H2D + KV append
++ hybrid attention, through the C ABI's fused entry point hg_hybrid_step.
 The N=1 workload is BASELINE.json configs[1] (Llama-2-7B attention shape,
 512-token prefill chunk + 64 decodes at ctx 1-4K: "c1").  With --gpus N > 1
 (torchrun, one rank per GPU) KV heads are sharded across ranks and outputs are
@@ -200,7 +200,7 @@ def run_ours(args):
     total_ms = sum(step_ms)
     ms = total_ms / args.steps
     stats = hg.hg_last_plan_stats(wl.pool)
-    launches_per_step = stats["kernels"] + 1    # + append
+    launches_per_step = stats["kernels"]        # fused step: append + tcgen05 + split-K + combine
     T = spec.T
     value = T * args.steps / (total_ms / 1e3)
 
@@ -229,6 +229,10 @@ def run_ours(args):
         "kernel_ms": {"splitk": sk_avg, "tc": statistics.mean(tc_ms) if tc_ms else None,
                       "combine": statistics.mean(cb_ms) if cb_ms else None},
         "host_call_ms": statistics.median(host_s) * 1e3,
+        "step_breakdown_ms": ({"start_to_splitk": statistics.median(s.elapsed_time(e[2]) for s, e in zip(starts, kev)),
+                               "splitk": statistics.median(sk_ms),
+                               "splitk_to_end": statistics.median(e[3].elapsed_time(x) for x, e in zip(ends, kev))}
+                              if sk_ms else None),
         "plan": stats,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,

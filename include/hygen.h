@@ -146,6 +146,15 @@ HG_API hg_status hg_hybrid_attention_ex(hg_kv_pool *pool, const hg_batch *batch,
                                  const void *q, void *out, float *lse, void *workspace,
                                  size_t workspace_bytes, void *stream, const hg_attn_opts *opts);
 
+/* Fused serving step on DEVICE buffers: hg_kv_append followed by
+ * hg_hybrid_attention_ex with one validation (append rules included), one plan
+ * and one descriptor upload; the append kernel derives each token's slot on the
+ * device from the attention descriptors.  Arguments as in the two calls;
+ * workspace from hg_hybrid_attention_workspace_size; opts may be NULL. */
+HG_API hg_status hg_hybrid_step(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads, const void *q,
+                                const void *k_new, const void *v_new, void *out, float *lse, void *workspace,
+                                size_t workspace_bytes, void *stream, const hg_attn_opts *opts);
+
 /* End-to-end serving step with HOST buffers (the e2e measurement of the
  * bench): H2D of q/k_new/v_new (host bf16, pinned for async overlap) into the
  * workspace, hg_kv_append, hg_hybrid_attention, D2H of out.  Synchronises the

@@ -83,6 +83,7 @@ _SIGS = {
     "hg_hybrid_attention": ([P, P, i32, P, P, P, P, ctypes.c_size_t, P], i32),
     "hg_hybrid_attention_ex": ([P, P, i32, P, P, P, P, ctypes.c_size_t, P, P], i32),
     "hg_hybrid_step_host": ([P, P, i32, P, P, P, P, P, ctypes.c_size_t, P], i32),
+    "hg_hybrid_step": ([P, P, i32, P, P, P, P, P, P, ctypes.c_size_t, P, P], i32),
     "hg_hybrid_step_host_workspace_size": ([P, P, i32, P], i32),
     "hg_batch_indices": ([P, P, P, P, P, P], i32),
     "hg_last_plan_stats": ([P, P], i32),
@@ -252,6 +253,15 @@ def hg_hybrid_attention(pool: KVPool, batch: Batch, num_q_heads: int, q, out, ls
     else:
         _check(lib().hg_hybrid_attention_ex(pool.h, batch.ref(), num_q_heads, _ptr(q), _ptr(out), _ptr(lse),
                                             _ptr(workspace), ws_bytes, _stream_ptr(stream), ctypes.byref(opts)))
+
+
+def hg_hybrid_step(pool: KVPool, batch: Batch, num_q_heads: int, q, k_new, v_new, out, lse=None, workspace=None,
+                   stream=None, opts: Optional[hg_attn_opts] = None) -> None:
+    """Fused hg_kv_append + hg_hybrid_attention (one plan, one descriptor upload)."""
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().hg_hybrid_step(pool.h, batch.ref(), num_q_heads, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
+                                _ptr(lse), _ptr(workspace), ws_bytes, _stream_ptr(stream),
+                                None if opts is None else ctypes.byref(opts)))
 
 
 def hg_hybrid_step_host_workspace_size(pool: KVPool, batch: Batch, num_q_heads: int) -> int:

@@ -38,6 +38,9 @@ struct hg_kv_pool {
     bool tmap_ok = false;
     hg_plan_stats last{};
     Plan plan;  // reused storage
+    // side stream: the split-K kernel runs beside the tcgen05 kernel (fork/join by events)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace hg {
@@ -123,6 +126,12 @@ extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
         if (s.host) cudaFreeHost(s.host);
         if (s.ev) cudaEventDestroy(s.ev);
     }
+    if (p->side) {
+        cudaStreamSynchronize(p->side);
+        cudaStreamDestroy(p->side);
+    }
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
     delete p;
     return HG_OK;
 }
@@ -278,10 +287,10 @@ static PlanOpts plan_opts(const hg_kv_pool *pool, const hg_attn_opts *o) {
 }
 
 static hg_status plan_call(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const hg_attn_opts *o,
-                           BatchView *v, Plan *plan) {
+                           BatchView *v, Plan *plan, bool append = false) {
     hg_status s = view_batch(batch, v);
     if (s) return s;
-    s = validate(*v, pool->desc.block_size, pool->desc.num_blocks, H_q, pool->desc.num_kv_heads, false);
+    s = validate(*v, pool->desc.block_size, pool->desc.num_blocks, H_q, pool->desc.num_kv_heads, append);
     if (s) return s;
     PlanOpts po = plan_opts(pool, o);
     if (!pool->tmap_ok) po.use_tc = false;
@@ -299,11 +308,14 @@ extern "C" hg_status hg_hybrid_attention_workspace_size(const hg_kv_pool *pool, 
     return HG_OK;
 }
 
+// k_new / v_new non-NULL: fused step, the append kernel runs first from the same
+// descriptors (slots computed on the device).
 static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, void *out,
-                                float *lse, void *ws, size_t ws_bytes, cudaStream_t st, const hg_attn_opts *o) {
+                                float *lse, void *ws, size_t ws_bytes, cudaStream_t st, const hg_attn_opts *o,
+                                bool fused = false, const void *k_new = nullptr, const void *v_new = nullptr) {
     BatchView v;
     Plan &plan = pool->plan;
-    hg_status s = plan_call(pool, batch, H_q, o, &v, &plan);
+    hg_status s = plan_call(pool, batch, H_q, o, &v, &plan, fused);
     if (s) return s;
     s = sticky_check();
     if (s) return s;
@@ -312,6 +324,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         return HG_OK;
     }
     if (!q || !out) return fail(HG_E_INVALID, "q / out NULL");
+    if (fused && (!k_new || !v_new)) return fail(HG_E_INVALID, "k_new / v_new NULL");
     if (!ws || ws_bytes < plan.total_bytes)
         return fail(HG_E_INVALID, "workspace %zu bytes < required %zu", ws_bytes, plan.total_bytes);
     // one image of all descriptors -> one pinned H2D copy
@@ -323,8 +336,8 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_sk, plan.sk.data(), sizeof(SkItem) * plan.sk.size());
     put(plan.off_tc, plan.tc.data(), sizeof(TcItem) * plan.tc.size());
     put(plan.off_rows, plan.tc_tok.data(), sizeof(int32_t) * plan.tc_tok.size());
-    put(plan.off_cbase, plan.comb_base.data(), sizeof(int32_t) * plan.comb_base.size());
-    put(plan.off_comb, plan.comb.data(), sizeof(CombItem) * plan.comb.size());
+    put(plan.off_cbase, plan.tok.data(), sizeof(TokDev) * plan.tok.size());
+    put(plan.off_comb, plan.comb.data(), sizeof(int32_t) * plan.comb.size());
     s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
     if (s) return s;
     uint8_t *w = (uint8_t *)ws;
@@ -339,8 +352,8 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.sk = (const SkItem *)(w + plan.off_sk);
     p.tc = (const TcItem *)(w + plan.off_tc);
     p.tc_tok = (const int32_t *)(w + plan.off_rows);
-    p.comb_base = (const int32_t *)(w + plan.off_cbase);
-    p.comb = (const CombItem *)(w + plan.off_comb);
+    p.tok = (const TokDev *)(w + plan.off_cbase);
+    p.comb = (const int32_t *)(w + plan.off_comb);
     p.part_o = (float *)(w + plan.off_part_o);
     p.part_lse = (float *)(w + plan.off_part_lse);
     p.H_q = H_q;
@@ -353,35 +366,69 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.d));
     p.trace = o ? (long long *)o->debug_trace : nullptr;
     int kernels = 0;
-    auto rec = [&](int k) {
-        if (o && o->events[k]) cudaEventRecord((cudaEvent_t)o->events[k], st);
+    auto rec = [&](int k, cudaStream_t on) {
+        if (o && o->events[k]) cudaEventRecord((cudaEvent_t)o->events[k], on);
     };
+    // The tcgen05 tiles (tensor-bound) and the split-K items (HBM-bound) are
+    // independent: the tcgen05 kernel is launched first on the caller's stream
+    // (its CTAs are placed first), the split-K kernel on a side stream forked
+    // after the descriptor copy; the combine waits for both.
+    if (fused) {
+        s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st);
+        if (s) return s;
+        ++kernels;
+    }
+    const bool overlap = p.n_tc && p.n_sk;
+    cudaStream_t sk_stream = st;
+    if (overlap) {
+        if (!pool->side) {
+            s = cuda_check(cudaStreamCreateWithFlags(&pool->side, cudaStreamNonBlocking), "side stream");
+            if (s) return s;
+            s = cuda_check(cudaEventCreateWithFlags(&pool->ev_fork, cudaEventDisableTiming), "fork event");
+            if (s) return s;
+            s = cuda_check(cudaEventCreateWithFlags(&pool->ev_join, cudaEventDisableTiming), "join event");
+            if (s) return s;
+        }
+        sk_stream = pool->side;
+        s = cuda_check(cudaEventRecord(pool->ev_fork, st), "fork record");
+        if (s) return s;
+    }
     if (p.n_tc) {
-        rec(0);
+        rec(0, st);
         s = launch_tc(p, pool->tmap_k, pool->tmap_v, st);
         if (s) return s;
-        rec(1);
+        rec(1, st);
         ++kernels;
     }
     if (p.n_sk) {
-        rec(2);
-        s = launch_splitk(p, st);
+        if (overlap) {
+            s = cuda_check(cudaStreamWaitEvent(sk_stream, pool->ev_fork, 0), "fork wait");
+            if (s) return s;
+        }
+        rec(2, sk_stream);
+        s = launch_splitk(p, sk_stream);
         if (s) return s;
-        rec(3);
+        rec(3, sk_stream);
         ++kernels;
     }
+    if (overlap) {
+        s = cuda_check(cudaEventRecord(pool->ev_join, sk_stream), "join record");
+        if (s) return s;
+        s = cuda_check(cudaStreamWaitEvent(st, pool->ev_join, 0), "join wait");
+        if (s) return s;
+    }
     if (p.n_comb) {
-        rec(4);
+        rec(4, st);
         s = launch_combine(p, st);
         if (s) return s;
-        rec(5);
+        rec(5, st);
         ++kernels;
     }
     hg_plan_stats &ls = pool->last;
     ls.tc_tiles = p.n_tc;
     ls.prefix_tiles = plan.prefix_tiles;
-    ls.splitk_items = p.n_sk;
-    ls.combine_rows = p.n_comb;
+    ls.splitk_items = p.n_sk * p.H_kv;   // CTAs: items x KV heads
+    ls.combine_rows = p.n_comb * p.H_kv; // (token, KV head) pairs
     ls.kernels = kernels;
     ls.kv_bytes_unique = plan.kv_bytes_unique;
     ls.kv_bytes_read = plan.kv_bytes_read;
@@ -394,6 +441,14 @@ extern "C" hg_status hg_hybrid_attention_ex(hg_kv_pool *pool, const hg_batch *ba
     if (!pool) return fail(HG_E_INVALID, "pool is NULL");
     return attention_impl(pool, batch, num_q_heads, q, out, lse, workspace, workspace_bytes,
                           (cudaStream_t)stream, opts);
+}
+
+extern "C" hg_status hg_hybrid_step(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads, const void *q,
+                                    const void *k_new, const void *v_new, void *out, float *lse, void *workspace,
+                                    size_t workspace_bytes, void *stream, const hg_attn_opts *opts) {
+    if (!pool) return fail(HG_E_INVALID, "pool is NULL");
+    return attention_impl(pool, batch, num_q_heads, q, out, lse, workspace, workspace_bytes, (cudaStream_t)stream,
+                          opts, true, k_new, v_new);
 }
 
 extern "C" hg_status hg_hybrid_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
@@ -462,9 +517,8 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     if (s) return s;
     s = cuda_check(cudaMemcpyAsync(v_d, v_new_host, T * Hk * d * 2, cudaMemcpyHostToDevice, st), "H2D v");
     if (s) return s;
-    s = append_impl(pool, v, k_d, v_d, slot_d, st);
-    if (s) return s;
-    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, workspace, attn, st, nullptr);
+    (void)slot_d;
+    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, workspace, attn, st, nullptr, true, k_d, v_d);
     if (s) return s;
     s = cuda_check(cudaMemcpyAsync(out_host, o_d, T * H_q * d * 2, cudaMemcpyDeviceToHost, st), "D2H out");
     if (s) return s;

@@ -23,17 +23,25 @@ struct ReqDev {
     int32_t bt_off;  // offset of the request's block ids in bt_flat
 };
 
-// Split-K item (sm_100a mma.sync path, kernels.cu): up to 16 stacked query rows
-// (token j0 + r / G_q, head g*G_q + r % G_q) of one request against keys
-// [k0, k1) further capped per row by causality (key <= c + j).
+// Split-K item (sm_100a mma.sync path, kernels.cu), launched once per KV head g
+// (grid.y): up to 16 stacked query rows (token j0 + r / G_q, head g*G_q + r % G_q)
+// of one request against keys [k0, k1) further capped per row by causality.
 struct SkItem {
     int32_t req;
-    int32_t g;
     int32_t j0;
     int32_t nt;     // token rows in the item (nt * G_q <= 16)
     int32_t k0;     // multiple of kBlock
     int32_t k1;
-    int32_t part;   // partial index for rows that are combined
+    int32_t part;   // partial index for rows that are combined (-1: direct write)
+};
+
+// Per batch token: where its partials live.  Partial slot of (token t, KV head
+// g, part, q-head-in-group hl) = base + (g * nparts + part) * G_q + hl;
+// base = -1 means the token's rows have one part and are written directly.
+struct TokDev {
+    int32_t base;
+    int32_t nparts;
+    int32_t req;    // owning request (device-side slot computation of the fused append)
     int32_t pad;
 };
 
@@ -56,14 +64,6 @@ struct TcItem {
     int32_t hl0;     // q-head-in-group of stacked row 0
 };
 
-// (token, KV head) pair whose rows are merged from several partials.
-struct CombItem {
-    int32_t t;
-    int32_t g;
-    int32_t base;    // first partial slot; slot = base + part * G_q + (h % G_q)
-    int32_t nparts;
-};
-
 // Device-side view of one attention call.
 struct AttnParams {
     const uint16_t *k_cache;
@@ -76,8 +76,8 @@ struct AttnParams {
     const SkItem *sk;
     const TcItem *tc;
     const int32_t *tc_tok;     // member tokens of prefix-group tiles
-    const int32_t *comb_base;  // [T * H_kv]: first partial slot of (t, g) or -1 (direct write)
-    const CombItem *comb;
+    const TokDev *tok;         // [T]
+    const int32_t *comb;       // tokens whose rows are merged (combine grid.x)
     float *part_o;             // [slots][d] normalised partial outputs
     float *part_lse;           // [slots] log2-domain LSE of each partial (-inf: empty)
     int32_t H_q, H_kv, G_q, d;
@@ -96,8 +96,8 @@ struct Plan {
     std::vector<int32_t> tc_tok;
     std::vector<SkItem> sk_tmp;
     std::vector<TcItem> tc_tmp;
-    std::vector<int32_t> comb_base;
-    std::vector<CombItem> comb;
+    std::vector<TokDev> tok;
+    std::vector<int32_t> comb;
     int64_t n_slots = 0;
     int32_t prefix_tiles = 0;
     int64_t kv_bytes_unique = 0;
@@ -138,6 +138,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
 hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache,
                         uint16_t *v_cache, const int64_t *slot, int T, int H_kv, int d,
                         void *stream);
+hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream);
 hg_status launch_splitk(const AttnParams &p, void *stream);
 hg_status launch_combine(const AttnParams &p, void *stream);
 hg_status launch_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v, void *stream);

@@ -231,7 +231,9 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         const int nb = ceil_div((int64_t)v.c[i] + v.n[i], B);
         memcpy(p->bt_flat.data() + p->reqs[i].bt_off, v.bt + (int64_t)i * v.W, sizeof(int32_t) * (size_t)nb);
     }
-    p->comb_base.assign((size_t)T * H_kv, -1);
+    p->tok.resize((size_t)T);
+    for (int i = 0; i < v.R; ++i)
+        for (int j = 0; j < v.n[i]; ++j) p->tok[(size_t)p->reqs[i].cu_q + j] = TokDev{-1, 1, i, 0};
 
     const std::vector<int32_t> &group = g_scr.group;
     const int ng = (int)g_scr.owners.size();
@@ -315,22 +317,19 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         const int pre = in_prefix_pass(ch.i) ? 1 : 0;
         const int pieces = std::max(1, ceil_div(ch.ke - ch.ks, chunk_tok));
         const int nparts = pre + pieces;
-        for (int g = 0; g < H_kv; ++g) {
-            if (nparts > 1) {
-                for (int jj = 0; jj < ch.nt; ++jj) {
-                    const int t = p->reqs[ch.i].cu_q + ch.j0 + jj;
-                    const int32_t base = (int32_t)p->n_slots;
-                    p->n_slots += (int64_t)nparts * G;
-                    p->comb_base[(size_t)t * H_kv + g] = base;
-                    p->comb.push_back(CombItem{t, g, base, nparts});
-                }
+        if (nparts > 1) {
+            for (int jj = 0; jj < ch.nt; ++jj) {
+                const int t = p->reqs[ch.i].cu_q + ch.j0 + jj;
+                p->tok[t] = TokDev{(int32_t)p->n_slots, nparts, ch.i, 0};
+                p->n_slots += (int64_t)nparts * G * H_kv;
+                p->comb.push_back(t);
             }
-            for (int k = 0; k < pieces; ++k) {
-                const int k0 = ch.ks + k * chunk_tok;
-                const int k1 = std::min(ch.ke, k0 + chunk_tok);
-                p->sk.push_back(SkItem{ch.i, g, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1, 0});
-                kv_tok_read += (k1 - k0);
-            }
+        }
+        for (int k = 0; k < pieces; ++k) {
+            const int k0 = ch.ks + k * chunk_tok;
+            const int k1 = std::min(ch.ke, k0 + chunk_tok);
+            p->sk.push_back(SkItem{ch.i, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1});
+            kv_tok_read += (int64_t)(k1 - k0) * H_kv;
         }
     }
     // ---- prefix group tiles (part 0 of every member row): member-major stacking ----
@@ -376,8 +375,8 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->off_sk = off;    off = align_up(off + sizeof(SkItem) * p->sk.size(), 16);
     p->off_tc = off;    off = align_up(off + sizeof(TcItem) * p->tc.size(), 16);
     p->off_rows = off;  off = align_up(off + sizeof(int32_t) * p->tc_tok.size(), 16);
-    p->off_cbase = off; off = align_up(off + sizeof(int32_t) * p->comb_base.size(), 16);
-    p->off_comb = off;  off = align_up(off + sizeof(CombItem) * p->comb.size(), 16);
+    p->off_cbase = off; off = align_up(off + sizeof(TokDev) * p->tok.size(), 16);
+    p->off_comb = off;  off = align_up(off + sizeof(int32_t) * p->comb.size(), 16);
     p->desc_bytes = off;
     off = align_up(off, 256);
     p->off_part_o = off;   off = align_up(off + sizeof(float) * (size_t)p->n_slots * d, 256);

@@ -54,6 +54,38 @@ hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
 }
 
+// Fused-step append: the slot of token t is derived on the device from the
+// attention descriptors (owning request, cached length, flattened block ids).
+__global__ void append_dev_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
+                                  uint4 *__restrict__ k_cache, uint4 *__restrict__ v_cache, const AttnParams p, int T,
+                                  int chunks_per_row) {
+    const int64_t total = (int64_t)T * p.H_kv * chunks_per_row;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = idx / chunks_per_row;
+        const int ch = (int)(idx % chunks_per_row);
+        const int t = (int)(row / p.H_kv);
+        const int g = (int)(row % p.H_kv);
+        const ReqDev rq = p.reqs[p.tok[t].req];
+        const int pos = rq.c + (t - rq.cu_q);
+        const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
+        const int64_t dst = ((blk * p.H_kv + g) * kBlock + pos % kBlock) * chunks_per_row + ch;
+        k_cache[dst] = k_new[idx];
+        v_cache[dst] = v_new[idx];
+    }
+}
+
+hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream) {
+    if (T == 0) return HG_OK;
+    const int cpr = p.d / 8;
+    const int64_t total = (int64_t)T * p.H_kv * cpr;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    append_dev_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)k_new, (const uint4 *)v_new,
+                                                                 (uint4 *)p.k_cache, (uint4 *)p.v_cache, p, T, cpr);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
+}
+
 // ----------------------------------------------------------------------------
 // PTX helpers
 // ----------------------------------------------------------------------------
@@ -127,6 +159,7 @@ splitk_kernel(const AttnParams p) {
     constexpr int NNT = D / 8;   // n-tiles over the head dim (PV)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SkItem it = p.sk[blockIdx.x];
+    const int g = blockIdx.y;   // KV head
     const ReqDev rq = p.reqs[it.req];
     const int G = p.G_q;
     const int nrows = it.nt * G;
@@ -139,7 +172,7 @@ splitk_kernel(const AttnParams p) {
         uint4 val = make_uint4(0, 0, 0, 0);
         if (r < nrows) {
             const int t = rq.cu_q + it.j0 + r / G;
-            const int h = it.g * G + r % G;
+            const int h = g * G + r % G;
             val = *reinterpret_cast<const uint4 *>(p.q + ((int64_t)t * p.H_q + h) * D + ch * 8);
         }
         *reinterpret_cast<uint4 *>(sQ + swz<D>(r, ch)) = val;
@@ -163,7 +196,7 @@ splitk_kernel(const AttnParams p) {
     const int64_t head_stride = (int64_t)kBlock * D;            // elements per (block, head)
     auto issue = [&](int bi, int stage) {
         const int kb = kb0 + warp + bi * kSkWarps;
-        const int64_t base = ((int64_t)bt[kb] * p.H_kv + it.g) * head_stride;
+        const int64_t base = ((int64_t)bt[kb] * p.H_kv + g) * head_stride;
         const uint16_t *gk = p.k_cache + base;
         const uint16_t *gv = p.v_cache + base;
         const uint32_t dk = sW_u + stage * SkSmem<D>::kStage;
@@ -317,8 +350,12 @@ splitk_kernel(const AttnParams p) {
             }
             const float inv = L > 0.f ? 1.f / L : 0.f;
             const int t = rq.cu_q + it.j0 + r / G;
-            const int h = it.g * G + r % G;
-            const int base = (it.part >= 0) ? p.comb_base[(int64_t)t * p.H_kv + it.g] : -1;
+            const int h = g * G + r % G;
+            int base = -1;
+            if (it.part >= 0) {
+                const TokDev tk = p.tok[t];
+                base = tk.base + g * tk.nparts * G;
+            }
             constexpr int PER = D / 8;
             float acc[PER];
 #pragma unroll
@@ -363,7 +400,7 @@ static hg_status launch_splitk_d(const AttnParams &p, cudaStream_t st) {
         cudaFuncSetAttribute(splitk_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         attr = true;
     }
-    splitk_kernel<D><<<p.n_sk, kSkWarps * 32, bytes, st>>>(p);
+    splitk_kernel<D><<<dim3(p.n_sk, p.H_kv), kSkWarps * 32, bytes, st>>>(p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "split-K launch: %s", cudaGetErrorString(e));
 }
@@ -377,28 +414,31 @@ hg_status launch_splitk(const AttnParams &p, void *stream) {
 
 // ----------------------------------------------------------------------------
 // a.7 combine: O = sum_s 2^{lse_s - LSE} o_s, LSE = log2 sum_s 2^{lse_s}
-// one warp per (token, KV head, q-head-in-group)
+// one warp per (merged token, KV head, q-head-in-group)
 // ----------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
-    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int G = p.G_q;
-    if (wid >= p.n_comb * G) return;
-    const CombItem ci = p.comb[wid / G];
-    const int hl = wid % G;
+    if (wid >= (int64_t)p.n_comb * p.H_kv * G) return;
+    const int t = p.comb[wid / (p.H_kv * G)];
+    const int rem = (int)(wid % (p.H_kv * G));
+    const int g = rem / G, hl = rem % G;
+    const TokDev tk = p.tok[t];
+    const int64_t base = tk.base + (int64_t)g * tk.nparts * G;
     float M = -CUDART_INF_F;
-    for (int s = 0; s < ci.nparts; ++s) M = fmaxf(M, p.part_lse[ci.base + s * G + hl]);
+    for (int s = 0; s < tk.nparts; ++s) M = fmaxf(M, p.part_lse[base + s * G + hl]);
     const float ref = (M == -CUDART_INF_F) ? 0.f : M;
     float L = 0.f;
-    for (int s = 0; s < ci.nparts; ++s) L += fast_exp2(p.part_lse[ci.base + s * G + hl] - ref);
+    for (int s = 0; s < tk.nparts; ++s) L += fast_exp2(p.part_lse[base + s * G + hl] - ref);
     const float inv = L > 0.f ? 1.f / L : 0.f;
     constexpr int PER = D / 32;
     float acc[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-    for (int s = 0; s < ci.nparts; ++s) {
-        const int64_t slot = ci.base + (int64_t)s * G + hl;
+    for (int s = 0; s < tk.nparts; ++s) {
+        const int64_t slot = base + (int64_t)s * G + hl;
         const float w = fast_exp2(p.part_lse[slot] - ref) * inv;
         const float *src = p.part_o + slot * D + lane * PER;
 #pragma unroll
@@ -408,17 +448,17 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
             acc[e + 1] += w * v.y;
         }
     }
-    const int h = ci.g * G + hl;
-    uint16_t *dst = p.out + ((int64_t)ci.t * p.H_q + h) * D + lane * PER;
+    const int h = g * G + hl;
+    uint16_t *dst = p.out + ((int64_t)t * p.H_q + h) * D + lane * PER;
 #pragma unroll
     for (int e = 0; e < PER; e += 2) *reinterpret_cast<uint32_t *>(dst + e) = pack_bf16(acc[e], acc[e + 1]);
     if (p.lse && lane == 0)
-        p.lse[(int64_t)ci.t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
+        p.lse[(int64_t)t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
 }
 
 hg_status launch_combine(const AttnParams &p, void *stream) {
     if (p.n_comb == 0) return HG_OK;
-    const int64_t warps = (int64_t)p.n_comb * p.G_q;
+    const int64_t warps = (int64_t)p.n_comb * p.H_kv * p.G_q;
     const int blocks = (int)((warps * 32 + 255) / 256);
     if (p.d == 128) combine_kernel<128><<<blocks, 256, 0, (cudaStream_t)stream>>>(p);
     else if (p.d == 64) combine_kernel<64><<<blocks, 256, 0, (cudaStream_t)stream>>>(p);

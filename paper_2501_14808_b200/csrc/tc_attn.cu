@@ -564,7 +564,11 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
             const float lse2 = l_sum > 0.f ? m_used + __log2f(l_sum) : -CUDART_INF_F;
             const int G = p.G_q;
-            const int base = (valid && it.part >= 0) ? p.comb_base[(int64_t)row.t * p.H_kv + it.g] : -1;
+            int base = -1;
+            if (valid && it.part >= 0) {
+                const TokDev tk = p.tok[row.t];
+                base = tk.base + it.g * tk.nparts * G;   // + part * G + hl below
+            }
 #pragma unroll 1
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t orr[32];

@@ -86,6 +86,11 @@ class Workload:
                                self.lse if lse else None, self.workspace(opts), stream, opts)
 
     def step(self, opts=None, stream=None):
+        """One serving iteration: fused append + attention (hg_hybrid_step)."""
+        hg.hg_hybrid_step(self.pool, self.batch, self.spec.H_q, self.q, self.k_new, self.v_new, self.out, self.lse,
+                          self.workspace(opts), stream, opts)
+
+    def step_unfused(self, opts=None, stream=None):
         self.append(stream)
         self.attention(opts, stream=stream)
 

@@ -241,7 +241,10 @@ def run_ours(args):
     if args.extra:
         line["extra"] = extra_configs(args, peaks, dev)
     if not args.profile and not args.no_predictor:
-        line["predictor"] = predictor_sweep(dev, iters=args.sweep_iters)
+        pred = predictor_sweep(dev, iters=args.sweep_iters)
+        model = pred.pop("_model")
+        line["predictor"] = pred
+        line["slo_loop"] = slo_loop(dev, model)
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -441,6 +444,8 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
         pred_us = (time.perf_counter() - t2) / len(te) * 1e6
         res[name] = {"mape_heldout": float(np.mean(np.abs(yh - y[te]) / y[te])), "train_mape": m.train_mape,
                      "fit_ms": fit_ms, "predict_us_python": pred_us, "w": list(m.w)}
+        if mask == hg.HG_MASK_ATTN:
+            res["_model"] = m
     # tokens/s versus mix (share of prefill tokens in the batch)
     pre = np.array(pre)
     mix = {}
@@ -451,6 +456,110 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
                                                  "tokens_per_s": float(np.sum(np.array(T)[sel]) / (np.sum(y[sel]) / 1e3))}
     res["tokens_per_s_vs_mix"] = mix
     return res
+
+
+def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8, 128)):
+    """NEXT-1 closed loop: HyGen's two-phase scheduling (Alg. 2 calls Alg. 1 for the
+    online then the offline phase) with hg_slo_aware_schedule over the
+    fitted predictor, on a bursty online trace + offline backlog (synth.trace
+    shapes); every composed batch runs through hg_hybrid_attention and its
+    measured kernel time is compared with the latency budget and the prediction."""
+    import math
+    import numpy as np
+    import torch
+    import paper_2501_14808_b200 as hg
+    from synth.configs import BatchSpec, Request
+    from synth.layout import make_layout
+    from synth.trace import BASE_QPS, ITER_S, PERIOD_S, _lognormal
+    rng = np.random.default_rng(seed)
+    B = 16
+    N = 40000
+    kc = torch.randn((N, H[1], B, H[2]), device=dev).to(torch.bfloat16)
+    vc = torch.randn((N, H[1], B, H[2]), device=dev).to(torch.bfloat16)
+    pool = hg.KVPool(kc, vc, N, B, H[1], H[2], dev.index)
+    q = torch.randn((4096, H[0], H[2]), device=dev).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+    online, offline = [], []   # [prompt, output, done_prompt, done_out, group, prefix]
+    t_sim, gid = rng.uniform(0, PERIOD_S), 0
+    rows = []
+    tok_on = tok_off = 0
+    for it in range(iters):
+        rate = 2.0 * BASE_QPS * (2.0 + math.sin(2 * math.pi * t_sim / PERIOD_S)) / 2.0
+        for _ in range(rng.poisson(rate * ITER_S)):
+            online.append([_lognormal(rng, 1024, 0.8, 32, 8192), _lognormal(rng, 128, 0.8, 1, 512), 0, 0, -1, 0])
+        while len(offline) < 64:
+            if rng.random() < 0.5:
+                for _ in range(32):
+                    offline.append([1024 + _lognormal(rng, 256, 0.8, 16, 2048), _lognormal(rng, 256, 0.8, 1, 512),
+                                    0, 0, gid, 1024])
+                gid += 1
+            else:
+                offline.append([_lognormal(rng, 6144, 0.5, 1024, 16384), _lognormal(rng, 256, 0.8, 1, 512), 0, 0, -1, 0])
+
+        def split(reqs):
+            run = [r for r in reqs if r[2] > 0]
+            que = [r for r in reqs if r[2] == 0]
+            f = lambda r: (r[2] + r[3], r[0] - r[2], r[5] if (r[4] >= 0 and r[2] >= r[5]) else 0, r[4])
+            return run, que, [f(r) for r in run], [f(r) for r in que]
+        entries = []
+        t, c, m = budget_ms, chunk, N // 2
+        for phase, reqs in ((True, online), (False, offline)):
+            run, que, rs, qs = split(reqs)
+            sched, t, c, m = hg.hg_slo_aware_schedule(model, rs, qs, t + (0.0 if phase else 0.0), c, m, phase)
+            t += model.w[0] if phase else 0.0   # the intercept is charged once per batch, in the first phase
+            for idx, l, tr in sched:
+                r = run[idx] if idx < len(run) else que[idx - len(run)]
+                entries.append((r, l, tr, phase))
+        if not entries:
+            t_sim += ITER_S
+            continue
+        reqs = []
+        for r, l, tr, phase in entries:
+            cached = r[2] + r[3]
+            share = r[4] >= 0 and r[2] >= r[5]
+            reqs.append(Request(cached, 1 if l == 0 else l, not phase, r[4], r[5], share=share))
+        spec = BatchSpec("slo", H[0], H[1], H[2], B, 0, reqs)
+        if spec.T > q.shape[0]:
+            continue
+        lay = make_layout(spec, seed=it, num_blocks=N)
+        b = hg.Batch(lay.block_table, [x.c for x in reqs], [x.n for x in reqs], None, lay.shared)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        flush.zero_()
+        hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, hg.make_opts(events=ev))
+        torch.cuda.synchronize()
+        st = hg.hg_last_plan_stats(pool)
+        first = 0 if st["tc_tiles"] else 2
+        last = 5 if st["combine_rows"] else 3 if st["splitk_items"] else 1
+        meas = ev[first].elapsed_time(ev[last])
+        pred = model.w[0] + sum(tr for _, _, tr, _ in entries)
+        rows.append((meas, pred))
+        for r, l, tr, phase in entries:
+            if l == 0:
+                r[3] += 1
+                if phase:
+                    tok_on += 1
+                else:
+                    tok_off += 1
+            else:
+                r[2] += l
+                if phase:
+                    tok_on += l
+                else:
+                    tok_off += l
+        online[:] = [r for r in online if r[3] < r[1]]
+        offline[:] = [r for r in offline if r[3] < r[1]]
+        t_sim += ITER_S
+    pool.close()
+    meas = np.array([r[0] for r in rows])
+    pred = np.array([r[1] for r in rows])
+    return {"iterations": len(rows), "budget_ms": budget_ms, "chunk_budget": chunk,
+            "within_budget_frac": float(np.mean(meas <= budget_ms)),
+            "p99_ms": float(np.percentile(meas, 99)), "mean_ms": float(meas.mean()),
+            "mape_pred_vs_measured": float(np.mean(np.abs(pred - meas) / meas)),
+            "online_tokens": tok_on, "offline_tokens": tok_off,
+            "note": "kernel-level analogue of the paper's SLO loop: budget = attention GPU time per iteration"}
 
 
 def run_tp(args, spec, rank, world, dev, peaks, peak_kind):

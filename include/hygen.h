@@ -250,6 +250,40 @@ HG_API hg_status hg_predictor_fit(const hg_features *X, const double *y_ms, int3
 /* w . [1, x], floored at 0. */
 HG_API double hg_predictor_predict(const hg_predictor *model, const hg_features *x);
 
+/* ------------------------------------------------------------------------ */
+/* SLO-aware batch composition (Alg. 1 SLO_AWARE_SCHEDULE)       */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t cached;               /* tokens already in the KV cache */
+    int32_t prompt_left;          /* prompt tokens not yet prefilled; 0 => the request decodes */
+    int32_t shared_prefix_tokens; /* tokens of a physically shared prefix (D_ctx counts it once per group) */
+    int32_t group;                /* shared-prefix group, -1 if none */
+} hg_sched_req;
+
+typedef struct {
+    int32_t index;  /* < n_running: running[index]; else queue[index - n_running] */
+    int32_t tokens; /* l of Alg. 1: 0 for a decode step, else the prefill chunk */
+    double t_req;   /* predicted marginal batch latency charged to the budget (ms) */
+} hg_sched_entry;
+
+/* One scheduling pass (online or offline phase) of Alg. 1 with the fitted
+ * predictor: running decodes first (admitted unconditionally when
+ * phase_online, else only while t_req <= t), then prefilling running requests
+ * and the queue in order, each given the largest chunk l that fits the
+ * remaining latency t, chunk c and memory m budgets (get_max_tokens, P:156;
+ * m decreases by GET_NUM_BLOCKS(l)); the first prefill that cannot be
+ * given a token ends the pass (preemption is not modelled, reading R21).
+ * t_req is the marginal increase of the batch prediction (clamped at 0); the
+ * model intercept is charged once (reading R19).  out must hold
+ * n_running + n_queue entries; *t_left / *c_left / *m_left (nullable) return
+ * the budgets left for the next phase (Alg. 2 runs the online then the
+ * offline phase). */
+HG_API hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t block_size, const hg_sched_req *running,
+                                       int32_t n_running, const hg_sched_req *queue, int32_t n_queue,
+                                       double latency_budget_ms, int32_t chunk_budget, int32_t memory_blocks,
+                                       int32_t phase_online, hg_sched_entry *out, int32_t *n_out, double *t_left,
+                                       int32_t *c_left, int32_t *m_left);
+
 #ifdef __cplusplus
 }
 #endif

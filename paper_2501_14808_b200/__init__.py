@@ -95,6 +95,7 @@ _SIGS = {
     "hg_batch_features": ([P, i32, P], i32),
     "hg_predictor_fit": ([P, P, i32, i32, P], i32),
     "hg_predictor_predict": ([P, P], ctypes.c_double),
+    "hg_slo_aware_schedule": ([P, i32, P, i32, P, i32, ctypes.c_double, i32, i32, i32, P, P, P, P, P], i32),
 }
 
 _LIB = None
@@ -368,3 +369,27 @@ def hg_predictor_predict(model: hg_predictor, x: hg_features) -> float:
 
 def features_from_array(a) -> hg_features:
     return hg_features(*[float(v) for v in a])
+
+
+# ---- SLO-aware scheduling (Alg. 1) ------------------------------------------------
+class hg_sched_req(ctypes.Structure):
+    _fields_ = [("cached", i32), ("prompt_left", i32), ("shared_prefix_tokens", i32), ("group", i32)]
+
+
+class hg_sched_entry(ctypes.Structure):
+    _fields_ = [("index", i32), ("tokens", i32), ("t_req", ctypes.c_double)]
+
+
+def hg_slo_aware_schedule(model: hg_predictor, running, queue, latency_budget_ms: float, chunk_budget: int,
+                          memory_blocks: int, phase_online: bool, block_size: int = 16):
+    """running / queue: sequences of (cached, prompt_left, shared_prefix_tokens, group).
+    Returns ([(index, tokens, t_req)], t_left, c_left, m_left)."""
+    R = (hg_sched_req * max(len(running), 1))(*[hg_sched_req(*r) for r in running])
+    Q = (hg_sched_req * max(len(queue), 1))(*[hg_sched_req(*r) for r in queue])
+    out = (hg_sched_entry * max(len(running) + len(queue), 1))()
+    n = ctypes.c_int32()
+    t, c, m = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().hg_slo_aware_schedule(ctypes.byref(model), block_size, R, len(running), Q, len(queue),
+                                       latency_budget_ms, chunk_budget, memory_blocks, int(phase_online), out,
+                                       ctypes.byref(n), ctypes.byref(t), ctypes.byref(c), ctypes.byref(m)))
+    return [(out[k].index, out[k].tokens, out[k].t_req) for k in range(n.value)], t.value, c.value, m.value

@@ -1,0 +1,132 @@
+// sched.cpp -- SLO_AWARE_SCHEDULE of HyGen Alg. 1 over the
+// fitted batch-latency predictor: the batch composer that
+// drives hg_hybrid_attention each iteration.
+//
+// Readings (R19-R21):
+//  * t_req of a request is its marginal batch-latency increase
+//    predict(B + r) - predict(B) under the linear model, clamped at 0; the
+//    intercept w[0] is charged once, before the first request (t <- t - w0).
+//  * get_max_tokens(t, c, m, r) = largest l <= min(c, prompt_left(r), m*B) whose
+//    marginal fits t (exact: binary search when the model is monotone in l,
+//    i.e. the S_p, S_p^2 and P2 weights are >= 0; a downward scan otherwise).
+//  * PERFORM_PREEMPTION is not modelled (preemption is out of scope): a prefill
+//    that does not fit ends the pass in both phases (Alg. 1's `break`).
+//  * Online decodes are admitted unconditionally and still decrement t.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "hg_internal.h"
+
+using namespace hg;
+
+namespace {
+struct Acc {   // batch features under construction, in the hg_features order
+    double f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+double lin(const hg_predictor &m, const double *f) {
+    double a = 0;
+    for (int k = 0; k < 8; ++k) a += m.w[1 + k] * f[k];
+    return a;
+}
+// features after adding one decode row of context c (shared prefix s_tok counted once per group)
+void add_decode(const Acc &a, int c, int s_tok_dup, double *out) {
+    for (int k = 0; k < 8; ++k) out[k] = a.f[k];
+    out[1] += 1;                                   // S_d
+    out[3] = out[1] * out[1];                      // S_d^2
+    out[5] += 1;                                   // N_d
+    out[7] += (double)(c + 1) - s_tok_dup;         // D_ctx (unique KV tokens)
+}
+void add_prefill(const Acc &a, int c, int l, double *out) {
+    for (int k = 0; k < 8; ++k) out[k] = a.f[k];
+    out[0] += l;                                   // S_p
+    out[2] = out[0] * out[0];                      // S_p^2
+    out[4] += 1;                                   // N_p
+    out[6] += (double)l * ((double)c + (double)(l + 1) / 2.0);  // P2
+}
+}  // namespace
+
+extern "C" hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t block_size, const hg_sched_req *running,
+                                           int32_t n_running, const hg_sched_req *queue, int32_t n_queue,
+                                           double t_budget, int32_t chunk_budget, int32_t memory_blocks,
+                                           int32_t phase_online, hg_sched_entry *out, int32_t *n_out, double *t_left,
+                                           int32_t *c_left, int32_t *m_left) {
+    if (!model || block_size < 1 || n_running < 0 || n_queue < 0 || (n_running && !running) || (n_queue && !queue) ||
+        !out || !n_out || chunk_budget < 0 || memory_blocks < 0)
+        return fail(HG_E_INVALID, "bad arguments");
+    const hg_predictor &M = *model;
+    double t = t_budget - M.w[0];   // the batch's fixed cost (intercept) is charged once
+    int64_t c = chunk_budget, m = memory_blocks;
+    int nb = 0;
+    Acc acc;
+    std::vector<int32_t> groups_in;   // shared-prefix groups that already have a decode row in B
+    double f[8];
+    auto marginal = [&](const double *fn) { return std::max(0.0, lin(M, fn) - lin(M, acc.f)); };
+    // ---- decodes of the running requests (Alg. 1 lines 6-13) ----
+    for (int i = 0; i < n_running; ++i) {
+        const hg_sched_req &r = running[i];
+        if (r.prompt_left > 0) continue;
+        int dup = 0;
+        if (r.group >= 0 && r.shared_prefix_tokens > 0 &&
+            std::find(groups_in.begin(), groups_in.end(), r.group) != groups_in.end())
+            dup = r.shared_prefix_tokens;
+        add_decode(acc, r.cached, dup, f);
+        const double t_req = marginal(f);
+        if (t_req <= t || phase_online) {
+            t -= t_req;
+            for (int k = 0; k < 8; ++k) acc.f[k] = f[k];
+            if (r.group >= 0 && r.shared_prefix_tokens > 0 && !dup) groups_in.push_back(r.group);
+            out[nb++] = hg_sched_entry{i, 0, t_req};
+        }
+    }
+    // ---- prefilling requests, then the queue (lines 14-33) ----
+    const bool monotone = M.w[1 + 0] >= 0 && M.w[1 + 2] >= 0 && M.w[1 + 6] >= 0;
+    const int n_all = n_running + n_queue;
+    for (int k = 0; k < n_all; ++k) {
+        const hg_sched_req &r = k < n_running ? running[k] : queue[k - n_running];
+        if (k < n_running && r.prompt_left <= 0) continue;   // decodes were handled above
+        if (r.prompt_left <= 0) continue;                    // a queued request with nothing to prefill
+        // get_max_tokens(t, c, m, r)
+        const int64_t hi = std::min<int64_t>(std::min<int64_t>(c, r.prompt_left), m * (int64_t)block_size);
+        auto fits = [&](int64_t l, double *t_req) {
+            add_prefill(acc, r.cached, (int)l, f);
+            *t_req = marginal(f);
+            return *t_req <= t;
+        };
+        int64_t l = 0;
+        double t_req = 0;
+        if (hi > 0) {
+            double tr;
+            if (fits(hi, &tr)) {
+                l = hi;
+                t_req = tr;
+            } else if (monotone) {
+                int64_t lo = 0, up = hi;   // fits(lo) (or lo == 0), !fits(up)
+                while (up - lo > 1) {
+                    const int64_t mid = (lo + up) / 2;
+                    if (fits(mid, &tr)) lo = mid; else up = mid;
+                }
+                l = lo;
+                if (l > 0) fits(l, &t_req);
+            } else {
+                for (int64_t cand = hi - 1; cand >= 1; --cand)
+                    if (fits(cand, &tr)) { l = cand; t_req = tr; break; }
+            }
+        }
+        if (l > 0) {
+            add_prefill(acc, r.cached, (int)l, f);
+            for (int q = 0; q < 8; ++q) acc.f[q] = f[q];
+            t -= t_req;
+            c -= l;
+            m -= hg_get_num_blocks((int32_t)l, block_size);   // GET_NUM_BLOCKS(l)
+            out[nb++] = hg_sched_entry{k, (int32_t)l, t_req};
+        } else {
+            break;   // (online: PERFORM_PREEMPTION + retry is out of scope, reading R21)
+        }
+    }
+    *n_out = nb;
+    if (t_left) *t_left = t;
+    if (c_left) *c_left = (int32_t)c;
+    if (m_left) *m_left = (int32_t)m;
+    return HG_OK;
+}

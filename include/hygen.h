@@ -284,6 +284,36 @@ HG_API hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t block_
                                        int32_t phase_online, hg_sched_entry *out, int32_t *n_out, double *t_left,
                                        int32_t *c_left, int32_t *m_left);
 
+/* ------------------------------------------------------------------------ */
+/* Prefix Sharing Maximization (§4.3; Alg. 3)           */
+/* ------------------------------------------------------------------------ */
+typedef struct hg_psm hg_psm; /* prefix tree T_p over offline prompts */
+HG_API hg_status hg_psm_create(hg_psm **out);
+HG_API hg_status hg_psm_destroy(hg_psm *psm);
+/* Insert request `request_id` (unique, >= 0) with its prompt tokens. */
+HG_API hg_status hg_psm_insert(hg_psm *psm, int32_t request_id, const int32_t *tokens, int32_t n);
+/* Remove a request (once scheduled).  HG_E_INVALID if absent. */
+HG_API hg_status hg_psm_remove(hg_psm *psm, int32_t request_id);
+HG_API int32_t hg_psm_size(const hg_psm *psm);
+/* The first `max` requests in DFS order of the tree (a node's own requests in
+ * insertion order, then its children in first-insertion order), and for each
+ * the length of the prefix it shares with its DFS predecessor (0 for the first)
+ * -- the shared-prefix length the attention kernel's prefix groups can reuse. */
+HG_API hg_status hg_psm_dfs_order(hg_psm *psm, int32_t *ids, int32_t *lcp_with_prev, int32_t max, int32_t *n_out);
+/* Alg. 3: running offline requests in order (a decode that does not fit the
+ * remaining budget ends the pass -- the inverted gate of P:550 read as
+ * `t < t_req => break`, reading R16; a prefill gets the largest fitting chunk or
+ * ends the pass), then new requests in the tree's DFS order, each given the
+ * largest fitting chunk (get_max_prefill) and removed from the tree.  by_id[k]
+ * describes tree request k (n_ids entries).  out entries index running[] for
+ * index < n_running, else request id + n_running.  Budgets and marginal
+ * latencies as in hg_slo_aware_schedule. */
+HG_API hg_status hg_psm_offline_schedule(const hg_predictor *model, int32_t block_size, hg_psm *psm,
+                                         const hg_sched_req *running, int32_t n_running, const hg_sched_req *by_id,
+                                         int32_t n_ids, double latency_budget_ms, int32_t chunk_budget,
+                                         int32_t memory_blocks, hg_sched_entry *out, int32_t *n_out, double *t_left,
+                                         int32_t *c_left, int32_t *m_left);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,13 @@ _SIGS = {
     "hg_predictor_fit": ([P, P, i32, i32, P], i32),
     "hg_predictor_predict": ([P, P], ctypes.c_double),
     "hg_slo_aware_schedule": ([P, i32, P, i32, P, i32, ctypes.c_double, i32, i32, i32, P, P, P, P, P], i32),
+    "hg_psm_create": ([P], i32),
+    "hg_psm_destroy": ([P], i32),
+    "hg_psm_insert": ([P, i32, P, i32], i32),
+    "hg_psm_remove": ([P, i32], i32),
+    "hg_psm_size": ([P], i32),
+    "hg_psm_dfs_order": ([P, P, P, i32, P], i32),
+    "hg_psm_offline_schedule": ([P, i32, P, P, i32, P, i32, ctypes.c_double, i32, i32, P, P, P, P, P], i32),
 }
 
 _LIB = None
@@ -392,4 +399,56 @@ def hg_slo_aware_schedule(model: hg_predictor, running, queue, latency_budget_ms
     _check(lib().hg_slo_aware_schedule(ctypes.byref(model), block_size, R, len(running), Q, len(queue),
                                        latency_budget_ms, chunk_budget, memory_blocks, int(phase_online), out,
                                        ctypes.byref(n), ctypes.byref(t), ctypes.byref(c), ctypes.byref(m)))
+    return [(out[k].index, out[k].tokens, out[k].t_req) for k in range(n.value)], t.value, c.value, m.value
+
+
+# ---- Prefix Sharing Maximization (Alg. 3) -----------------------------------------
+class PrefixTree:
+    """hg_psm: prefix tree T_p over offline prompts (DFS order = PSM admission order)."""
+
+    def __init__(self):
+        h = P()
+        _check(lib().hg_psm_create(ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().hg_psm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def hg_psm_insert(self, request_id: int, tokens) -> None:
+        a = np.ascontiguousarray(tokens, np.int32)
+        _check(lib().hg_psm_insert(self.h, request_id, _ptr(a) if a.size else None, int(a.size)))
+
+    def hg_psm_remove(self, request_id: int) -> None:
+        _check(lib().hg_psm_remove(self.h, request_id))
+
+    def hg_psm_size(self) -> int:
+        return int(lib().hg_psm_size(self.h))
+
+    def hg_psm_dfs_order(self, max_n: int = None):
+        n = self.hg_psm_size() if max_n is None else max_n
+        ids = np.zeros(max(n, 1), np.int32)
+        lcp = np.zeros(max(n, 1), np.int32)
+        k = ctypes.c_int32()
+        _check(lib().hg_psm_dfs_order(self.h, _ptr(ids), _ptr(lcp), n, ctypes.byref(k)))
+        return ids[:k.value].tolist(), lcp[:k.value].tolist()
+
+
+def hg_psm_offline_schedule(model: hg_predictor, tree: PrefixTree, running, by_id, latency_budget_ms: float,
+                            chunk_budget: int, memory_blocks: int, block_size: int = 16):
+    R = (hg_sched_req * max(len(running), 1))(*[hg_sched_req(*r) for r in running])
+    I = (hg_sched_req * max(len(by_id), 1))(*[hg_sched_req(*r) for r in by_id])
+    out = (hg_sched_entry * max(len(running) + len(by_id), 1))()
+    n = ctypes.c_int32()
+    t, c, m = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().hg_psm_offline_schedule(ctypes.byref(model), block_size, tree.h, R, len(running), I, len(by_id),
+                                         latency_budget_ms, chunk_budget, memory_blocks, out, ctypes.byref(n),
+                                         ctypes.byref(t), ctypes.byref(c), ctypes.byref(m)))
     return [(out[k].index, out[k].tokens, out[k].t_req) for k in range(n.value)], t.value, c.value, m.value

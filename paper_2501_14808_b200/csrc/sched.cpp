@@ -130,3 +130,102 @@ extern "C" hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t bl
     if (m_left) *m_left = (int32_t)m;
     return HG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Alg. 3 PREFIX_SHARING_OFFLINE_SCHEDULE: running offline requests
+// in their order (decode: stop at the first that does not fit -- reading R16
+// of the inverted `IF t > t_req THEN break`; prefill: largest fitting chunk or
+// stop), then new requests in the prefix tree's DFS order (T_p.get_next_request),
+// each removed from the tree once scheduled.
+// ---------------------------------------------------------------------------
+extern "C" hg_status hg_psm_offline_schedule(const hg_predictor *model, int32_t block_size, hg_psm *psm,
+                                             const hg_sched_req *running, int32_t n_running,
+                                             const hg_sched_req *by_id, int32_t n_ids, double t_budget,
+                                             int32_t chunk_budget, int32_t memory_blocks, hg_sched_entry *out,
+                                             int32_t *n_out, double *t_left, int32_t *c_left, int32_t *m_left) {
+    if (!model || !psm || block_size < 1 || n_running < 0 || (n_running && !running) || n_ids < 0 ||
+        (n_ids && !by_id) || !out || !n_out || chunk_budget < 0 || memory_blocks < 0)
+        return fail(HG_E_INVALID, "bad arguments");
+    const hg_predictor &M = *model;
+    double t = t_budget - M.w[0];
+    int64_t c = chunk_budget, m = memory_blocks;
+    int nb = 0;
+    Acc acc;
+    std::vector<int32_t> groups_in;
+    double f[8];
+    auto marginal = [&](const double *fn) { return std::max(0.0, lin(M, fn) - lin(M, acc.f)); };
+    const bool monotone = M.w[1 + 0] >= 0 && M.w[1 + 2] >= 0 && M.w[1 + 6] >= 0;
+    auto max_prefill = [&](const hg_sched_req &r, double *t_req) -> int64_t {
+        const int64_t hi = std::min<int64_t>(std::min<int64_t>(c, r.prompt_left), m * (int64_t)block_size);
+        double tr;
+        auto fits = [&](int64_t l) {
+            add_prefill(acc, r.cached, (int)l, f);
+            tr = marginal(f);
+            return tr <= t;
+        };
+        if (hi <= 0) return 0;
+        if (fits(hi)) { *t_req = tr; return hi; }
+        int64_t l = 0;
+        if (monotone) {
+            int64_t lo = 0, up = hi;
+            while (up - lo > 1) {
+                const int64_t mid = (lo + up) / 2;
+                if (fits(mid)) lo = mid; else up = mid;
+            }
+            l = lo;
+        } else {
+            for (int64_t cand = hi - 1; cand >= 1; --cand)
+                if (fits(cand)) { l = cand; break; }
+        }
+        if (l > 0) { fits(l); *t_req = tr; }
+        return l;
+    };
+    auto take_prefill = [&](const hg_sched_req &r, int64_t l, double t_req, int32_t index) {
+        add_prefill(acc, r.cached, (int)l, f);
+        for (int q = 0; q < 8; ++q) acc.f[q] = f[q];
+        t -= t_req;
+        c -= l;
+        m -= hg_get_num_blocks((int32_t)l, block_size);
+        out[nb++] = hg_sched_entry{index, (int32_t)l, t_req};
+    };
+    bool stopped = false;
+    for (int i = 0; i < n_running && !stopped; ++i) {
+        const hg_sched_req &r = running[i];
+        if (r.prompt_left <= 0) {
+            int dup = 0;
+            if (r.group >= 0 && r.shared_prefix_tokens > 0 &&
+                std::find(groups_in.begin(), groups_in.end(), r.group) != groups_in.end())
+                dup = r.shared_prefix_tokens;
+            add_decode(acc, r.cached, dup, f);
+            const double t_req = marginal(f);
+            if (t < t_req) { stopped = true; break; }
+            t -= t_req;
+            for (int q = 0; q < 8; ++q) acc.f[q] = f[q];
+            if (r.group >= 0 && r.shared_prefix_tokens > 0 && !dup) groups_in.push_back(r.group);
+            out[nb++] = hg_sched_entry{i, 0, t_req};
+        } else {
+            double t_req = 0;
+            const int64_t l = max_prefill(r, &t_req);
+            if (l > 0) take_prefill(r, l, t_req, i);
+            else stopped = true;
+        }
+    }
+    while (!stopped && hg_psm_size(psm) > 0) {
+        int32_t rid, n1 = 0;
+        hg_status s = hg_psm_dfs_order(psm, &rid, nullptr, 1, &n1);
+        if (s) return s;
+        if (n1 == 0) break;
+        if (rid < 0 || rid >= n_ids) return fail(HG_E_INVALID, "prefix-tree request %d has no entry in by_id", rid);
+        const hg_sched_req &r = by_id[rid];
+        double t_req = 0;
+        const int64_t l = max_prefill(r, &t_req);
+        if (l <= 0) break;
+        take_prefill(r, l, t_req, n_running + rid);
+        hg_psm_remove(psm, rid);
+    }
+    *n_out = nb;
+    if (t_left) *t_left = t;
+    if (c_left) *c_left = (int32_t)c;
+    if (m_left) *m_left = (int32_t)m;
+    return HG_OK;
+}

@@ -245,6 +245,7 @@ def run_ours(args):
         model = pred.pop("_model")
         line["predictor"] = pred
         line["slo_loop"] = slo_loop(dev, model)
+        line["psm_vs_fcfs"] = psm_vs_fcfs(dev)
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -560,6 +561,73 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
             "mape_pred_vs_measured": float(np.mean(np.abs(pred - meas) / meas)),
             "online_tokens": tok_on, "offline_tokens": tok_off,
             "note": "kernel-level analogue of the paper's SLO loop: budget = attention GPU time per iteration"}
+
+
+def psm_vs_fcfs(dev, groups=64, per_group=32, batch=128, H=(32, 8, 128), seed=0):
+    """NEXT-2 measured: MMLU-like offline backlog (groups of 32 sharing a 1024-token
+    prefix) admitted in arrival (FCFS) order vs the PSM prefix tree's DFS
+    order (hg_psm_dfs_order); consecutive batches of decodes run through
+    hg_hybrid_attention.  Reports unique KV bytes and attention tokens/s."""
+    import numpy as np
+    import torch
+    import paper_2501_14808_b200 as hg
+    from synth.configs import BatchSpec, Request
+    from synth.layout import make_layout
+    rng = np.random.default_rng(seed)
+    reqs = []   # (group, cached context, prompt tokens)
+    for g in range(groups):
+        prefix = list(rng.integers(0, 32000, 1024))
+        for _ in range(per_group):
+            suf = int(rng.integers(64, 512))
+            reqs.append((g, 1024 + suf + int(rng.integers(1, 256)), prefix + list(rng.integers(0, 32000, suf))))
+    arrival = list(rng.permutation(len(reqs)))
+    tree = hg.PrefixTree()
+    for rid in arrival:
+        tree.hg_psm_insert(int(rid), reqs[rid][2])
+    psm_order, _ = tree.hg_psm_dfs_order()
+    tree.close()
+    B = 16
+    need = max(sum(-(-(reqs[i][1] + 1) // B) for i in order[k:k + batch])
+               for order in (arrival, psm_order) for k in range(0, len(reqs), batch))
+    N = need + 64
+    kc = torch.randn((N, H[1], B, H[2]), device=dev).to(torch.bfloat16)
+    vc = torch.randn((N, H[1], B, H[2]), device=dev).to(torch.bfloat16)
+    pool = hg.KVPool(kc, vc, N, B, H[1], H[2], dev.index)
+    q = torch.randn((batch, H[0], H[2]), device=dev).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    res = {}
+    for name, order in (("fcfs", arrival), ("psm", psm_order)):
+        tot_ms, tot_tok, uniq = 0.0, 0, 0
+        for k in range(0, len(order), batch):
+            ids = order[k:k + batch]
+            cnt = {}
+            for i in ids:
+                cnt[reqs[i][0]] = cnt.get(reqs[i][0], 0) + 1
+            rr = [Request(reqs[i][1], 1, True, reqs[i][0], 1024, share=cnt[reqs[i][0]] > 1) for i in ids]
+            spec = BatchSpec(name, H[0], H[1], H[2], B, 0, rr)
+            lay = make_layout(spec, seed=k, num_blocks=N)
+            b = hg.Batch(lay.block_table, [r.c for r in rr], [1] * len(rr), None, lay.shared)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            times = []
+            for rep in range(3):
+                flush.zero_()
+                hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, hg.make_opts(events=ev))
+                torch.cuda.synchronize()
+                st = hg.hg_last_plan_stats(pool)
+                first = 0 if st["tc_tiles"] else 2
+                last = 5 if st["combine_rows"] else 3
+                times.append(ev[first].elapsed_time(ev[last]))
+            tot_ms += min(times)
+            tot_tok += len(rr)
+            uniq += st["kv_bytes_unique"]
+        res[name] = {"tokens_per_s": tot_tok / (tot_ms / 1e3), "attention_ms": tot_ms, "kv_bytes_unique": uniq}
+    pool.close()
+    res["speedup_psm_over_fcfs"] = res["psm"]["tokens_per_s"] / res["fcfs"]["tokens_per_s"]
+    res["kv_bytes_saved_frac"] = 1 - res["psm"]["kv_bytes_unique"] / res["fcfs"]["kv_bytes_unique"]
+    res["workload"] = f"{groups} groups x {per_group} decodes sharing 1024-token prefixes, batches of {batch}"
+    return res
 
 
 def run_tp(args, spec, rank, world, dev, peaks, peak_kind):

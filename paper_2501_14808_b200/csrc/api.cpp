@@ -363,6 +363,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.n_sk = (int32_t)plan.sk.size();
     p.n_tc = (int32_t)plan.tc.size();
     p.n_comb = (int32_t)plan.comb.size();
+    p.tc_ctas = plan.tc_ctas;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.d));
     p.trace = o ? (long long *)o->debug_trace : nullptr;
     int kernels = 0;

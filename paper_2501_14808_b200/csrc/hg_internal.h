@@ -82,6 +82,7 @@ struct AttnParams {
     float *part_lse;           // [slots] log2-domain LSE of each partial (-inf: empty)
     int32_t H_q, H_kv, G_q, d;
     int32_t n_sk, n_tc, n_comb;
+    int32_t tc_ctas;           // persistent tcgen05 grid (<= n_tc); 0: one CTA per item
     float scale_log2;          // log2(e) / sqrt(d)
     long long *trace;          // debug: per-event clock64 stamps of tcgen05 CTA 0 (NULL: off)
 };
@@ -102,6 +103,7 @@ struct Plan {
     int32_t prefix_tiles = 0;
     int64_t kv_bytes_unique = 0;
     int64_t kv_bytes_read = 0;
+    int32_t tc_ctas = 0;        // persistent tcgen05 grid chosen by the planner
     // device layout (byte offsets inside the workspace)
     size_t off_reqs = 0, off_bt = 0, off_sk = 0, off_tc = 0, off_rows = 0, off_cbase = 0,
            off_comb = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;

@@ -365,6 +365,12 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         }
     }
     p->kv_bytes_read = kv_tok_read * 4ll * d;
+    // Persistent tcgen05 grid: one CTA per SM at most (each needs the SM's whole
+    // shared memory); items beyond that are processed in LPT order by the same
+    // CTAs without re-initialising the pipeline.  (Confining the tiles to a few
+    // SMs beside the HBM-bound split-K kernel was measured slower: their K/V
+    // loads queue behind split-K's HBM traffic.)
+    p->tc_ctas = std::min((int)p->tc.size(), o.num_sms);
     lpt_sort(p->sk, p->sk_tmp);
     stream_sort(p->tc, p->tc_tmp);
 

@@ -265,7 +265,7 @@ struct TcSmem {
 };
 
 enum { BAR_KFULL = 0, BAR_KEMPTY = 3, BAR_VFULL = 6, BAR_VEMPTY = 8, BAR_SFULL = 10, BAR_PFULL = 12, BAR_ODONE = 14,
-       BAR_QREADY = 15, BAR_PHALF = 16, BAR_N = 18 };
+       BAR_QREADY = 15, BAR_PHALF = 16, BAR_OFREE = 18, BAR_N = 19 };
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -297,10 +297,12 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     auto bar = [&](int i) { return bars + 8u * i; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TcItem it = p.tc[blockIdx.x];
-    const int nkt = (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys;
-    const int ntiles = it.nrows > kTcRows ? 2 : 1;
-    long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;   // debug timeline (NULL: off)
+    // Persistent: CTA b processes items b, b + gridDim.x, ... (LPT-ordered by the
+    // planner).  Every role walks the same item sequence; barrier phases come
+    // from running counters, so the pipelines never drain between items.
+    long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;   // debug timeline of CTA 0's first item (NULL: off)
+    auto nkt_of = [&](const TcItem &it) { return (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys; };
+    auto ntiles_of = [&](const TcItem &it) { return it.nrows > kTcRows ? 2 : 1; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < L::kKStages; ++i) {
@@ -316,6 +318,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         }
         mbar_init(bar(BAR_ODONE), 1);
         mbar_init(bar(BAR_QREADY), 256);
+        mbar_init(bar(BAR_OFREE), 256);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 9) {  // TMEM: tile t: S/P at [256 t, 256 t + 128), O at [256 t + 128, 256 t + 128 + D)
@@ -334,41 +337,43 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         // ===================== TMA producers: warp 8 streams K, warp 10 streams V =====================
         // (separate threads so a V slot that is still busy never delays the next K load)
         if (lane == 0) {
-            const int32_t *bt = p.bt_flat + it.bt_off;
-            const int kb0 = it.k0 / kBlock;
-            const int kb_last = (it.k1 - 1) / kBlock;
-            auto rows_of = [&](int j, int *rows) {
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    int kb = kb0 + j * 8 + b;
-                    kb = kb <= kb_last ? kb : kb0;  // rows past k1 are masked; keep the data finite
-                    rows[b] = (bt[kb] * p.H_kv + it.g) * kBlock;
-                }
-            };
-            auto load = [&](const CUtensorMap *tm, uint32_t dst, uint32_t fb, const int *rows) {
-                mbar_expect_tx(fb, L::kKV);
-#pragma unroll
-                for (int b = 0; b < 8; ++b)
-#pragma unroll
-                    for (int h = 0; h < NH; ++h)
-                        tma_load_2d(dst + h * L::kHalf + b * (kBlock * 128), tm, h * 64, rows[b], fb);
-            };
-            if (warp == 8) {
-                for (int j = 0; j < nkt; ++j) {
-                    const int ks = j % L::kKStages;
-                    if (j >= L::kKStages) mbar_wait(bar(BAR_KEMPTY + ks), ((j / L::kKStages) - 1) & 1);
-                    if (tr && j < 64) tr[1024 + 2 * j] = clock64();
+            int64_t gn = 0;   // K (or V) tiles loaded by this CTA so far
+            for (int item = blockIdx.x; item < p.n_tc; item += gridDim.x) {
+                const TcItem it = p.tc[item];
+                const int nkt = nkt_of(it);
+                const int32_t *bt = p.bt_flat + it.bt_off;
+                const int kb0 = it.k0 / kBlock;
+                const int kb_last = (it.k1 - 1) / kBlock;
+                for (int j = 0; j < nkt; ++j, ++gn) {
                     int rows[8];
-                    rows_of(j, rows);
-                    load(&tmap_k, sK + ks * L::kKV, bar(BAR_KFULL + ks), rows);
-                }
-            } else {
-                for (int jv = 0; jv < nkt; ++jv) {
-                    const int vs = jv & 1;
-                    if (jv >= 2) mbar_wait(bar(BAR_VEMPTY + vs), ((jv >> 1) - 1) & 1);
-                    int rows[8];
-                    rows_of(jv, rows);
-                    load(&tmap_v, sV + vs * L::kKV, bar(BAR_VFULL + vs), rows);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        int kb = kb0 + j * 8 + b;
+                        kb = kb <= kb_last ? kb : kb0;  // rows past k1 are masked; keep the data finite
+                        rows[b] = (bt[kb] * p.H_kv + it.g) * kBlock;
+                    }
+                    uint32_t dst, fb;
+                    const CUtensorMap *tm;
+                    if (warp == 8) {
+                        const int st = (int)(gn % L::kKStages);
+                        if (gn >= L::kKStages) mbar_wait(bar(BAR_KEMPTY + st), ((gn / L::kKStages) - 1) & 1);
+                        if (tr && item == (int)blockIdx.x && j < 64) tr[1024 + 2 * j] = clock64();
+                        dst = sK + st * L::kKV;
+                        fb = bar(BAR_KFULL + st);
+                        tm = &tmap_k;
+                    } else {
+                        const int st = (int)(gn & 1);
+                        if (gn >= 2) mbar_wait(bar(BAR_VEMPTY + st), ((gn >> 1) - 1) & 1);
+                        dst = sV + st * L::kKV;
+                        fb = bar(BAR_VFULL + st);
+                        tm = &tmap_v;
+                    }
+                    mbar_expect_tx(fb, L::kKV);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+#pragma unroll
+                        for (int h = 0; h < NH; ++h)
+                            tma_load_2d(dst + h * L::kHalf + b * (kBlock * 128), tm, h * 64, rows[b], fb);
                 }
             }
         }
@@ -383,221 +388,254 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         const uint64_t dQ0 = smem_desc(sQ, 16, 1024);
         const uint64_t dK0 = smem_desc(sK, 16, 1024);
         const uint64_t dV0 = smem_desc(sV, L::kHalf, 1024);
-        mbar_wait(bar(BAR_QREADY), 0);
-        auto issue_qk = [&](int t, int j) {
-            const uint32_t tS = tmem + 256 * t;
-            const uint64_t dq = dQ0 + (uint64_t)((t * L::kQ) >> 4);
-            const uint64_t dk = dK0 + (uint64_t)(((j % L::kKStages) * L::kKV) >> 4);
-            if (elect_one()) {
+        int64_t gk = 0, gv = 0;          // K / V tiles consumed so far
+        int ps[2] = {0, 0};              // P steps consumed per Q tile
+        int n_item = 0;
+        for (int item = blockIdx.x; item < p.n_tc; item += gridDim.x, ++n_item) {
+            const TcItem it = p.tc[item];
+            const int nkt = nkt_of(it), ntiles = ntiles_of(it);
+            const bool trace = tr && item == (int)blockIdx.x;
+            auto issue_qk = [&](int t, int64_t kt, bool last_tile) {
+                const uint32_t tS = tmem + 256 * t;
+                const uint64_t dq = dQ0 + (uint64_t)((t * L::kQ) >> 4);
+                const uint64_t dk = dK0 + (uint64_t)(((kt % L::kKStages) * L::kKV) >> 4);
+                if (elect_one()) {
 #pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks) {
-                    constexpr int kh = L::kHalf;
-                    const uint32_t off = ((ks / 4) * kh + (ks % 4) * 32) >> 4;
-                    umma_bf16(tS, dq + off, dk + off, idS, ks > 0);
+                    for (int ks = 0; ks < D / 16; ++ks) {
+                        constexpr int kh = L::kHalf;
+                        const uint32_t off = ((ks / 4) * kh + (ks % 4) * 32) >> 4;
+                        umma_bf16(tS, dq + off, dk + off, idS, ks > 0);
+                    }
+                    umma_commit(bar(BAR_SFULL + t));
+                    if (last_tile) umma_commit(bar(BAR_KEMPTY + kt % L::kKStages));  // every QK read K(kt)
                 }
-                umma_commit(bar(BAR_SFULL + t));
-                if (t == ntiles - 1) umma_commit(bar(BAR_KEMPTY + j % L::kKStages));  // both QKs read K(j)
-            }
-            __syncwarp();
-        };
-        mbar_wait(bar(BAR_KFULL), 0);
-        tc_fence_after();
-        for (int t = 0; t < ntiles; ++t) issue_qk(t, 0);
-        for (int j = 0; j < nkt; ++j) {
-            const int s = j & 1;
-            const uint64_t dv = dV0 + (uint64_t)((s * L::kKV) >> 4);
-            for (int t = 0; t < ntiles; ++t) {
-                // PV in two halves: keys 0-63 as soon as the softmax has written them
-                mbar_wait(bar(BAR_PHALF + t), j & 1);
-                if (tr && j < 64 && lane == 0) tr[8 * j + 2 * t] = clock64();
-                if (t == 0) mbar_wait(bar(BAR_VFULL + s), (j >> 1) & 1);
+                __syncwarp();
+            };
+            mbar_wait(bar(BAR_QREADY), n_item & 1);
+            mbar_wait(bar(BAR_KFULL + gk % L::kKStages), (gk / L::kKStages) & 1);
+            tc_fence_after();
+            for (int t = 0; t < ntiles; ++t) issue_qk(t, gk, t == ntiles - 1);
+            if (n_item > 0) {   // the previous item's epilogue has read O out of TMEM
+                mbar_wait(bar(BAR_OFREE), (n_item - 1) & 1);
                 tc_fence_after();
-                const uint32_t tS = tmem + 256 * t, tO = tS + 128;
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    if (half == 1) {
-                        mbar_wait(bar(BAR_PFULL + t), j & 1);
-                        tc_fence_after();
-                    }
-                    if (elect_one()) {
-#pragma unroll
-                        for (int kk = 0; kk < kTcKeys / 32; ++kk) {   // P: 16 keys = 8 packed columns per k-step
-                            const int ks = half * (kTcKeys / 32) + kk;
-                            umma_bf16_ts(tO, tS + ks * 8, dv + (uint64_t)((ks * 2048) >> 4), idO, (j > 0 || ks > 0));
-                        }
-                    }
-                    __syncwarp();
-                }
-                if (j + 1 < nkt) {
-                    if (t == 0) {
-                        mbar_wait(bar(BAR_KFULL + (j + 1) % L::kKStages), ((j + 1) / L::kKStages) & 1);
-                        tc_fence_after();
-                    }
-                    issue_qk(t, j + 1);   // in-order after PV(t, j): overwrites S/P of tile t safely
-                }
-                if (tr && j < 64 && lane == 0) tr[8 * j + 2 * t + 1] = clock64();
             }
-            if (elect_one()) umma_commit(bar(BAR_VEMPTY + s));   // both PVs read V(j)
+            for (int j = 0; j < nkt; ++j, ++gk, ++gv) {
+                const int s = (int)(gv & 1);
+                const uint64_t dv = dV0 + (uint64_t)((s * L::kKV) >> 4);
+                for (int t = 0; t < ntiles; ++t) {
+                    // PV in two halves: keys 0-63 as soon as the softmax has written them
+                    mbar_wait(bar(BAR_PHALF + t), ps[t] & 1);
+                    if (trace && j < 64 && lane == 0) tr[8 * j + 2 * t] = clock64();
+                    if (t == 0) mbar_wait(bar(BAR_VFULL + s), (gv >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t tS = tmem + 256 * t, tO = tS + 128;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        if (half == 1) {
+                            mbar_wait(bar(BAR_PFULL + t), ps[t] & 1);
+                            tc_fence_after();
+                        }
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < kTcKeys / 32; ++kk) {   // P: 16 keys = 8 packed columns per k-step
+                                const int ks = half * (kTcKeys / 32) + kk;
+                                umma_bf16_ts(tO, tS + ks * 8, dv + (uint64_t)((ks * 2048) >> 4), idO,
+                                             (j > 0 || ks > 0));
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    ++ps[t];
+                    if (j + 1 < nkt) {
+                        if (t == 0) {
+                            mbar_wait(bar(BAR_KFULL + (gk + 1) % L::kKStages), ((gk + 1) / L::kKStages) & 1);
+                            tc_fence_after();
+                        }
+                        issue_qk(t, gk + 1, t == ntiles - 1);   // in order after PV(t, j): S/P of tile t is free
+                    }
+                    if (trace && j < 64 && lane == 0) tr[8 * j + 2 * t + 1] = clock64();
+                }
+                if (elect_one()) umma_commit(bar(BAR_VEMPTY + s));   // every PV read V(j)
+                __syncwarp();
+            }
+            if (elect_one()) umma_commit(bar(BAR_ODONE));
             __syncwarp();
         }
-        if (elect_one()) umma_commit(bar(BAR_ODONE));
-        __syncwarp();
     } else if (warp < 8) {
         // ===================== softmax / correction / epilogue (warps 0-7) =====================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
         const int t = warp >> 2;             // Q tile of this warpgroup
         const int r = threadIdx.x & 127;     // row in the tile == TMEM lane
         const int rr = t * kTcRows + r;      // stacked row of the item
-        const bool valid = rr < it.nrows;
-        struct { int t, h, lim; } row{0, 0, 0};
-        if (valid) {
-            const int x = it.hl0 + rr, j = x / p.G_q;
-            row.h = it.g * p.G_q + (x - j * p.G_q);
-            if (it.mode == 0) {
-                row.t = it.t0 + j;
-                row.lim = it.pos0 + j + 1;
-            } else {
-                row.t = p.tc_tok[it.t0 + j];
-                row.lim = it.k1;
-            }
-        }
-        // Q row -> smem, K-major 128B swizzle: half h, row r at h*16K + r*128, chunk c at (c ^ (r&7))*16
-        if (t < ntiles) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(p.q + ((int64_t)row.t * p.H_q + row.h) * D);
-            const uint32_t qb = sQ + t * L::kQ + r * 128;
-#pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
-                const uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
-                sts128(qb + (c >> 3) * L::kHalf + (((c & 7) ^ (r & 7)) << 4), v);
-            }
-            fence_async_smem();
-        }
-        mbar_arrive(bar(BAR_QREADY));
-        if (t < ntiles) {
-            const int lim = valid ? row.lim : 0;
-            const float sc = p.scale_log2;
-            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-            const uint32_t tS = tmem + 256 * t + lane_base, tO = tS + 128;
-            float m_used = -CUDART_INF_F;  // reference max (log2 domain) of the exponentials
-            float l_sum = 0.f;
-            for (int j = 0; j < nkt; ++j) {
-                mbar_wait(bar(BAR_SFULL + t), j & 1);   // QK(t, j) and everything before it (PV(t, j-1)) done
-                if (tr && r == 0 && j < 64) tr[512 + 256 * t + 2 * j] = clock64();
-                tc_fence_after();
-                uint32_t sr[128];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) TMEM_LD32(tS + c * 32, (&sr[c * 32]));
-                tmem_wait_ld();
-                const int kbase = it.k0 + j * kTcKeys;
-                if (kbase + kTcKeys > lim) {  // diagonal / tail tile: mask keys >= lim
-#pragma unroll
-                    for (int c = 0; c < 128; ++c)
-                        if (kbase + c >= lim) sr[c] = __float_as_uint(-CUDART_INF_F);
-                }
-                float mx[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) mx[e] = __uint_as_float(sr[e]);
-#pragma unroll
-                for (int c = 8; c < 128; ++c) mx[c & 7] = fmaxf(mx[c & 7], __uint_as_float(sr[c]));
-                const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-                const float mt = mraw * sc;   // scale > 0: max commutes with scaling
-                // lazy rescaling: move the reference only when the row max grew by > 2^8
-                const bool bump = mt > m_used + kRescaleThreshold;
-                float alpha = 1.f;
-                if (bump) {
-                    alpha = (m_used == -CUDART_INF_F) ? 0.f : ex2(m_used - mt);
-                    m_used = mt;
-                }
-                if (j > 0 && __any_sync(0xffffffffu, bump)) {  // O(t) is stable: PV(t, j-1) completed
-                    uint32_t orr[32];
-#pragma unroll 1
-                    for (int c = 0; c < D / 32; ++c) {
-                        TMEM_LD32(tO + c * 32, orr);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
-                        TMEM_ST32(tO + c * 32, orr);
-                    }
-                }
-                const float nref = (m_used == -CUDART_INF_F) ? 0.f : -m_used;
-                const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(nref, nref);
-                uint64_t ls2[2] = {0ull, 0ull};
-                uint32_t pk[64];
-#pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    if (c == 32) {   // first half of P (keys 0-63) -> TMEM: the MMA can start PV on it
-                        TMEM_ST32(tS, pk);
-                        tmem_wait_st();
-                        tc_fence_before();
-                        mbar_arrive(bar(BAR_PHALF + t));
-                    }
-                    const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
-                                              nref2);
-                    float a, b;
-                    if ((c & 3) == 3) {   // one pair in four on the FMA pipe, three on MUFU (FA4-style offload)
-                        exp2_poly2(x2, a, b);
-                    } else {
-                        float x0, x1;
-                        f2unpack(x2, x0, x1);
-                        a = ex2(x0);
-                        b = ex2(x1);
-                    }
-                    const uint64_t ab = f2pack(a, b);
-                    ls2[c & 1] = fadd2(ls2[c & 1], ab);
-                    pk[c] = pack2(a, b);
-                }
-                float l0, l1, l2, l3;
-                f2unpack(ls2[0], l0, l1);
-                f2unpack(ls2[1], l2, l3);
-                l_sum = l_sum * alpha + ((l0 + l1) + (l2 + l3));
-                // second half of P (bf16 pairs, keys 64-127) over S's columns 32-63 of this lane
-                TMEM_ST32(tS + 32, (&pk[32]));
-                tmem_wait_st();
-                tc_fence_before();
-                mbar_arrive(bar(BAR_PFULL + t));
-                if (tr && r == 0 && j < 64) tr[512 + 256 * t + 2 * j + 1] = clock64();
-            }
-            // ---- epilogue ----
-            mbar_wait(bar(BAR_ODONE), 0);
-            tc_fence_after();
-            const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-            const float lse2 = l_sum > 0.f ? m_used + __log2f(l_sum) : -CUDART_INF_F;
-            const int G = p.G_q;
-            int base = -1;
-            if (valid && it.part >= 0) {
-                const TokDev tk = p.tok[row.t];
-                base = tk.base + it.g * tk.nparts * G;   // + part * G + hl below
-            }
-#pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t orr[32];
-                TMEM_LD32(tO + c * 32, orr);
-                tmem_wait_ld();
-                if (!valid) continue;
-                if (it.part < 0) {
-                    uint4 *dst = reinterpret_cast<uint4 *>(p.out + ((int64_t)row.t * p.H_q + row.h) * D + c * 32);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        dst[e] = make_uint4(pack2(__uint_as_float(orr[8 * e + 0]) * inv, __uint_as_float(orr[8 * e + 1]) * inv),
-                                            pack2(__uint_as_float(orr[8 * e + 2]) * inv, __uint_as_float(orr[8 * e + 3]) * inv),
-                                            pack2(__uint_as_float(orr[8 * e + 4]) * inv, __uint_as_float(orr[8 * e + 5]) * inv),
-                                            pack2(__uint_as_float(orr[8 * e + 6]) * inv, __uint_as_float(orr[8 * e + 7]) * inv));
-                } else {
-                    const int64_t slot = base + (int64_t)it.part * G + (row.h % G);
-                    float4 *dst = reinterpret_cast<float4 *>(p.part_o + slot * D + c * 32);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        dst[e] = make_float4(__uint_as_float(orr[4 * e]) * inv, __uint_as_float(orr[4 * e + 1]) * inv,
-                                             __uint_as_float(orr[4 * e + 2]) * inv, __uint_as_float(orr[4 * e + 3]) * inv);
-                }
-            }
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + 256 * t + lane_base, tO = tS + 128;
+        const float sc = p.scale_log2;
+        int ss = 0;                          // S steps consumed by this Q tile
+        int n_item = 0;
+        for (int item = blockIdx.x; item < p.n_tc; item += gridDim.x, ++n_item) {
+            const TcItem it = p.tc[item];
+            const int nkt = nkt_of(it), ntiles = ntiles_of(it);
+            const bool trace = tr && item == (int)blockIdx.x;
+            const bool valid = rr < it.nrows;
+            struct { int t, h, lim; } row{0, 0, 0};
             if (valid) {
-                if (it.part < 0) {
-                    if (p.lse) p.lse[(int64_t)row.t * p.H_q + row.h] = lse2 * 0.69314718055994531f;
+                const int x = it.hl0 + rr, j = x / p.G_q;
+                row.h = it.g * p.G_q + (x - j * p.G_q);
+                if (it.mode == 0) {
+                    row.t = it.t0 + j;
+                    row.lim = it.pos0 + j + 1;
                 } else {
-                    p.part_lse[base + (int64_t)it.part * G + (row.h % G)] = lse2;
+                    row.t = p.tc_tok[it.t0 + j];
+                    row.lim = it.k1;
                 }
+            }
+            // Q row -> smem, K-major 128B swizzle: half h, row r at h*16K + r*128, chunk c at (c ^ (r&7))*16.
+            // The previous item's QKs are complete: this warpgroup waited its ODONE.
+            if (t < ntiles) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(p.q + ((int64_t)row.t * p.H_q + row.h) * D);
+                const uint32_t qb = sQ + t * L::kQ + r * 128;
+#pragma unroll
+                for (int c = 0; c < D / 8; ++c) {
+                    const uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
+                    sts128(qb + (c >> 3) * L::kHalf + (((c & 7) ^ (r & 7)) << 4), v);
+                }
+                fence_async_smem();
+            }
+            mbar_arrive(bar(BAR_QREADY));
+            if (t < ntiles) {
+                const int lim = valid ? row.lim : 0;
+                float m_used = -CUDART_INF_F;  // reference max (log2 domain) of the exponentials
+                float l_sum = 0.f;
+                for (int j = 0; j < nkt; ++j, ++ss) {
+                    mbar_wait(bar(BAR_SFULL + t), ss & 1);   // QK(t, j) and everything before it (PV(t, j-1)) done
+                    if (trace && r == 0 && j < 64) tr[512 + 256 * t + 2 * j] = clock64();
+                    tc_fence_after();
+                    uint32_t sr[128];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) TMEM_LD32(tS + c * 32, (&sr[c * 32]));
+                    tmem_wait_ld();
+                    const int kbase = it.k0 + j * kTcKeys;
+                    if (kbase + kTcKeys > lim) {  // diagonal / tail tile: mask keys >= lim
+#pragma unroll
+                        for (int c = 0; c < 128; ++c)
+                            if (kbase + c >= lim) sr[c] = __float_as_uint(-CUDART_INF_F);
+                    }
+                    float mx[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) mx[e] = __uint_as_float(sr[e]);
+#pragma unroll
+                    for (int c = 8; c < 128; ++c) mx[c & 7] = fmaxf(mx[c & 7], __uint_as_float(sr[c]));
+                    const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                             fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                    const float mt = mraw * sc;   // scale > 0: max commutes with scaling
+                    // lazy rescaling: move the reference only when the row max grew by > 2^8
+                    const bool bump = mt > m_used + kRescaleThreshold;
+                    float alpha = 1.f;
+                    if (bump) {
+                        alpha = (m_used == -CUDART_INF_F) ? 0.f : ex2(m_used - mt);
+                        m_used = mt;
+                    }
+                    if (j > 0 && __any_sync(0xffffffffu, bump)) {  // O(t) is stable: PV(t, j-1) completed
+                        uint32_t orr[32];
+#pragma unroll 1
+                        for (int c = 0; c < D / 32; ++c) {
+                            TMEM_LD32(tO + c * 32, orr);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+                            TMEM_ST32(tO + c * 32, orr);
+                        }
+                    }
+                    const float nref = (m_used == -CUDART_INF_F) ? 0.f : -m_used;
+                    const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(nref, nref);
+                    uint64_t ls2[2] = {0ull, 0ull};
+                    uint32_t pk[64];
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        if (c == 32) {   // first half of P (keys 0-63) -> TMEM: the MMA can start PV on it
+                            TMEM_ST32(tS, pk);
+                            tmem_wait_st();
+                            tc_fence_before();
+                            mbar_arrive(bar(BAR_PHALF + t));
+                        }
+                        const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
+                                                  sc2, nref2);
+                        float a, b;
+                        if ((c & 3) == 3) {   // one pair in four on the FMA pipe, three on MUFU (FA4-style offload)
+                            exp2_poly2(x2, a, b);
+                        } else {
+                            float x0, x1;
+                            f2unpack(x2, x0, x1);
+                            a = ex2(x0);
+                            b = ex2(x1);
+                        }
+                        const uint64_t ab = f2pack(a, b);
+                        ls2[c & 1] = fadd2(ls2[c & 1], ab);
+                        pk[c] = pack2(a, b);
+                    }
+                    float l0, l1, l2, l3;
+                    f2unpack(ls2[0], l0, l1);
+                    f2unpack(ls2[1], l2, l3);
+                    l_sum = l_sum * alpha + ((l0 + l1) + (l2 + l3));
+                    // second half of P (bf16 pairs, keys 64-127) over S's columns 32-63 of this lane
+                    TMEM_ST32(tS + 32, (&pk[32]));
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(bar(BAR_PFULL + t));
+                    if (trace && r == 0 && j < 64) tr[512 + 256 * t + 2 * j + 1] = clock64();
+                }
+                // ---- epilogue ----
+                mbar_wait(bar(BAR_ODONE), n_item & 1);
+                tc_fence_after();
+                const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+                const float lse2 = l_sum > 0.f ? m_used + __log2f(l_sum) : -CUDART_INF_F;
+                const int G = p.G_q;
+                int base = -1;
+                if (valid && it.part >= 0) {
+                    const TokDev tk = p.tok[row.t];
+                    base = tk.base + it.g * tk.nparts * G;   // + part * G + hl below
+                }
+#pragma unroll 1
+                for (int c = 0; c < D / 32; ++c) {
+                    uint32_t orr[32];
+                    TMEM_LD32(tO + c * 32, orr);
+                    tmem_wait_ld();
+                    if (c == D / 32 - 1) {   // O fully read: the next item's PV may overwrite it
+                        tc_fence_before();
+                        mbar_arrive(bar(BAR_OFREE));
+                    }
+                    if (!valid) continue;
+                    if (it.part < 0) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(p.out + ((int64_t)row.t * p.H_q + row.h) * D + c * 32);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            dst[e] = make_uint4(
+                                pack2(__uint_as_float(orr[8 * e + 0]) * inv, __uint_as_float(orr[8 * e + 1]) * inv),
+                                pack2(__uint_as_float(orr[8 * e + 2]) * inv, __uint_as_float(orr[8 * e + 3]) * inv),
+                                pack2(__uint_as_float(orr[8 * e + 4]) * inv, __uint_as_float(orr[8 * e + 5]) * inv),
+                                pack2(__uint_as_float(orr[8 * e + 6]) * inv, __uint_as_float(orr[8 * e + 7]) * inv));
+                    } else {
+                        const int64_t slot = base + (int64_t)it.part * G + (row.h % G);
+                        float4 *dst = reinterpret_cast<float4 *>(p.part_o + slot * D + c * 32);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            dst[e] = make_float4(__uint_as_float(orr[4 * e]) * inv, __uint_as_float(orr[4 * e + 1]) * inv,
+                                                 __uint_as_float(orr[4 * e + 2]) * inv,
+                                                 __uint_as_float(orr[4 * e + 3]) * inv);
+                    }
+                }
+                if (valid) {
+                    if (it.part < 0) {
+                        if (p.lse) p.lse[(int64_t)row.t * p.H_q + row.h] = lse2 * 0.69314718055994531f;
+                    } else {
+                        p.part_lse[base + (int64_t)it.part * G + (row.h % G)] = lse2;
+                    }
+                }
+            } else {
+                // an unused Q tile holds no O; stay in step with the item (QREADY / OFREE
+                // phases must not mix arrivals of different items)
+                mbar_wait(bar(BAR_ODONE), n_item & 1);
+                mbar_arrive(bar(BAR_OFREE));
             }
         }
     }
@@ -618,7 +656,8 @@ static hg_status launch_tc_d(const AttnParams &p, const void *tk, const void *tv
         if (e != cudaSuccess) return fail(HG_E_CUDA, "tc smem attribute: %s", cudaGetErrorString(e));
         attr = true;
     }
-    tc_attn_kernel<D><<<p.n_tc, kTcThreads, bytes, st>>>(p, *(const CUtensorMap *)tk, *(const CUtensorMap *)tv);
+    const int grid = std::max(1, std::min(p.n_tc, p.tc_ctas > 0 ? p.tc_ctas : p.n_tc));
+    tc_attn_kernel<D><<<grid, kTcThreads, bytes, st>>>(p, *(const CUtensorMap *)tk, *(const CUtensorMap *)tv);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "tcgen05 launch: %s", cudaGetErrorString(e));
 }

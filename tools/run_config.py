@@ -20,15 +20,16 @@ ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--no-tc", action="store_true")
 ap.add_argument("--no-prefix", action="store_true")
 ap.add_argument("--time", action="store_true")
+ap.add_argument("--split", type=int, default=0)
 a = ap.parse_args()
 spec = make_config(a.config, 0)
 wl = Workload(spec)
-opts = hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix)
+opts = hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split)
 for _ in range(2):
     wl.step(opts)
 torch.cuda.synchronize()
 ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(a.steps)]
-ops = [hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, events=e) for e in ev]
+ops = [hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split, events=e) for e in ev]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for k in range(a.steps):
     flush.zero_()
@@ -38,6 +39,6 @@ if a.time:
     st = hg.hg_last_plan_stats(wl.pool)
     for k in range(a.steps):
         e = ev[k]
-        print(a.config, "tc %.4f" % (e[0].elapsed_time(e[1]) if st["tc_tiles"] else 0),
+        print(a.config, "split", a.split, "tc %.4f" % (e[0].elapsed_time(e[1]) if st["tc_tiles"] else 0),
               "splitk %.4f" % (e[2].elapsed_time(e[3]) if st["splitk_items"] else 0),
               "comb %.4f" % (e[4].elapsed_time(e[5]) if st["combine_rows"] else 0), st)

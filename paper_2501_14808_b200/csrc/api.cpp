@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <vector>
@@ -394,24 +395,30 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         s = cuda_check(cudaEventRecord(pool->ev_fork, st), "fork record");
         if (s) return s;
     }
-    if (p.n_tc) {
+    auto do_tc = [&]() -> hg_status {
+        if (!p.n_tc) return HG_OK;
         rec(0, st);
-        s = launch_tc(p, pool->tmap_k, pool->tmap_v, st);
-        if (s) return s;
+        hg_status r = launch_tc(p, pool->tmap_k, pool->tmap_v, st);
+        if (r) return r;
         rec(1, st);
         ++kernels;
-    }
-    if (p.n_sk) {
+        return HG_OK;
+    };
+    auto do_sk = [&]() -> hg_status {
+        if (!p.n_sk) return HG_OK;
         if (overlap) {
-            s = cuda_check(cudaStreamWaitEvent(sk_stream, pool->ev_fork, 0), "fork wait");
-            if (s) return s;
+            hg_status r = cuda_check(cudaStreamWaitEvent(sk_stream, pool->ev_fork, 0), "fork wait");
+            if (r) return r;
         }
         rec(2, sk_stream);
-        s = launch_splitk(p, sk_stream);
-        if (s) return s;
+        hg_status r = launch_splitk(p, sk_stream);
+        if (r) return r;
         rec(3, sk_stream);
         ++kernels;
-    }
+        return HG_OK;
+    };
+    if ((s = do_tc())) return s;   // first: its CTAs are placed before split-K fills the SMs
+    if ((s = do_sk())) return s;
     if (overlap) {
         s = cuda_check(cudaEventRecord(pool->ev_join, sk_stream), "join record");
         if (s) return s;

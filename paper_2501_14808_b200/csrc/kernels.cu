@@ -136,8 +136,14 @@ __device__ __forceinline__ uint32_t swz(int row, int ch) {
 // ----------------------------------------------------------------------------
 // a.6 split-K attention item kernel
 // ----------------------------------------------------------------------------
-constexpr int kSkWarps = 4;
-constexpr int kSkStages = 2;
+#ifndef HG_SK_WARPS
+#define HG_SK_WARPS 4
+#endif
+#ifndef HG_SK_STAGES
+#define HG_SK_STAGES 2
+#endif
+constexpr int kSkWarps = HG_SK_WARPS;    // warps per split-K CTA (each streams its own blocks)
+constexpr int kSkStages = HG_SK_STAGES;  // cp.async stages per warp (one 16-token K+V block each)
 
 template <int D>
 struct SkSmem {
@@ -209,8 +215,11 @@ splitk_kernel(const AttnParams p) {
             cp_async16(dv + swz<D>(r, ch), gv + r * D + ch * 8);
         }
     };
-    if (nblk_w > 0) issue(0, 0);
-    cp_async_commit();
+#pragma unroll
+    for (int b = 0; b < kSkStages - 1; ++b) {   // prologue: blocks 0 .. S-2 in flight
+        if (b < nblk_w) issue(b, b);
+        cp_async_commit();
+    }
     __syncthreads();  // Q tile visible
 
     // Q A-fragments (all warps hold the same 16 x D tile)
@@ -232,10 +241,10 @@ splitk_kernel(const AttnParams p) {
     float l_a = 0.f, l_b = 0.f;                      // per-lane partial sums
 
     for (int bi = 0; bi < nblk_w; ++bi) {
-        const int stage = bi & 1;
-        if (bi + 1 < nblk_w) issue(bi + 1, stage ^ 1);
+        const int stage = bi % kSkStages;
+        if (bi + kSkStages - 1 < nblk_w) issue(bi + kSkStages - 1, (bi + kSkStages - 1) % kSkStages);
         cp_async_commit();
-        cp_async_wait<1>();
+        cp_async_wait<kSkStages - 1>();
         __syncwarp();
         const uint32_t sk = sW_u + stage * SkSmem<D>::kStage;
         const uint32_t sv = sk + SkSmem<D>::kTile;

@@ -515,10 +515,13 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     for (int c = 0; c < 4; ++c) TMEM_LD32(tS + c * 32, (&sr[c * 32]));
                     tmem_wait_ld();
                     const int kbase = it.k0 + j * kTcKeys;
-                    if (kbase + kTcKeys > lim) {  // diagonal / tail tile: mask keys >= lim
+                    // diagonal / tail tile: mask keys >= lim.  The branch is made
+                    // warp-uniform so full tiles skip the (if-converted) mask body.
+                    const int nvalid = lim - kbase;
+                    if (__any_sync(0xffffffffu, nvalid < kTcKeys)) {
 #pragma unroll
                         for (int c = 0; c < 128; ++c)
-                            if (kbase + c >= lim) sr[c] = __float_as_uint(-CUDART_INF_F);
+                            if (c >= nvalid) sr[c] = __float_as_uint(-CUDART_INF_F);
                     }
                     float mx[8];
 #pragma unroll

@@ -7,8 +7,10 @@ host plan (validation, indices, prefix tile map) + one descriptor H2D + KV appen
 + hybrid attention, through the C ABI's fused entry point hg_hybrid_step.
 The N=1 workload is BASELINE.json configs[1] (Llama-2-7B attention shape,
 512-token prefill chunk + 64 decodes at ctx 1-4K: "c1").  With --gpus N > 1
-(torchrun, one rank per GPU) KV heads are sharded across ranks and outputs are
-all-gathered with NCCL (hg_hybrid_attention_tp): total work fixed -> "strong".
+(torchrun, one rank per GPU) KV heads are sharded across ranks and the outputs
+are all-gathered by the attention epilogues themselves, storing into every
+rank's peer window over NVLink (hg_hybrid_attention_tp with an open window;
+NCCL is only the fallback): total work fixed -> "strong".
 
 --impl reference times the fp64 CPU oracle (oracle/, the only reference this
 paper-only task has) on the host cores, on a bounded sample of the same
@@ -631,7 +633,7 @@ def psm_vs_fcfs(dev, groups=64, per_group=32, batch=128, H=(32, 8, 128), seed=0)
 
 
 def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
-    """KV-head sharded attention on `world` GPUs + NCCL all-gather (strong scaling)."""
+    """KV-head sharded attention on `world` GPUs, all-gather fused via peer windows (strong scaling)."""
     import torch
     import torch.distributed as dist
     import paper_2501_14808_b200 as hg
@@ -644,7 +646,12 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     uid = [hg.hg_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = hg.Comm(uid[0], rank, world, dev.index)
-    out = torch.empty((spec.T, spec.H_q, spec.d), dtype=torch.bfloat16, device=dev)
+    # v2: a peer window per rank, mapped by every other rank (CUDA IPC over NVLink);
+    # the attention epilogues store straight into all ranks' windows
+    handles = [None] * world
+    dist.all_gather_object(handles, comm.hg_comm_window_create(spec.T * spec.H_q * spec.d * 2))
+    comm.hg_comm_window_open(handles)
+    out = comm.window((spec.T, spec.H_q, spec.d))
     ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q), dtype=torch.uint8,
                      device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -674,9 +681,9 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
             "metric": METRIC, "value": spec.T * args.steps / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "parallelism": f"kv-head tp{world} + NCCL all-gather",
+            "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "parallelism": f"kv-head tp{world}, all-gather fused into the epilogues (peer window)",
                        "l2": "KV working set 2.7 GB total > L2"},
-            "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 2) * args.steps,
+            "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 3) * args.steps,  # + append, 2 barriers
             "clocks": clk.summary(),
         }))
     comm.close()

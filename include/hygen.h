@@ -190,9 +190,31 @@ typedef struct hg_comm hg_comm;
 /* Writes a 128-byte NCCL unique id (rank 0 creates it; broadcast it with
  * torch.distributed).  HG_E_NCCL if libnccl.so.2 cannot be loaded. */
 HG_API hg_status hg_comm_unique_id(void *out_128_bytes);
+/* nccl_unique_id NULL: a communicator without NCCL, usable only through a
+ * peer window (below).  world <= 8. */
 HG_API hg_status hg_comm_init(const void *nccl_unique_id, int32_t rank, int32_t world, int32_t device,
                        hg_comm **out);
 HG_API hg_status hg_comm_destroy(hg_comm *comm);
+/* Peer window (SURVEY §8(e) "v2 fuses the gather"): a library-owned device
+ * buffer of `bytes` on every rank, mapped into every other rank with CUDA IPC
+ * (NVLink peer memory).  Once open, hg_hybrid_attention_tp makes every
+ * attention epilogue store its O rows straight into all ranks' windows at this
+ * rank's head offset of [T][H_q][d] -- the all-gather is done by the kernels,
+ * with no NCCL call and no transpose -- bracketed by two system-scope flag
+ * barriers (entry: no rank overwrites a window its owner may still be reading;
+ * exit: every rank's rows have landed).  The gathered O is then at *window_out;
+ * it is copied to out_gathered unless out_gathered == *window_out.  A rank that
+ * never reaches a barrier makes the others trap after ~30 s (HG_E_CUDA).
+ * Steps, collectively on every rank:
+ *   hg_comm_window_create(comm, bytes, handle, &win)  -> HG_IPC_HANDLE_BYTES opaque bytes
+ *   all-gather the handles (e.g. torch.distributed), rank-major [world][64]
+ *   hg_comm_window_open(comm, handles)
+ * Calls whose T*H_q*d*2 exceeds `bytes` fall back to the NCCL path (HG_E_INVALID
+ * if the communicator has none).  Readers of the window must be ordered before
+ * the next hg_hybrid_attention_tp on the same stream. */
+#define HG_IPC_HANDLE_BYTES 64
+HG_API hg_status hg_comm_window_create(hg_comm *comm, size_t bytes, void *ipc_handle_out, void **window_out);
+HG_API hg_status hg_comm_window_open(hg_comm *comm, const void *handles);
 /* Rank r holds KV heads [r*H_kv/G, (r+1)*H_kv/G) in `pool` and q-heads
  * [r*H_q/G, (r+1)*H_q/G) in q_local ([T][H_q/G][d]); every rank receives the
  * full out_gathered [T][H_q][d].  workspace must hold

@@ -90,6 +90,8 @@ _SIGS = {
     "hg_comm_unique_id": ([P], i32),
     "hg_comm_init": ([P, i32, i32, i32, P], i32),
     "hg_comm_destroy": ([P], i32),
+    "hg_comm_window_create": ([P, ctypes.c_size_t, P, P], i32),
+    "hg_comm_window_open": ([P, P], i32),
     "hg_hybrid_attention_tp_workspace_size": ([P, P, P, i32, P], i32),
     "hg_hybrid_attention_tp": ([P, P, P, i32, P, P, P, ctypes.c_size_t, P], i32),
     "hg_batch_features": ([P, i32, P], i32),
@@ -321,13 +323,51 @@ def hg_comm_unique_id() -> bytes:
     return bytes(buf)
 
 
+HG_IPC_HANDLE_BYTES = 64
+
+
+class _CudaBuf:
+    """Library-owned device bytes exposed through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, nbytes: int, device: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
 class Comm:
-    def __init__(self, uid: bytes, rank: int, world: int, device: int):
-        _preload_nccl()
-        buf = (ctypes.c_char * 128).from_buffer_copy(uid)
+    """hg_comm.  uid None: no NCCL communicator (peer-window only)."""
+
+    def __init__(self, uid: Optional[bytes], rank: int, world: int, device: int):
+        buf = None
+        if uid is not None:
+            _preload_nccl()
+            buf = (ctypes.c_char * 128).from_buffer_copy(uid)
         h = P()
         _check(lib().hg_comm_init(buf, rank, world, device, ctypes.byref(h)))
-        self.h, self.rank, self.world = h, rank, world
+        self.h, self.rank, self.world, self.device = h, rank, world, device
+        self.window_ptr = None
+
+    def hg_comm_window_create(self, nbytes: int) -> bytes:
+        """Allocates this rank's window; returns its IPC handle (to all-gather)."""
+        buf = (ctypes.c_char * HG_IPC_HANDLE_BYTES)()
+        ptr = P()
+        _check(lib().hg_comm_window_create(self.h, nbytes, buf, ctypes.byref(ptr)))
+        self.window_ptr = ptr.value
+        return bytes(buf)
+
+    def hg_comm_window_open(self, handles: Sequence[bytes]) -> None:
+        blob = b"".join(handles)
+        assert len(blob) == HG_IPC_HANDLE_BYTES * self.world
+        buf = (ctypes.c_char * len(blob)).from_buffer_copy(blob)
+        _check(lib().hg_comm_window_open(self.h, buf))
+
+    def window(self, shape, dtype=None):
+        """The gathered-output window as a torch tensor view (no copy)."""
+        import torch
+        dtype = dtype or torch.bfloat16
+        n = int(np.prod(shape))
+        holder = _CudaBuf(self.window_ptr, n * torch.empty((), dtype=dtype).element_size(), self.device)
+        return torch.as_tensor(holder, device=f"cuda:{self.device}").view(dtype).view(*shape)
 
     def close(self):
         if self.h:

@@ -311,9 +311,12 @@ extern "C" hg_status hg_hybrid_attention_workspace_size(const hg_kv_pool *pool, 
 
 // k_new / v_new non-NULL: fused step, the append kernel runs first from the same
 // descriptors (slots computed on the device).
+// outs non-NULL: O goes to every destination it lists (peer-window all-gather)
+// instead of `out`.
 static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, void *out,
                                 float *lse, void *ws, size_t ws_bytes, cudaStream_t st, const hg_attn_opts *o,
-                                bool fused = false, const void *k_new = nullptr, const void *v_new = nullptr) {
+                                bool fused = false, const void *k_new = nullptr, const void *v_new = nullptr,
+                                const OutSpec *outs = nullptr) {
     BatchView v;
     Plan &plan = pool->plan;
     hg_status s = plan_call(pool, batch, H_q, o, &v, &plan, fused);
@@ -324,7 +327,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         pool->last = hg_plan_stats{};
         return HG_OK;
     }
-    if (!q || !out) return fail(HG_E_INVALID, "q / out NULL");
+    if (!q || (!out && !outs)) return fail(HG_E_INVALID, "q / out NULL");
     if (fused && (!k_new || !v_new)) return fail(HG_E_INVALID, "k_new / v_new NULL");
     if (!ws || ws_bytes < plan.total_bytes)
         return fail(HG_E_INVALID, "workspace %zu bytes < required %zu", ws_bytes, plan.total_bytes);
@@ -346,7 +349,15 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.k_cache = (const uint16_t *)pool->desc.k_cache;
     p.v_cache = (const uint16_t *)pool->desc.v_cache;
     p.q = (const uint16_t *)q;
-    p.out = (uint16_t *)out;
+    if (outs) {
+        p.n_out = outs->n;
+        for (int k = 0; k < outs->n; ++k) p.outs[k] = outs->ptr[k];
+        p.out_ld = outs->ld;
+    } else {
+        p.n_out = 1;
+        p.outs[0] = (uint16_t *)out;
+        p.out_ld = (int64_t)H_q * pool->desc.head_dim;
+    }
     p.lse = lse;
     p.reqs = (const ReqDev *)(w + plan.off_reqs);
     p.bt_flat = (const int32_t *)(w + plan.off_bt);
@@ -442,6 +453,14 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     ls.kv_bytes_read = plan.kv_bytes_read;
     return HG_OK;
 }
+
+namespace hg {
+hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
+                       void *ws, size_t ws_bytes, void *stream) {
+    return attention_impl(pool, batch, H_q, q, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr, false,
+                          nullptr, nullptr, &outs);
+}
+}  // namespace hg
 
 extern "C" hg_status hg_hybrid_attention_ex(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
                                             const void *q, void *out, float *lse, void *workspace,

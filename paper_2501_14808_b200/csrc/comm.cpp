@@ -46,14 +46,25 @@ bool load_nccl() {
 }
 }  // namespace
 
+// Peer window: [flags: kMaxOuts x u64, padded to kWinHdr][data].  Every rank
+// maps every other rank's window through CUDA IPC (NVLink peer memory).
+constexpr size_t kWinHdr = 4096;
+
 struct hg_comm {
-    nccl_comm comm = nullptr;
+    nccl_comm comm = nullptr;   // NULL: peer-window-only communicator
     int rank = 0, world = 1, device = 0;
+    uint8_t *win = nullptr;     // this rank's window (cudaMalloc, library-owned)
+    size_t win_bytes = 0;       // data bytes
+    uint8_t *peer[hg::kMaxOuts] = {};   // window bases of every rank (self = win)
+    bool open = false;
+    unsigned long long epoch = 0;
 };
 
 using namespace hg;
 
 namespace hg {
+hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
+                              unsigned long long epoch, void *stream);
 hg_status launch_gather_transpose(const uint16_t *src, uint16_t *dst, int G, int T, int row_elems, void *stream);
 int pool_num_kv_heads(const hg_kv_pool *p);
 int pool_head_dim(const hg_kv_pool *p);
@@ -70,16 +81,19 @@ extern "C" hg_status hg_comm_unique_id(void *out) {
 }
 
 extern "C" hg_status hg_comm_init(const void *uid, int32_t rank, int32_t world, int32_t device, hg_comm **out) {
-    if (!uid || !out || world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "bad arguments");
-    if (!load_nccl()) return fail(HG_E_NCCL, "libnccl.so.2 not loadable (set HG_NCCL_PATH)");
+    if (!out || world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "bad arguments");
+    if (world > kMaxOuts) return fail(HG_E_INVALID, "world %d > %d", world, kMaxOuts);
+    if (uid && !load_nccl()) return fail(HG_E_NCCL, "libnccl.so.2 not loadable (set HG_NCCL_PATH)");
     if (cudaSetDevice(device) != cudaSuccess) return fail(HG_E_CUDA, "cudaSetDevice(%d)", device);
-    nccl_uid id;
-    memcpy(id.internal, uid, 128);
     hg_comm *c = new hg_comm();
-    nccl_result r = g_nccl.CommInitRank(&c->comm, world, id, rank);
-    if (r) {
-        delete c;
-        return fail(HG_E_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+    if (uid) {
+        nccl_uid id;
+        memcpy(id.internal, uid, 128);
+        nccl_result r = g_nccl.CommInitRank(&c->comm, world, id, rank);
+        if (r) {
+            delete c;
+            return fail(HG_E_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+        }
     }
     c->rank = rank;
     c->world = world;
@@ -91,7 +105,64 @@ extern "C" hg_status hg_comm_init(const void *uid, int32_t rank, int32_t world, 
 extern "C" hg_status hg_comm_destroy(hg_comm *c) {
     if (!c) return HG_OK;
     if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+    cudaSetDevice(c->device);
+    for (int k = 0; k < c->world; ++k)
+        if (c->peer[k] && c->peer[k] != c->win) cudaIpcCloseMemHandle(c->peer[k]);
+    if (c->win) cudaFree(c->win);
+    cudaGetLastError();
     delete c;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_comm_window_create(hg_comm *c, size_t bytes, void *ipc_handle_out, void **window_out) {
+    if (!c || !ipc_handle_out || !window_out || bytes == 0) return fail(HG_E_INVALID, "bad arguments");
+    if (c->win) return fail(HG_E_INVALID, "window already created");
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(HG_E_CUDA, "cudaSetDevice(%d)", c->device);
+    const size_t total = kWinHdr + (bytes + 255) / 256 * 256;
+    if (cudaMalloc(&c->win, total) != cudaSuccess) {
+        cudaGetLastError();
+        c->win = nullptr;
+        return fail(HG_E_OOM, "window of %zu bytes", total);
+    }
+    cudaIpcMemHandle_t h;
+    if (cudaMemset(c->win, 0, kWinHdr) != cudaSuccess || cudaIpcGetMemHandle(&h, c->win) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        cudaError_t e = cudaGetLastError();
+        cudaFree(c->win);
+        c->win = nullptr;
+        return fail(HG_E_CUDA, "window setup: %s", cudaGetErrorString(e));
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == HG_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(ipc_handle_out, &h, sizeof h);
+    c->win_bytes = bytes;
+    *window_out = c->win + kWinHdr;
+    return HG_OK;
+}
+
+extern "C" hg_status hg_comm_window_open(hg_comm *c, const void *handles) {
+    if (!c || !handles) return fail(HG_E_INVALID, "bad arguments");
+    if (!c->win) return fail(HG_E_INVALID, "hg_comm_window_create first");
+    if (c->open) return fail(HG_E_INVALID, "window already open");
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(HG_E_CUDA, "cudaSetDevice(%d)", c->device);
+    for (int k = 0; k < c->world; ++k) {
+        if (k == c->rank) {
+            c->peer[k] = c->win;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const uint8_t *)handles + (size_t)k * HG_IPC_HANDLE_BYTES, sizeof h);
+        void *ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            for (int j = 0; j < k; ++j)
+                if (c->peer[j] && c->peer[j] != c->win) cudaIpcCloseMemHandle(c->peer[j]);
+            memset(c->peer, 0, sizeof c->peer);
+            return fail(HG_E_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", k, cudaGetErrorString(e));
+        }
+        c->peer[k] = (uint8_t *)ptr;
+    }
+    c->open = true;
     return HG_OK;
 }
 
@@ -124,6 +195,35 @@ extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, con
     size_t attn = 0;
     s = hg_hybrid_attention_workspace_size(pool, batch, Hl, &attn);
     if (s) return s;
+    const size_t out_bytes = (size_t)T * H_q * d * 2;
+    if (comm->open && out_bytes <= comm->win_bytes) {
+        // v2: every epilogue stores its O rows into all ranks' windows, at this
+        // rank's head offset of the gathered [T][H_q][d] layout.  Entry barrier:
+        // no rank overwrites a window its owner may still read from the last call.
+        if (T == 0) return HG_OK;
+        unsigned long long *fl[kMaxOuts];
+        for (int k = 0; k < G; ++k) fl[k] = (unsigned long long *)comm->peer[k];
+        unsigned long long *mine = (unsigned long long *)comm->win;
+        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
+        if (s) return s;
+        OutSpec os;
+        os.n = G;
+        os.ld = (int64_t)H_q * d;
+        for (int k = 0; k < G; ++k) os.ptr[k] = (uint16_t *)(comm->peer[k] + kWinHdr) + (size_t)comm->rank * Hl * d;
+        s = attention_to(pool, batch, Hl, q_local, os, workspace, attn, stream);
+        if (s) return s;
+        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
+        if (s) return s;
+        uint8_t *data = comm->win + kWinHdr;
+        if (out_gathered != data) {
+            cudaError_t e = cudaMemcpyAsync(out_gathered, data, out_bytes, cudaMemcpyDeviceToDevice,
+                                            (cudaStream_t)stream);
+            if (e != cudaSuccess) return fail(HG_E_CUDA, "window copy: %s", cudaGetErrorString(e));
+        }
+        return HG_OK;
+    }
+    if (!comm->comm && G > 1) return fail(HG_E_INVALID, "no NCCL communicator and no open window of %zu bytes",
+                                          out_bytes);
     uint8_t *w = (uint8_t *)workspace;
     uint16_t *gather = (uint16_t *)(w + al256(attn));  // [G][T][Hl][d], rank-major (NCCL layout)
     const size_t count = (size_t)T * Hl * d;

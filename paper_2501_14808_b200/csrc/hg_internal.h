@@ -14,6 +14,7 @@ constexpr int kBlock = 16;        // KV block size B handled by the kernels
 constexpr int kSkRows = 16;       // query rows per split-K item (one m16 MMA tile)
 constexpr int kTcRows = 128;      // query rows per tcgen05 tile (UMMA M)
 constexpr int kTcKeys = 128;      // keys per tcgen05 KV tile (UMMA N of S = Q K^T)
+constexpr int kMaxOuts = 8;       // O copies one launch writes (ranks of a peer window)
 
 // Per-request record in the device descriptor.
 struct ReqDev {
@@ -69,7 +70,13 @@ struct AttnParams {
     const uint16_t *k_cache;
     const uint16_t *v_cache;
     const uint16_t *q;
-    uint16_t *out;
+    // O destinations: element (t, h, :) of every copy lives at outs[k] + t*out_ld + h*d.
+    // One copy on a single GPU; under KV-head sharding with a peer window, one per
+    // rank (NVLink peer pointers, already offset to this rank's head slice), so the
+    // epilogues do the all-gather themselves.
+    uint16_t *outs[kMaxOuts];
+    int32_t n_out;
+    int64_t out_ld;
     float *lse;
     const ReqDev *reqs;
     const int32_t *bt_flat;
@@ -135,6 +142,15 @@ struct PlanOpts {
     int num_sms = 148;
 };
 hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpts &o, Plan *p);
+
+// O destinations of one attention call (AttnParams::outs).
+struct OutSpec {
+    int n = 0;
+    uint16_t *ptr[kMaxOuts] = {};
+    int64_t ld = 0;   // elements between token rows
+};
+hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
+                       void *ws, size_t ws_bytes, void *stream);
 
 // ---- kernel launchers (kernels.cu / tc_attn.cu) -----------------------------
 hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache,

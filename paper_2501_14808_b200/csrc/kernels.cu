@@ -378,7 +378,7 @@ splitk_kernel(const AttnParams p) {
             }
             const float lse2 = (L > 0.f) ? ref + __log2f(L) : -CUDART_INF_F;
             if (base < 0) {
-                uint16_t *dst = p.out + ((int64_t)t * p.H_q + h) * D + part8 * PER;
+                const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + part8 * PER;
 #pragma unroll
                 for (int e = 0; e < PER; e += 8) {
                     uint4 v;
@@ -386,7 +386,7 @@ splitk_kernel(const AttnParams p) {
                     v.y = pack_bf16(acc[e + 2], acc[e + 3]);
                     v.z = pack_bf16(acc[e + 4], acc[e + 5]);
                     v.w = pack_bf16(acc[e + 6], acc[e + 7]);
-                    *reinterpret_cast<uint4 *>(dst + e) = v;
+                    for (int k = 0; k < p.n_out; ++k) *reinterpret_cast<uint4 *>(p.outs[k] + off + e) = v;
                 }
                 if (p.lse && part8 == 0) p.lse[(int64_t)t * p.H_q + h] = lse2 * 0.69314718055994531f;
             } else {
@@ -458,9 +458,14 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
         }
     }
     const int h = g * G + hl;
-    uint16_t *dst = p.out + ((int64_t)t * p.H_q + h) * D + lane * PER;
+    const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + lane * PER;
+    uint32_t pk[PER / 2];
 #pragma unroll
-    for (int e = 0; e < PER; e += 2) *reinterpret_cast<uint32_t *>(dst + e) = pack_bf16(acc[e], acc[e + 1]);
+    for (int e = 0; e < PER; e += 2) pk[e / 2] = pack_bf16(acc[e], acc[e + 1]);
+    for (int k = 0; k < p.n_out; ++k) {
+#pragma unroll
+        for (int e = 0; e < PER / 2; ++e) reinterpret_cast<uint32_t *>(p.outs[k] + off)[e] = pk[e];
+    }
     if (p.lse && lane == 0)
         p.lse[(int64_t)t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
 }
@@ -500,5 +505,44 @@ hg_status launch_gather_transpose(const uint16_t *src, uint16_t *dst, int G, int
     gather_transpose_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)src, (uint4 *)dst, G, T, chunks);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "transpose launch: %s", cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Peer-window barrier.  Thread k (< world) publishes `epoch`
+// into rank k's flag slot [rank] with a system-scope release store, then waits
+// (acquire) until rank k's own arrival shows up in the local slot [k].  Flags
+// only grow, so no reset is needed.  Kernels earlier in the stream have
+// completed, so their peer stores precede the release.  A peer that never
+// arrives is a broken job: after ~30 s the kernel traps (sticky HG_E_CUDA)
+// instead of hanging the GPU.
+// ---------------------------------------------------------------------------
+struct PeerFlags {
+    unsigned long long *flags[kMaxOuts];  // flags[k]: rank k's flag array (peer mapping)
+};
+
+__global__ void peer_barrier_kernel(PeerFlags pf, unsigned long long *mine, int rank, int world,
+                                    unsigned long long epoch) {
+    const int k = threadIdx.x;
+    if (k >= world) return;
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(pf.flags[k] + rank), "l"(epoch) : "memory");
+    unsigned long long t0, now, v;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine + k) : "memory");
+        if (v >= epoch) break;
+        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
+        if (now - t0 > 30000000000ull) __trap();
+        __nanosleep(256);
+    }
+}
+
+hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
+                              unsigned long long epoch, void *stream) {
+    PeerFlags pf{};
+    for (int k = 0; k < world; ++k) pf.flags[k] = flags[k];
+    peer_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(pf, mine, rank, world, epoch);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "peer barrier launch: %s", cudaGetErrorString(e));
 }
 }  // namespace hg

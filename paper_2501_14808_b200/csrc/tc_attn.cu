@@ -609,14 +609,20 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     }
                     if (!valid) continue;
                     if (it.part < 0) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(p.out + ((int64_t)row.t * p.H_q + row.h) * D + c * 32);
+                        const int64_t off = (int64_t)row.t * p.out_ld + (int64_t)row.h * D + c * 32;
+                        uint4 v[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
-                            dst[e] = make_uint4(
+                            v[e] = make_uint4(
                                 pack2(__uint_as_float(orr[8 * e + 0]) * inv, __uint_as_float(orr[8 * e + 1]) * inv),
                                 pack2(__uint_as_float(orr[8 * e + 2]) * inv, __uint_as_float(orr[8 * e + 3]) * inv),
                                 pack2(__uint_as_float(orr[8 * e + 4]) * inv, __uint_as_float(orr[8 * e + 5]) * inv),
                                 pack2(__uint_as_float(orr[8 * e + 6]) * inv, __uint_as_float(orr[8 * e + 7]) * inv));
+                        for (int k = 0; k < p.n_out; ++k) {
+                            uint4 *dst = reinterpret_cast<uint4 *>(p.outs[k] + off);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) dst[e] = v[e];
+                        }
                     } else {
                         const int64_t slot = base + (int64_t)it.part * G + (row.h % G);
                         float4 *dst = reinterpret_cast<float4 *>(p.part_o + slot * D + c * 32);

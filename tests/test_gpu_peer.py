@@ -1,0 +1,170 @@
+"""KV-head sharding with the fused peer-window all-gather.
+
+gpurun offers one GPU, so the multi-rank case runs two processes on the SAME
+device: CUDA IPC maps each process's window into the other exactly as it would
+across NVLink, the epilogues store into both windows, and the system-scope flag
+barriers order them.  The transport must be exact: every rank's slice of the
+gathered output is bit-identical to that slice computed alone (same plan, same
+kernels, only the destination pointers differ).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _slice_inputs(wl, spec, world, r):
+    """Rank r's KV heads of the populated pool and its q heads (contiguous copies)."""
+    Hk, Hq = spec.H_kv // world, spec.H_q // world
+    k = wl.k_cache[:, r * Hk:(r + 1) * Hk].contiguous()
+    v = wl.v_cache[:, r * Hk:(r + 1) * Hk].contiguous()
+    q = wl.q[:, r * Hq:(r + 1) * Hq].contiguous()
+    return k, v, q
+
+
+def _reference_slices(hg, wl, spec, world, dev):
+    """Each rank's O slice computed alone with hg_hybrid_attention."""
+    outs = []
+    for r in range(world):
+        k, v, q = _slice_inputs(wl, spec, world, r)
+        pool = hg.KVPool(k, v, wl.lay.num_blocks, spec.B, spec.H_kv // world, spec.d, dev)
+        o = torch.empty((spec.T, spec.H_q // world, spec.d), dtype=torch.bfloat16, device="cuda")
+        ws = torch.empty(hg.hg_hybrid_attention_workspace_size(pool, wl.batch, spec.H_q // world) + (1 << 20),
+                         dtype=torch.uint8, device="cuda")
+        hg.hg_hybrid_attention(pool, wl.batch, spec.H_q // world, q, o, None, ws)
+        torch.cuda.synchronize()
+        pool.close()
+        outs.append(o)
+    return torch.cat(outs, dim=1)
+
+
+def _spec(name):
+    from synth.configs import make_config, make_fuzz
+    if name.startswith("fuzz"):
+        return make_fuzz(int(name[4:]), H_kv=2, G_q=4)
+    return make_config(name, 0)
+
+
+@pytest.mark.parametrize("zero_copy", [False, True])
+def test_window_world1(zero_copy):
+    """1-rank peer-only communicator: the window path equals the plain call bit for bit."""
+    _cuda()
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    spec = _spec("toy_b")
+    wl = Workload(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    dev = torch.cuda.current_device()
+    comm = hg.Comm(None, 0, 1, dev)
+    h = comm.hg_comm_window_create(spec.T * spec.H_q * spec.d * 2)
+    comm.hg_comm_window_open([h])
+    ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q),
+                     dtype=torch.uint8, device="cuda")
+    win = comm.window((spec.T, spec.H_q, spec.d))
+    out = win if zero_copy else torch.empty_like(wl.out)
+    for _ in range(3):   # epochs advance; flags only grow
+        out.fill_(0)
+        hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, out, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), wl.out.view(torch.int16))
+    comm.close()
+
+
+def test_peer_only_comm_without_window_rejects_world2():
+    _cuda()
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    spec = _spec("toy_b")
+    wl = Workload(spec)
+    comm = hg.Comm(None, 0, 2, torch.cuda.current_device())
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(wl.out)
+    with pytest.raises(hg.HgError) as e:
+        hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q[:, :spec.H_q // 2].contiguous(), out, ws)
+    assert e.value.status == hg.HG_E_INVALID
+    comm.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, names, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2501_14808_b200 as hg
+        from paper_2501_14808_b200.harness import Workload
+        torch.cuda.set_device(0)
+        dev = 0
+        comm = hg.Comm(None, rank, world, dev)
+        cap = 1 << 24
+        h = comm.hg_comm_window_create(cap)
+        hs = [None] * world
+        dist.all_gather_object(hs, h)
+        comm.hg_comm_window_open(hs)
+        res = []
+        for name in names:
+            spec = _spec(name)
+            wl = Workload(spec)          # same seeded values in every process
+            ref = _reference_slices(hg, wl, spec, world, dev)
+            k, v, ql = _slice_inputs(wl, spec, world, rank)
+            pool = hg.KVPool(k, v, wl.lay.num_blocks, spec.B, spec.H_kv // world, spec.d, dev)
+            ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(pool, comm, wl.batch, spec.H_q),
+                             dtype=torch.uint8, device="cuda")
+            for it in range(3):
+                zero_copy = it == 1
+                out = comm.window((spec.T, spec.H_q, spec.d)) if zero_copy else \
+                    torch.full((spec.T, spec.H_q, spec.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+                hg.hg_hybrid_attention_tp(pool, comm, wl.batch, spec.H_q, ql, out, ws)
+                torch.cuda.synchronize()
+                ok = torch.equal(out.view(torch.int16), ref.view(torch.int16))
+                res.append((name, it, bool(ok)))
+                dist.barrier()            # readers of the window finish before the next call
+            pool.close()
+        comm.close()
+        q.put((rank, res, None))
+    except Exception as e:  # report, do not hang the peer
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_same_gpu_peer_window():
+    _cuda()
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    names = ["toy_b", "fuzz0", "fuzz3", "fuzz7", "c2_g8"]
+    port = _free_port()
+    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, names, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in ps:
+        rank, res, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}:\n{err}"
+        got[rank] = res
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        bad = [x for x in got[r] if not x[2]]
+        assert not bad, (r, bad)
+        assert len(got[r]) == 3 * len(names)

@@ -97,8 +97,11 @@ typedef struct {
     const int32_t *new_len;      /* host [R]: n_i >= 1 new tokens this iteration (l of Alg. 1; 1 = decode) */
     const uint8_t *is_offline;   /* host [R] or NULL: 0 online / 1 offline; no numeric effect (reading R6) */
     const int32_t *shared_prefix_blocks; /* host [R] or NULL: s_i, block_table[i][0:s_i] are shared read-only
-                                            prefix blocks (PSM); requests with the same first
-                                            shared id must list identical sequences */
+                                            prefix blocks (PSM).  The shared sequences must form
+                                            a trie (nested prefixes, e.g. system prompt -> few-shot block):
+                                            an id listed by several rows sits at the same column in each,
+                                            after identical ids; an id in one row's shared prefix appears
+                                            in no other row's private part (else HG_E_INVALID) */
 } hg_batch;
 
 /* Write the new tokens' K and V rows into the cache: token j of request i

@@ -84,14 +84,14 @@ def validate(block_table, c, n, s, B: int, num_blocks: int, H_q: int = None, H_k
             for (i, col) in users:
                 if col >= int(s[i]):
                     return E_INVALID
-    # requests whose first shared id coincides must share identical sequences
-    first: Dict[int, Tuple[int, ...]] = {}
-    for i in range(R):
-        if int(s[i]) > 0:
-            seq = tuple(int(x) for x in bt[i][:int(s[i])])
-            if seq[0] in first and first[seq[0]] != seq:
-                return E_INVALID
-            first.setdefault(seq[0], seq)
+    # shared prefixes form a trie (NEXT-3, R23): every row that shares
+    # an id has it at the same column, after the same sequence of ids
+    for x, users in owner.items():
+        if len(users) > 1:
+            i0, col0 = users[0]
+            for (i, col) in users[1:]:
+                if col != col0 or [int(y) for y in bt[i][:col]] != [int(y) for y in bt[i0][:col0]]:
+                    return E_INVALID
     if append:
         for i in range(R):
             if int(c[i]) < int(s[i]) * B:

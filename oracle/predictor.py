@@ -9,7 +9,8 @@ total prefill / decode tokens, N_p / N_d the request counts.
 
 Attention-exact extensions (readings R13-R15):
   P2    = sum over prefill requests of n_i (c_i + (n_i + 1) / 2)  (attended pairs)
-  D_ctx = unique KV tokens read by decode rows (shared prefix counted once per group)
+  D_ctx = unique KV slots read by decode rows (a physically shared slot counted
+          once, at any prefix depth: NEXT-3 / R23)
 
 Feature order (index k, weight w[1 + k]; w[0] is the intercept):
   0 S_p, 1 S_d, 2 S_p2, 3 S_d2, 4 N_p, 5 N_d, 6 P2, 7 D_ctx
@@ -53,6 +54,25 @@ def features(c, n, shared_tokens=None, group=None):
             S_p += ni
             P2 += ni * (ci + (ni + 1) / 2.0)
     return np.array([S_p, S_d, float(S_p) ** 2, float(S_d) ** 2, N_p, N_d, P2, D], np.float64)
+
+
+def features_paged(c, n, block_table, s, B: int):
+    """The same features with D_ctx counted on the paged layout itself: the set
+    of KV slots the decode rows read, a slot being (physical block, offset) for
+    positions inside a row's s_i shared blocks and (row, position) otherwise."""
+    f = features(c, n)
+    slots = set()
+    D = 0
+    for i in range(len(c)):
+        ci, ni = int(c[i]), int(n[i])
+        if ni == 1 and ci >= 1:
+            for p in range(ci + 1):
+                if p < int(s[i]) * B:
+                    slots.add((int(block_table[i][p // B]), p % B))
+                else:
+                    D += 1
+    f[7] = D + len(slots)
+    return f
 
 
 def design(X, mask: int):

@@ -30,7 +30,8 @@ def fill_pool(spec, lay, req_sel=None, pool=None, device="cpu"):
     sel = None if req_sel is None else set(int(i) for i in req_sel)
     for st in history_steps(spec, lay):
         rows = [k for k, i in enumerate(st.req)
-                if sel is None or i in sel or _group_needed(spec, i, sel)]
+                if sel is None or (st.group[k] < 0 and i in sel) or
+                (st.group[k] >= 0 and _group_needed(spec, st.group[k], sel))]
         if not rows:
             continue
         ks, vs = [], []
@@ -51,10 +52,10 @@ def fill_pool(spec, lay, req_sel=None, pool=None, device="cpu"):
     return pool
 
 
-def _group_needed(spec, i, sel):
-    g = spec.requests[i].group
-    return g >= 0 and spec.shared_blocks(i) > 0 and any(
-        spec.requests[j].group == g and spec.shared_blocks(j) > 0 for j in sel)
+def _group_needed(spec, g, sel):
+    """Some selected request reads group g's physical prefix blocks."""
+    return any(spec.shared_blocks(j) > 0 and g in [x for x, _ in spec.group_chain(spec.requests[j].group)]
+               for j in sel)
 
 
 def run(spec, lay=None, req_sel=None, pool=None, device="cpu"):

@@ -561,28 +561,30 @@ extern "C" hg_status hg_batch_features(const hg_batch *batch, int32_t block_size
     hg_status s = view_batch(batch, &v);
     if (s) return s;
     hg_features f{};
-    // groups of physically shared prefixes: key = first shared id (validated identical sequences)
-    std::vector<std::pair<int32_t, int32_t>> seen;  // (first id, shared tokens) of decode groups
+    // D_ctx = unique KV slots read by decode rows (R15): a slot of a physically
+    // shared block is counted once however many decode rows (at whatever prefix
+    // depth) see it; a row sees positions [0, c_i] of its table.
+    static thread_local std::vector<std::pair<int32_t, int32_t>> seen;  // (shared id, slots visible)
+    seen.clear();
     for (int i = 0; i < v.R; ++i) {
         const int64_t c = v.c[i], n = v.n[i];
         if (n == 1 && c >= 1) {
             f.N_d += 1;
             f.S_d += 1;
-            f.D_ctx += (double)(c + 1);
-            if (v.s[i] > 0) {
-                const int32_t id0 = v.bt[(int64_t)i * v.W];
-                bool dup = false;
-                for (auto &e : seen)
-                    if (e.first == id0) { dup = true; break; }
-                if (dup) f.D_ctx -= (double)v.s[i] * block_size;
-                else seen.push_back({id0, v.s[i] * block_size});
-            }
+            const int64_t s_tok = std::min<int64_t>((int64_t)v.s[i] * block_size, c + 1);
+            f.D_ctx += (double)(c + 1 - s_tok);
+            const int32_t *row = v.bt + (int64_t)i * v.W;
+            for (int64_t k = 0; k * block_size < s_tok; ++k)
+                seen.push_back({row[k], (int32_t)std::min<int64_t>(block_size, s_tok - k * block_size)});
         } else {
             f.N_p += 1;
             f.S_p += (double)n;
             f.P2 += (double)n * ((double)c + (double)(n + 1) / 2.0);
         }
     }
+    std::sort(seen.begin(), seen.end());
+    for (size_t k = 0; k < seen.size(); ++k)   // the largest visible count per id (last of its run)
+        if (k + 1 == seen.size() || seen[k + 1].first != seen[k].first) f.D_ctx += (double)seen[k].second;
     f.S_p2 = f.S_p * f.S_p;
     f.S_d2 = f.S_d * f.S_d;
     *out = f;

@@ -55,7 +55,7 @@ struct TokDev {
 struct TcItem {
     int32_t bt_off;  // block table (bt_flat offset) the keys are read through
     int32_t g;
-    int32_t k0;      // multiple of kTcKeys
+    int32_t k0;      // multiple of kBlock (0 for mode 0)
     int32_t k1;
     int32_t mode;
     int32_t t0;

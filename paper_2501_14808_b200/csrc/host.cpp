@@ -50,21 +50,30 @@ hg_status view_batch(const hg_batch *b, BatchView *v) {
     return HG_OK;
 }
 
-// Per-thread scratch reused across calls: an epoch-stamped owner table for
-// first shared ids (touched R times per call) and three bitmaps over block ids
-// (N_blk / 8 bytes each, L1/L2 resident) for the duplicate / sharing rules.
+// Per-thread scratch reused across calls: epoch-stamped per-block records for
+// the shared (prefix) blocks of the batch (touched sum(s_i) times per call) and
+// a bitmap over block ids (N_blk / 8 bytes, L1/L2 resident) for the duplicate /
+// sharing rules.
 struct Scratch {
-    std::vector<uint64_t> stamp;  // epoch << 32 | owner row
+    std::vector<uint64_t> stamp;  // epoch << 32 | column of the shared block
+    std::vector<int32_t> par;     // id before it in every row that shares it (-1: column 0)
+    std::vector<int32_t> gid;     // prefix group of the sequences ending at this block (-1: none yet)
+    std::vector<int32_t> cnt;     // build_plan: prefix-pass rows whose shared path passes the block
+    std::vector<int32_t> node;    // build_plan: tile-map node starting at the block (-1: none)
     uint32_t epoch = 0;
-    std::vector<uint64_t> bm_shared, bm_priv, bm_row;
+    std::vector<uint64_t> bm_priv;   // ids already used (shared prefixes, private blocks)
     std::vector<int32_t> group;   // prefix group of each row (valid after validate)
     std::vector<int32_t> owners;
+    int64_t n_shared = 0;         // distinct shared block ids in the batch
+    // build_plan: prefix-pass extent of each row and its tile-map nodes
+    struct Node { int32_t a, e, rep, depth, nm, first; };
+    std::vector<int32_t> pre_end, npre;
+    std::vector<Node> nodes;
 };
 static thread_local Scratch g_scr;
 
 static inline bool bm_test(const uint64_t *bm, uint32_t b) { return bm[b >> 6] >> (b & 63) & 1; }
 static inline void bm_set(uint64_t *bm, uint32_t b) { bm[b >> 6] |= 1ull << (b & 63); }
-static inline void bm_clr(uint64_t *bm, uint32_t b) { bm[b >> 6] &= ~(1ull << (b & 63)); }
 
 hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, int H_kv, bool append) {
     if (num_q_heads >= 0) {
@@ -74,13 +83,14 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
     }
     Scratch &sc = g_scr;
     const size_t words = ((size_t)num_blocks + 63) / 64;
-    if (sc.stamp.size() < (size_t)num_blocks) sc.stamp.assign((size_t)num_blocks, 0);
-    if (sc.bm_shared.size() < words) {
-        sc.bm_shared.assign(words, 0);
-        sc.bm_priv.assign(words, 0);
-        sc.bm_row.assign(words, 0);
+    if (sc.stamp.size() < (size_t)num_blocks) {
+        sc.stamp.assign((size_t)num_blocks, 0);
+        sc.par.assign((size_t)num_blocks, -1);
+        sc.gid.assign((size_t)num_blocks, -1);
+        sc.cnt.assign((size_t)num_blocks, 0);
+        sc.node.assign((size_t)num_blocks, -1);
     }
-    memset(sc.bm_shared.data(), 0, words * 8);
+    if (sc.bm_priv.size() < words) sc.bm_priv.assign(words, 0);
     memset(sc.bm_priv.data(), 0, words * 8);
     if (++sc.epoch == 0) {
         std::fill(sc.stamp.begin(), sc.stamp.end(), 0);
@@ -90,7 +100,11 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
     sc.group.assign((size_t)v.R, -1);
     sc.owners.clear();
     int ng = 0, shared_write = -1;
-    // pass A: shapes, id ranges, group ownership by first shared id
+    sc.n_shared = 0;
+    uint64_t *bp = sc.bm_priv.data();
+    // pass A: shapes, id ranges; shared prefixes must form a trie (NEXT-3,
+    // DESIGN.md R23): a block shared by several rows sits at the same column in
+    // each, after the same id (hence after identical sequences, by induction).
     for (int i = 0; i < v.R; ++i) {
         const int64_t c = v.c[i], n = v.n[i], s = v.s[i];
         if (n < 1 || c < 0 || s < 0)
@@ -108,35 +122,31 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
         }
         if (nb > 0 && (lo < 0 || hi >= num_blocks))
             return fail(HG_E_INVALID, "request %d: block id outside [0, %d)", i, num_blocks);
-        if (s > 0) {
-            const uint64_t t = sc.stamp[row[0]];
+        for (int col = 0; col < s; ++col) {
+            const int32_t b = row[col], parent = col ? row[col - 1] : -1;
+            const uint64_t t = sc.stamp[b];
             if ((t & ~0xFFFFFFFFull) == ep) {
-                const int o = (int)(t & 0xFFFFFFFFu);
-                if (v.s[o] != s || memcmp(v.bt + (int64_t)o * v.W, row, sizeof(int32_t) * (size_t)s) != 0)
-                    return fail(HG_E_INVALID, "requests %d and %d share block %d but not an identical prefix", o, i,
-                                row[0]);
-                sc.group[i] = sc.group[o];
+                if ((int)(t & 0xFFFFFFFFu) != col || sc.par[b] != parent)
+                    return fail(HG_E_INVALID, "request %d shares block %d but not an identical prefix before it",
+                                i, b);
             } else {
-                sc.stamp[row[0]] = ep | (uint32_t)i;
-                sc.group[i] = ng++;
-                sc.owners.push_back(i);
+                sc.stamp[b] = ep | (uint32_t)col;
+                sc.par[b] = parent;
+                sc.gid[b] = -1;
+                sc.cnt[b] = 0;
+                sc.node[b] = -1;
+                bm_set(bp, (uint32_t)b);  // shared ids are "taken" for pass C
+                ++sc.n_shared;
             }
         }
-    }
-    // pass B: shared prefixes (one walk per group): no repeats inside a prefix
-    uint64_t *bs = sc.bm_shared.data(), *bp = sc.bm_priv.data(), *br = sc.bm_row.data();
-    for (int o : sc.owners) {
-        const int32_t *row = v.bt + (int64_t)o * v.W;
-        const int s = v.s[o];
-        int bad = -1;
-        for (int col = 0; col < s; ++col) {
-            const uint32_t b = (uint32_t)row[col];
-            if (bm_test(br, b)) { bad = (int)b; break; }
-            bm_set(br, b);
-            bm_set(bp, b);  // shared ids are also "taken" for pass C
+        if (s > 0) {   // prefix group = identical whole shared sequence = same last shared block
+            int32_t &g = sc.gid[row[s - 1]];
+            if (g < 0) {
+                g = ng++;
+                sc.owners.push_back(i);
+            }
+            sc.group[i] = g;
         }
-        for (int col = 0; col < s; ++col) bm_clr(br, (uint32_t)row[col]);
-        if (bad >= 0) return fail(HG_E_INVALID, "request %d lists block %d twice", o, bad);
     }
     // pass C: private blocks are used exactly once and never inside any shared prefix
     for (int i = 0; i < v.R; ++i) {
@@ -235,16 +245,45 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     for (int i = 0; i < v.R; ++i)
         for (int j = 0; j < v.n[i]; ++j) p->tok[(size_t)p->reqs[i].cu_q + j] = TokDev{-1, 1, i, 0};
 
-    const std::vector<int32_t> &group = g_scr.group;
-    const int ng = (int)g_scr.owners.size();
+    Scratch &sc = g_scr;
     const bool tc_ok = o.use_tc && tc_supported(d) && G <= kTcRows;
-    // prefix pass for groups with >= 2 decode members (a lone member gains nothing)
-    std::vector<int32_t> gcount((size_t)ng + 1, 0);
-    for (int i = 0; i < v.R; ++i)
-        if (group[i] >= 0 && v.n[i] == 1) gcount[group[i]]++;
-    auto in_prefix_pass = [&](int i) {
-        return o.prefix_pass && tc_ok && group[i] >= 0 && v.n[i] == 1 && gcount[group[i]] >= 2;
-    };
+    // ---- a.4 tile map over the trie of shared prefixes (NEXT-3) -------------------
+    // cnt[b] = decode rows whose shared path passes block b.  A row's prefix pass
+    // covers its leading columns with cnt >= 2 (a lone member gains nothing; cnt
+    // never grows along a path).  Those columns split into runs of equal cnt, i.e.
+    // of one member set: each run is a node whose keys are read once for the
+    // stacked rows of all its members, as partial `depth` of every member row.
+    sc.pre_end.assign((size_t)v.R, 0);
+    sc.npre.assign((size_t)v.R, 0);
+    sc.nodes.clear();
+    if (o.prefix_pass && tc_ok) {
+        for (int i = 0; i < v.R; ++i)
+            if (v.n[i] == 1 && v.s[i] > 0) {
+                const int32_t *row = v.bt + (int64_t)i * v.W;
+                for (int col = 0; col < v.s[i]; ++col) sc.cnt[row[col]]++;
+            }
+        for (int i = 0; i < v.R; ++i) {
+            if (v.n[i] != 1 || v.s[i] == 0) continue;
+            const int32_t *row = v.bt + (int64_t)i * v.W;
+            int e = 0;
+            while (e < v.s[i] && sc.cnt[row[e]] >= 2) ++e;
+            sc.pre_end[i] = e;
+            int a = 0, depth = 0;
+            while (a < e) {
+                const int32_t b = row[a];
+                int z = a + 1;
+                while (z < e && sc.cnt[row[z]] == sc.cnt[b]) ++z;
+                if (sc.node[b] < 0) {
+                    sc.node[b] = (int32_t)sc.nodes.size();
+                    sc.nodes.push_back(Scratch::Node{a, z, i, depth, 0, 0});
+                }
+                sc.nodes[sc.node[b]].nm++;
+                a = z;
+                ++depth;
+            }
+            sc.npre[i] = depth;
+        }
+    }
     // rows per tcgen05 CTA: 256 (two Q tiles sharing K/V, half the L2 traffic per
     // FLOP) when that still gives every SM a CTA, else 128 (more CTAs)
     int ipr = kTcRows;
@@ -252,21 +291,14 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         int64_t n256 = 0;
         for (int i = 0; i < v.R; ++i)
             if (v.n[i] > 1) n256 += (int64_t)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows);
-        for (int gi = 0; gi < ng; ++gi)
-            if (gcount[gi] >= 2 && o.prefix_pass) n256 += (int64_t)H_kv * ceil_div((int64_t)gcount[gi] * G, 2 * kTcRows);
+        for (const Scratch::Node &nd : sc.nodes) n256 += (int64_t)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows);
         if (n256 >= o.num_sms) ipr = 2 * kTcRows;
     }
-    // algorithmic unique KV tokens U: shared prefix counted once per group
+    // algorithmic unique KV tokens U: every shared block counted once
     {
         int64_t U = 0;
-        std::vector<char> seen((size_t)ng + 1, 0);
-        for (int i = 0; i < v.R; ++i) {
-            U += (int64_t)v.c[i] + v.n[i];
-            if (group[i] >= 0) {
-                if (seen[group[i]]) U -= (int64_t)v.s[i] * B;
-                seen[group[i]] = 1;
-            }
-        }
+        for (int i = 0; i < v.R; ++i) U += (int64_t)v.c[i] + v.n[i] - (int64_t)v.s[i] * B;
+        U += sc.n_shared * B;
         p->kv_bytes_unique = 4ll * d * H_kv * U;
     }
     int64_t kv_tok_read = 0;
@@ -296,7 +328,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     int64_t total_keys = 0;
     for (int i = 0; i < v.R; ++i) {
         if (tc_ok && v.n[i] > 1) continue;
-        const int ks = in_prefix_pass(i) ? v.s[i] * B : 0;
+        const int ks = sc.pre_end[i] * B;
         for (int j0 = 0; j0 < v.n[i]; j0 += tpi) {
             const int nt = std::min(tpi, v.n[i] - j0);
             Chunk ch{i, j0, nt, ks, v.c[i] + j0 + nt};
@@ -314,7 +346,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         chunk_tok = (int)((ct + B - 1) / B * B);
     }
     for (const Chunk &ch : ch_list) {
-        const int pre = in_prefix_pass(ch.i) ? 1 : 0;
+        const int pre = sc.npre[ch.i];
         const int pieces = std::max(1, ceil_div(ch.ke - ch.ks, chunk_tok));
         const int nparts = pre + pieces;
         if (nparts > 1) {
@@ -332,32 +364,32 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             kv_tok_read += (int64_t)(k1 - k0) * H_kv;
         }
     }
-    // ---- prefix group tiles (part 0 of every member row): member-major stacking ----
-    if (ng > 0 && o.prefix_pass && tc_ok) {
-        std::vector<int32_t> first((size_t)ng + 1, 0);
-        for (int i = 0; i < v.R; ++i)
-            if (in_prefix_pass(i)) first[group[i] + 1]++;
-        for (int gi = 0; gi < ng; ++gi) first[gi + 1] += first[gi];
-        const int32_t base_off = 0;
-        p->tc_tok.resize((size_t)first[ng]);
-        std::vector<int32_t> fill(first.begin(), first.end() - 1);
-        std::vector<int32_t> rep((size_t)ng, -1);
-        for (int i = 0; i < v.R; ++i)
-            if (in_prefix_pass(i)) {
-                if (rep[group[i]] < 0) rep[group[i]] = i;
-                p->tc_tok[fill[group[i]]++] = p->reqs[i].cu_q;
+    // ---- prefix node tiles (partial `depth` of every member row): member-major stacking ----
+    if (!sc.nodes.empty()) {
+        int32_t off = 0;
+        for (Scratch::Node &nd : sc.nodes) {
+            nd.first = off;
+            off += nd.nm;
+            nd.nm = 0;
+        }
+        p->tc_tok.resize((size_t)off);
+        for (int i = 0; i < v.R; ++i) {
+            const int32_t *row = v.bt + (int64_t)i * v.W;
+            for (int a = 0; a < sc.pre_end[i];) {
+                Scratch::Node &nd = sc.nodes[sc.node[row[a]]];
+                p->tc_tok[(size_t)nd.first + nd.nm++] = p->reqs[i].cu_q;
+                a = nd.e;
             }
-        for (int gi = 0; gi < ng; ++gi) {
-            const int nm = first[gi + 1] - first[gi];
-            if (nm == 0) continue;
-            const int P = v.s[rep[gi]] * B;
-            const int rows = nm * G;
+        }
+        for (const Scratch::Node &nd : sc.nodes) {
+            const int rows = nd.nm * G;
             for (int g = 0; g < H_kv; ++g) {
                 for (int r0 = 0; r0 < rows; r0 += ipr) {
                     const int nr = std::min(ipr, rows - r0);
                     const int m0 = r0 / G;
-                    TcItem it{p->reqs[rep[gi]].bt_off, g, 0, P, 1, base_off + first[gi] + m0, nr, 0, 0, r0 - m0 * G};
-                    kv_tok_read += P;
+                    TcItem it{p->reqs[nd.rep].bt_off, g, nd.a * B, nd.e * B, 1, nd.first + m0, nr, nd.depth, 0,
+                              r0 - m0 * G};
+                    kv_tok_read += (int64_t)(nd.e - nd.a) * B;
                     p->tc.push_back(it);
                     p->prefix_tiles++;
                 }

@@ -62,8 +62,8 @@ class Workload:
                                 for k in sel])
                 vs = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_V, device=self.device)
                                 for k in sel])
-                # pseudo rows writing a group prefix have s = 0; private history starts at s*B
-                shared = [0 if st.c[k] == 0 else spec.shared_blocks(st.req[k]) for k in sel]
+                # rows list the blocks before their write position that are shared
+                shared = [st.shared[k] for k in sel]
                 b = hg.Batch(np.array([st.tables[k] for k in sel], np.int32), [st.c[k] for k in sel],
                              [st.n[k] for k in sel], None, shared)
                 hg.hg_kv_append(self.pool, b, ks, vs)

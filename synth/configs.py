@@ -10,12 +10,12 @@ Nothing here computes attention or indexes the paged layout.
 from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
-from typing import List
+from typing import Dict, List, Tuple
 
 import numpy as np
 
 CONFIG_NAMES = ("toy_a", "toy_b", "c1", "c1_long", "c2", "c2_g8", "c2_none", "c2_private",
-                "c3", "p1", "p2")
+                "c2_nested", "c3", "p1", "p2")
 
 
 @dataclass
@@ -39,6 +39,10 @@ class BatchSpec:
     seed: int
     requests: List[Request] = field(default_factory=list)
     q_scale: float = 1.0
+    # nested prefix sharing (NEXT-3): child group -> (parent group, tokens of the
+    # child's prefix that are the parent's); a member of the child holds the
+    # parent's content on [0, split) and the child's on [split, prefix_tokens)
+    group_parent: Dict[int, Tuple[int, int]] = field(default_factory=dict)
 
     @property
     def T(self) -> int:
@@ -54,6 +58,16 @@ class BatchSpec:
         if r.group < 0 or not r.share:
             return 0
         return r.prefix_tokens // self.B
+
+    def group_chain(self, g: int) -> List[Tuple[int, int]]:
+        """[(group, start token)] from the root down to g: group k's content
+        covers [start_k, start_{k+1})."""
+        chain = [(g, 0)]
+        while chain[0][0] in self.group_parent:
+            parent, split = self.group_parent[chain[0][0]]
+            chain[0] = (chain[0][0], split)
+            chain.insert(0, (parent, 0))
+        return chain
 
     def with_(self, **kw) -> "BatchSpec":
         return replace(self, **kw)
@@ -95,11 +109,17 @@ def make_config(name: str, seed: int = 0, q_scale: float = 1.0) -> BatchSpec:
                 reqs.append(Request(c, 1, True, group=0, prefix_tokens=1024))
             elif name == "c2_g8":
                 reqs.append(Request(c, 1, True, group=k // 32, prefix_tokens=1024))
+            elif name == "c2_nested":
+                # NEXT-3: one 1024-token system prefix shared by all 256 (group 8),
+                # then 8 few-shot blocks of 512 tokens shared by 32 each (groups 0-7)
+                reqs.append(Request(c, 1, True, group=k // 32, prefix_tokens=1536))
             elif name == "c2_private":
                 reqs.append(Request(c, 1, True, group=0, prefix_tokens=1024, share=False))
             else:
                 reqs.append(Request(c, 1, True))
         spec.requests = reqs
+        if name == "c2_nested":
+            spec.group_parent = {g: (8, 1024) for g in range(8)}
         return spec
     if name == "c3":
         spec = BatchSpec(name, 64, 8, 128, 16, seed, q_scale=q_scale)
@@ -142,4 +162,46 @@ def make_fuzz(seed: int, d: int = None, G_q: int = None, H_kv: int = None, B: in
         n = 1 if (rng.random() < 0.5 and c > 0) else int(rng.integers(1, 41))
         reqs.append(Request(c, n, bool(rng.random() < 0.5), group=g, prefix_tokens=pt))
     spec.requests = reqs
+    return spec
+
+
+def make_fuzz_nested(seed: int, d: int = None, G_q: int = None, H_kv: int = None, B: int = 16) -> BatchSpec:
+    """Random small batch with a prefix trie of depth <= 3 (NEXT-3): roots, children
+    and grandchildren groups with block-aligned splits; members at every level,
+    prefill rows among them, and rows without sharing."""
+    rng = np.random.default_rng(20_000 + seed)
+    d = d if d is not None else int(rng.choice([64, 128]))
+    G_q = G_q if G_q is not None else int(rng.choice([1, 4, 8]))
+    H_kv = H_kv if H_kv is not None else int(rng.choice([1, 2]))
+    spec = BatchSpec(f"nfuzz{seed}", G_q * H_kv, H_kv, d, B, seed)
+    # groups: (tokens of the whole prefix), parents with their split
+    plen, parent = {}, {}
+    ng = 0
+    for _ in range(int(rng.integers(1, 3))):           # roots
+        root = ng
+        plen[root] = int(rng.integers(1, 5)) * B
+        ng += 1
+        for _ in range(int(rng.integers(0, 3))):       # children
+            ch = ng
+            plen[ch] = plen[root] + int(rng.integers(1, 4)) * B
+            parent[ch] = (root, plen[root])
+            ng += 1
+            for _ in range(int(rng.integers(0, 2))):   # grandchildren
+                gc = ng
+                plen[gc] = plen[ch] + int(rng.integers(1, 3)) * B
+                parent[gc] = (ch, plen[ch])
+                ng += 1
+    reqs = []
+    for k in range(int(rng.integers(2, 20))):
+        g = int(rng.integers(-1, ng))
+        if g >= 0:
+            pt = plen[g]
+            c = pt + int(rng.integers(0, 150))
+        else:
+            pt = 0
+            c = int(rng.integers(0, 301))
+        n = 1 if (rng.random() < 0.7 and c > 0) else int(rng.integers(1, 41))
+        reqs.append(Request(c, n, bool(rng.random() < 0.5), group=g, prefix_tokens=pt))
+    spec.requests = reqs
+    spec.group_parent = parent
     return spec

@@ -68,12 +68,27 @@ def gen_block(seed: int, kind: int, cid: int, pos: torch.Tensor, heads: int, dim
     return x.to(torch.bfloat16)
 
 
+def segments(spec, i: int):
+    """[(start, end, content id)] covering request i's positions: its prefix
+    groups root to leaf (nested sharing, NEXT-3), then its own content."""
+    r = spec.requests[i]
+    out = []
+    if r.group >= 0 and r.prefix_tokens > 0:
+        chain = spec.group_chain(r.group)
+        for k, (g, start) in enumerate(chain):
+            end = chain[k + 1][1] if k + 1 < len(chain) else r.prefix_tokens
+            if end > start:
+                out.append((start, end, GROUP_CID_BASE + g))
+    out.append((r.prefix_tokens if r.group >= 0 else 0, 1 << 62, own_cid(spec, i)))
+    return out
+
+
 def content_id(spec, i: int, pos: int) -> int:
     """Content id of request i's token at absolute position ``pos``."""
-    r = spec.requests[i]
-    if r.group >= 0 and pos < r.prefix_tokens:
-        return GROUP_CID_BASE + r.group
-    return own_cid(spec, i)
+    for a, b, cid in segments(spec, i):
+        if a <= pos < b:
+            return cid
+    raise ValueError(pos)
 
 
 def own_cid(spec, i: int) -> int:
@@ -85,18 +100,15 @@ def kv_values(spec, i: int, start: int, end: int, kind: int, device="cpu") -> to
     """K (kind=KIND_K) or V (kind=KIND_V) rows of request i for positions [start, end).
 
     Returns bf16 [end-start][H_kv][d]; positions inside the group prefix take
-    the group's content, the rest the request's own content.
+    the content of the group owning them (root to leaf), the rest the request's
+    own content.
     """
-    r = spec.requests[i]
     parts = []
-    cut = r.prefix_tokens if r.group >= 0 else 0
-    if start < min(end, cut):
-        pos = torch.arange(start, min(end, cut), dtype=torch.int64)
-        parts.append(gen_block(spec.seed, kind, GROUP_CID_BASE + r.group, pos, spec.H_kv, spec.d,
-                               device=device))
-    if max(start, cut) < end:
-        pos = torch.arange(max(start, cut), end, dtype=torch.int64)
-        parts.append(gen_block(spec.seed, kind, own_cid(spec, i), pos, spec.H_kv, spec.d, device=device))
+    for a, b, cid in segments(spec, i):
+        lo, hi = max(start, a), min(end, b)
+        if lo < hi:
+            pos = torch.arange(lo, hi, dtype=torch.int64)
+            parts.append(gen_block(spec.seed, kind, cid, pos, spec.H_kv, spec.d, device=device))
     if not parts:
         return torch.empty((0, spec.H_kv, spec.d), dtype=torch.bfloat16, device=device)
     return torch.cat(parts, 0) if len(parts) > 1 else parts[0]

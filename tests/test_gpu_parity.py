@@ -200,7 +200,8 @@ def test_error_leaves_outputs_untouched():
     spec = make_config("toy_a", 0)
     wl = make(spec)
     wl.out.fill_(7.0)
-    bad = hg.Batch(wl.lay.block_table, [0, 32, 32], [16, 1, 1], None, [0, 1, 2])
+    # block S shared by r1 but private in r2: not a valid sharing (§8(b))
+    bad = hg.Batch(wl.lay.block_table, [0, 32, 32], [16, 1, 1], None, [0, 1, 0])
     k_before = wl.k_cache.clone()
     st = hg.status_of(hg.hg_hybrid_attention, wl.pool, bad, spec.H_q, wl.q, wl.out, None, wl.workspace())
     assert st == hg.HG_E_INVALID
@@ -347,3 +348,60 @@ def test_fused_step_equals_append_then_attention(name):
     assert torch.equal(a.out.view(torch.int16), b.out.view(torch.int16))
     assert torch.equal(a.k_cache.view(torch.int16), b.k_cache.view(torch.int16))
     assert torch.equal(a.v_cache.view(torch.int16), b.v_cache.view(torch.int16))
+
+
+# ---- nested prefix sharing (NEXT-3) ------------------------------------------------
+def _unique_kv_bytes(spec, lay):
+    """4*d*H_kv*U with U = unique KV slots of the batch: every physically shared
+    block once, private positions per row."""
+    shared = set()
+    U = 0
+    for i, r in enumerate(spec.requests):
+        s = int(lay.shared[i])
+        U += r.c + r.n - s * spec.B
+        shared.update(int(x) for x in lay.block_table[i][:s])
+    return 4 * spec.d * spec.H_kv * (U + len(shared) * spec.B)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_nested_fuzz(seed):
+    from synth.configs import make_fuzz_nested
+    spec = make_fuzz_nested(seed)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    compare(spec, wl)
+    assert hg_stats(wl)["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
+
+
+@pytest.mark.parametrize("variant", ["no_tc", "no_prefix", "split64"])
+@pytest.mark.parametrize("seed", range(6))
+def test_nested_plan_variants(variant, seed):
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_fuzz_nested
+    spec = make_fuzz_nested(100 + seed)
+    opts = {"no_tc": hg.make_opts(disable_tc=True), "split64": hg.make_opts(split_tokens=64),
+            "no_prefix": hg.make_opts(disable_prefix_pass=True)}[variant]
+    wl = make(spec)
+    wl.append()
+    wl.attention(opts)
+    torch.cuda.synchronize()
+    compare(spec, wl, tag=f"[{variant}]")
+
+
+def test_c2_nested_full_size():
+    """256 decodes: a 1024-token root shared by all, 8 x 512-token children shared by
+    32 each.  Two tile-map levels: the root read once for 256 members, each child
+    once for its 32; the rest per request by split-K."""
+    from synth.configs import make_config
+    spec = make_config("c2_nested", 0)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    st = hg_stats(wl)
+    # root: 256 members x G_q=4 = 1024 stacked rows; children: 32 x 4 = 128 rows each.
+    # 256-row CTAs would give H_kv*(4 + 8) = 96 < 148 CTAs, so the planner uses 128-row tiles
+    assert st["prefix_tiles"] == spec.H_kv * (1024 // 128 + 8), st
+    assert st["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
+    compare(spec, wl, req_sel=_sample(spec, 10))
+    wl.close()

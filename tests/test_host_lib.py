@@ -11,7 +11,7 @@ import pytest
 import paper_2501_14808_b200 as hg
 from oracle import mirror
 from oracle import predictor as OP
-from synth.configs import make_config, make_fuzz, CONFIG_NAMES
+from synth.configs import make_config, make_fuzz, make_fuzz_nested, CONFIG_NAMES
 from synth.layout import make_layout
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -118,6 +118,19 @@ def test_batch_indices_fuzz_bit_exact(seed):
     assert np.array_equal(slot, mslot) and np.array_equal(pg, mpg)
 
 
+@pytest.mark.parametrize("seed", range(200))
+def test_batch_indices_nested_fuzz_bit_exact(seed):
+    """Prefix tries (NEXT-3): groups = identical whole shared sequences."""
+    spec = make_fuzz_nested(seed)
+    lay = make_layout(spec, seed=seed)
+    p = pool(lay.num_blocks, spec.H_kv, spec.d)
+    got = hg.hg_batch_indices(p, _batch_of(spec, lay))
+    exp = mirror.batch_indices(lay.block_table, [r.c for r in spec.requests], [r.n for r in spec.requests],
+                               lay.shared, 16)
+    for a, b in zip(got, exp):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("name", CONFIG_NAMES)
 def test_batch_indices_configs(name):
     spec = make_config(name)
@@ -133,7 +146,7 @@ def test_batch_indices_configs(name):
 def _mutations(rng, bt, c, n, s, N):
     """Random rule-breaking edits of a valid batch."""
     bt, c, n, s = bt.copy(), list(c), list(n), list(s)
-    k = int(rng.integers(0, 7))
+    k = int(rng.integers(0, 9))
     i = int(rng.integers(0, len(c)))
     if k == 0:
         n[i] = 0
@@ -148,15 +161,20 @@ def _mutations(rng, bt, c, n, s, N):
         bt[j, 0] = bt[i, 0]
     elif k == 5:
         s[i] = s[i] + 1
+    elif k == 7 and s[i] >= 2:
+        bt[i, 0], bt[i, 1] = bt[i, 1], bt[i, 0]       # shared ids at other columns
+    elif k == 8 and s[i] >= 2:
+        bt[i, 0] = N - 1 - i                             # a different root before shared ids
     else:
         c[i] = c[i] + bt.shape[1] * 16
     return bt, c, n, s
 
 
+@pytest.mark.parametrize("nested", [False, True])
 @pytest.mark.parametrize("seed", range(120))
-def test_validation_status_matches_mirror(seed):
+def test_validation_status_matches_mirror(seed, nested):
     rng = np.random.default_rng(seed)
-    spec = make_fuzz(seed)
+    spec = make_fuzz_nested(seed) if nested else make_fuzz(seed)
     lay = make_layout(spec, seed=seed)
     c = [r.c for r in spec.requests]
     n = [r.n for r in spec.requests]
@@ -215,6 +233,17 @@ def test_features_match_oracle(seed):
     grp = [r.group if spec.shared_blocks(i) else -1 for i, r in enumerate(spec.requests)]
     st = [spec.shared_blocks(i) * 16 for i in range(len(spec.requests))]
     e = OP.features([r.c for r in spec.requests], [r.n for r in spec.requests], st, grp)
+    assert np.array_equal(f, e)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_features_nested_match_paged_definition(seed):
+    """D_ctx on prefix tries: unique (block, offset) slots of decode rows."""
+    spec = make_fuzz_nested(seed) if seed % 2 else make_fuzz(seed)
+    lay = make_layout(spec, seed=seed)
+    f = hg.hg_batch_features(_batch_of(spec, lay)).as_array()
+    e = OP.features_paged([r.c for r in spec.requests], [r.n for r in spec.requests], lay.block_table,
+                          lay.shared, 16)
     assert np.array_equal(f, e)
 
 

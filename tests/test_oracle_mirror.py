@@ -82,7 +82,14 @@ def test_validate_rules():
     assert mirror.validate([[0, 16]], [4], [1], [0], B, N) == mirror.E_INVALID
     assert mirror.validate([[3, 3]], [4], [1], [0], B, N) == mirror.E_INVALID
     assert mirror.validate([[0, 1], [0, 2]], [3, 5], [1, 1], [1, 1], B, N, append=True) == mirror.E_SHARED_WRITE
-    assert mirror.validate([[0, 1, 5], [0, 2, 6]], [9, 9], [1, 1], [2, 2], B, N) == mirror.E_INVALID
+    # nested sharing (NEXT-3, R23): a common root block, then different children: valid
+    assert mirror.validate([[0, 1, 5], [0, 2, 6]], [9, 9], [1, 1], [2, 2], B, N) == 0
+    assert mirror.validate([[0, 1, 5], [0, 1, 6], [0, 7, 8]], [9, 9, 9], [1, 1, 1], [2, 2, 1], B, N) == 0
+    # not a trie: a shared id at different columns, or after different ids
+    assert mirror.validate([[0, 1, 5], [1, 0, 6]], [9, 9], [1, 1], [2, 2], B, N) == mirror.E_INVALID
+    assert mirror.validate([[0, 1, 5], [2, 1, 6]], [9, 9], [1, 1], [2, 2], B, N) == mirror.E_INVALID
+    # a block inside one row's shared prefix but private in another
+    assert mirror.validate([[0, 1, 5], [0, 2, 1]], [9, 9], [1, 1], [2, 1], B, N) == mirror.E_INVALID
     assert mirror.validate([[0, 1]], [4], [1], [0], B, N, H_q=6, H_kv=4) == mirror.E_INVALID
 
 

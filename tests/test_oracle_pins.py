@@ -9,7 +9,7 @@ import torch
 from oracle import OraclePool, merge_partials
 from oracle.brute import attention_dense
 from oracle.run import fill_pool, run
-from synth.configs import BatchSpec, Request, make_config, make_fuzz
+from synth.configs import BatchSpec, Request, make_config, make_fuzz, make_fuzz_nested
 from synth.layout import make_layout
 from synth.values import KIND_K, KIND_V, kv_values, q_values
 
@@ -64,6 +64,16 @@ def test_brute_force_toy(name, q_scale):
 @pytest.mark.parametrize("seed", range(6))
 def test_brute_force_fuzz(seed):
     brute_check(make_fuzz(seed))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_brute_force_nested_prefixes(seed):
+    """Prefix trie of depth <= 3 (NEXT-3): the paged oracle over physically shared
+    root / child / grandchild blocks == dense brute force on each logical sequence."""
+    spec = make_fuzz_nested(seed)
+    lay = make_layout(spec)
+    assert len(set(map(tuple, (row[:s] for row, s in zip(lay.block_table.tolist(), lay.shared) if s)))) >= 1
+    brute_check(spec)
 
 
 def test_sdpa_textbook_causal():
@@ -127,6 +137,15 @@ def test_shared_prefix_equals_private_copies_bitwise(seed):
     o_p, l_p = run(priv)
     assert make_layout(spec).num_blocks != make_layout(priv).num_blocks
     assert np.array_equal(o_s, o_p) and np.array_equal(l_s, l_p)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_nested_shared_prefix_equals_private_copies_bitwise(seed):
+    spec = make_fuzz_nested(seed)
+    priv = spec.with_(requests=[r.__class__(**{**r.__dict__, "share": False}) for r in spec.requests])
+    o_s, l_s = run(spec)
+    o_p, l_p = run(priv)
+    assert np.array_equal(o_s, o_p, equal_nan=True) and np.array_equal(l_s, l_p, equal_nan=True)
 
 
 def test_block_permutation_invariance():

@@ -342,6 +342,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_rows, plan.tc_tok.data(), sizeof(int32_t) * plan.tc_tok.size());
     put(plan.off_cbase, plan.tok.data(), sizeof(TokDev) * plan.tok.size());
     put(plan.off_comb, plan.comb.data(), sizeof(int32_t) * plan.comb.size());
+    put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
     s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
     if (s) return s;
     uint8_t *w = (uint8_t *)ws;
@@ -366,6 +367,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.tc_tok = (const int32_t *)(w + plan.off_rows);
     p.tok = (const TokDev *)(w + plan.off_cbase);
     p.comb = (const int32_t *)(w + plan.off_comb);
+    p.tc_off = (const int32_t *)(w + plan.off_tcoff);
     p.part_o = (float *)(w + plan.off_part_o);
     p.part_lse = (float *)(w + plan.off_part_lse);
     p.H_q = H_q;

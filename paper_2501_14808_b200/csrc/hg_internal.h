@@ -89,7 +89,8 @@ struct AttnParams {
     float *part_lse;           // [slots] log2-domain LSE of each partial (-inf: empty)
     int32_t H_q, H_kv, G_q, d;
     int32_t n_sk, n_tc, n_comb;
-    int32_t tc_ctas;           // persistent tcgen05 grid (<= n_tc); 0: one CTA per item
+    int32_t tc_ctas;           // persistent tcgen05 grid (<= n_tc)
+    const int32_t *tc_off;     // [tc_ctas + 1]: CTA b processes tc items [tc_off[b], tc_off[b+1])
     float scale_log2;          // log2(e) / sqrt(d)
     long long *trace;          // debug: per-event clock64 stamps of tcgen05 CTA 0 (NULL: off)
 };
@@ -104,6 +105,7 @@ struct Plan {
     std::vector<int32_t> tc_tok;
     std::vector<SkItem> sk_tmp;
     std::vector<TcItem> tc_tmp;
+    std::vector<int32_t> tc_off;   // per-CTA item ranges of the persistent tcgen05 grid
     std::vector<TokDev> tok;
     std::vector<int32_t> comb;
     int64_t n_slots = 0;
@@ -113,7 +115,7 @@ struct Plan {
     int32_t tc_ctas = 0;        // persistent tcgen05 grid chosen by the planner
     // device layout (byte offsets inside the workspace)
     size_t off_reqs = 0, off_bt = 0, off_sk = 0, off_tc = 0, off_rows = 0, off_cbase = 0,
-           off_comb = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
+           off_comb = 0, off_tcoff = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
 };
 
 // ---- host helpers (host.cpp) ------------------------------------------------

@@ -297,10 +297,12 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     auto bar = [&](int i) { return bars + 8u * i; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // Persistent: CTA b processes items b, b + gridDim.x, ... (LPT-ordered by the
-    // planner).  Every role walks the same item sequence; barrier phases come
-    // from running counters, so the pipelines never drain between items.
+    // Persistent: CTA b processes items [tc_off[b], tc_off[b+1]) (greedy LPT
+    // assignment by the planner).  Every role walks the same item sequence;
+    // barrier phases come from running counters, so the pipelines never drain
+    // between items.
     long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;   // debug timeline of CTA 0's first item (NULL: off)
+    const int it_begin = p.tc_off[blockIdx.x], it_end = p.tc_off[blockIdx.x + 1];
     auto nkt_of = [&](const TcItem &it) { return (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys; };
     auto ntiles_of = [&](const TcItem &it) { return it.nrows > kTcRows ? 2 : 1; };
 
@@ -338,7 +340,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         // (separate threads so a V slot that is still busy never delays the next K load)
         if (lane == 0) {
             int64_t gn = 0;   // K (or V) tiles loaded by this CTA so far
-            for (int item = blockIdx.x; item < p.n_tc; item += gridDim.x) {
+            for (int item = it_begin; item < it_end; ++item) {
                 const TcItem it = p.tc[item];
                 const int nkt = nkt_of(it);
                 const int32_t *bt = p.bt_flat + it.bt_off;
@@ -357,7 +359,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     if (warp == 8) {
                         const int st = (int)(gn % L::kKStages);
                         if (gn >= L::kKStages) mbar_wait(bar(BAR_KEMPTY + st), ((gn / L::kKStages) - 1) & 1);
-                        if (tr && item == (int)blockIdx.x && j < 64) tr[1024 + 2 * j] = clock64();
+                        if (tr && item == it_begin && j < 64) tr[1024 + 2 * j] = clock64();
                         dst = sK + st * L::kKV;
                         fb = bar(BAR_KFULL + st);
                         tm = &tmap_k;
@@ -391,10 +393,10 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         int64_t gk = 0, gv = 0;          // K / V tiles consumed so far
         int ps[2] = {0, 0};              // P steps consumed per Q tile
         int n_item = 0;
-        for (int item = blockIdx.x; item < p.n_tc; item += gridDim.x, ++n_item) {
+        for (int item = it_begin; item < it_end; ++item, ++n_item) {
             const TcItem it = p.tc[item];
             const int nkt = nkt_of(it), ntiles = ntiles_of(it);
-            const bool trace = tr && item == (int)blockIdx.x;
+            const bool trace = tr && item == it_begin;
             auto issue_qk = [&](int t, int64_t kt, bool last_tile) {
                 const uint32_t tS = tmem + 256 * t;
                 const uint64_t dq = dQ0 + (uint64_t)((t * L::kQ) >> 4);
@@ -472,10 +474,10 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         const float sc = p.scale_log2;
         int ss = 0;                          // S steps consumed by this Q tile
         int n_item = 0;
-        for (int item = blockIdx.x; item < p.n_tc; item += gridDim.x, ++n_item) {
+        for (int item = it_begin; item < it_end; ++item, ++n_item) {
             const TcItem it = p.tc[item];
             const int nkt = nkt_of(it), ntiles = ntiles_of(it);
-            const bool trace = tr && item == (int)blockIdx.x;
+            const bool trace = tr && item == it_begin;
             const bool valid = rr < it.nrows;
             struct { int t, h, lim; } row{0, 0, 0};
             if (valid) {

@@ -31,14 +31,17 @@ torch.cuda.synchronize()
 ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(a.steps)]
 ops = [hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split, events=e) for e in ev]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+tot = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
 for k in range(a.steps):
     flush.zero_()
+    tot[k][0].record()
     wl.step(ops[k])
+    tot[k][1].record()
 torch.cuda.synchronize()
 if a.time:
     st = hg.hg_last_plan_stats(wl.pool)
     for k in range(a.steps):
         e = ev[k]
-        print(a.config, "split", a.split, "tc %.4f" % (e[0].elapsed_time(e[1]) if st["tc_tiles"] else 0),
+        print(a.config, "split", a.split, "step %.4f" % tot[k][0].elapsed_time(tot[k][1]), "tc %.4f" % (e[0].elapsed_time(e[1]) if st["tc_tiles"] else 0),
               "splitk %.4f" % (e[2].elapsed_time(e[3]) if st["splitk_items"] else 0),
               "comb %.4f" % (e[4].elapsed_time(e[5]) if st["combine_rows"] else 0), st)

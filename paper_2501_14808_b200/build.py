@@ -38,7 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc")] + ARCH
+              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc")] + ARCH + \
+        os.environ.get("HG_NVCC_DEFS", "").split()   # experiment knobs (e.g. -DHG_POLY_MASK=0xAA)
     objs = []
     procs = []
     for src in sources():

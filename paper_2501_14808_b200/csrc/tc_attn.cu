@@ -222,6 +222,12 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
+// Which exp2 pairs (bit c & 7 of the 128-key row's pair index c) go to the FMA-pipe
+// polynomial instead of MUFU.EX2: 0x88 = one in four.
+#ifndef HG_POLY_MASK
+#define HG_POLY_MASK 0x88
+#endif
+
 // exp2_poly on a pair: 2 FMNMX + 3 FADD2/FFMA2 + 3 FFMA2 + 2 IMAD for two values.
 // The exponent add folds (bits(t) - 0x4B400000) << 23 into bits(t) << 23 (the
 // constant vanishes mod 2^32).
@@ -294,6 +300,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     const uint32_t sQ = sbase + L::oQ, sK = sbase + L::oK, sV = sbase + L::oV;
     const uint32_t bars = sbase + L::oBar;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::oBar + BAR_N * 8);
+    const uint32_t s_zero = sbase + L::oBar + BAR_N * 8 + 8;   // a 0.0f word (scheduling fence, see softmax)
     auto bar = [&](int i) { return bars + 8u * i; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -321,6 +328,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         mbar_init(bar(BAR_ODONE), 1);
         mbar_init(bar(BAR_QREADY), 256);
         mbar_init(bar(BAR_OFREE), 256);
+        asm volatile("st.shared.u32 [%0], 0;\n" ::"r"(s_zero) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 9) {  // TMEM: tile t: S/P at [256 t, 256 t + 128), O at [256 t + 128, 256 t + 128 + D)
@@ -516,6 +524,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
 #pragma unroll
                     for (int c = 0; c < 4; ++c) TMEM_LD32(tS + c * 32, (&sr[c * 32]));
                     tmem_wait_ld();
+                    if (trace && r == 0 && j < 64) tr[2048 + 512 * t + 8 * j + 0] = clock64();
                     const int kbase = it.k0 + j * kTcKeys;
                     // diagonal / tail tile: mask keys >= lim.  The branch is made
                     // warp-uniform so full tiles skip the (if-converted) mask body.
@@ -551,22 +560,34 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                             TMEM_ST32(tO + c * 32, orr);
                         }
                     }
+                    if (trace && r == 0 && j < 64) tr[2048 + 512 * t + 8 * j + 1] = clock64();
                     const float nref = (m_used == -CUDART_INF_F) ? 0.f : -m_used;
-                    const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(nref, nref);
+                    const uint64_t sc2 = f2pack(sc, sc);
+                    uint64_t nref2 = f2pack(nref, nref);
                     uint64_t ls2[2] = {0ull, 0ull};
                     uint32_t pk[64];
 #pragma unroll
                     for (int c = 0; c < 64; ++c) {
                         if (c == 32) {   // first half of P (keys 0-63) -> TMEM: the MMA can start PV on it
+                            if (trace && r == 0 && j < 64) tr[2048 + 512 * t + 8 * j + 2] = clock64();
                             TMEM_ST32(tS, pk);
                             tmem_wait_st();
                             tc_fence_before();
                             mbar_arrive(bar(BAR_PHALF + t));
+                            if (trace && r == 0 && j < 64) tr[2048 + 512 * t + 8 * j + 3] = clock64();
+                            // keep the second half's exponentials after this point: otherwise
+                            // ptxas hoists nearly all MUFU work above the first store and the PV
+                            // of keys 0-63 cannot start until the whole row is done.  The second
+                            // half's offset comes from a volatile load of a 0.0f word, ordered
+                            // after the arrive.
+                            float zero;
+                            asm volatile("ld.volatile.shared.f32 %0, [%1];\n" : "=f"(zero) : "r"(s_zero) : "memory");
+                            nref2 = f2pack(nref + zero, nref + zero);
                         }
                         const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
                                                   sc2, nref2);
                         float a, b;
-                        if ((c & 3) == 3) {   // one pair in four on the FMA pipe, three on MUFU (FA4-style offload)
+                        if ((HG_POLY_MASK >> (c & 7)) & 1) {   // pairs on the FMA pipe, the rest on MUFU (FA4-style offload)
                             exp2_poly2(x2, a, b);
                         } else {
                             float x0, x1;

@@ -8,7 +8,7 @@ from synth.configs import make_config
 spec = make_config(sys.argv[1] if len(sys.argv) > 1 else "p2", 0)
 wl = Workload(spec)
 wl.step()
-tr = torch.zeros(4096, dtype=torch.int64, device="cuda")
+tr = torch.zeros(8192, dtype=torch.int64, device="cuda")
 o = hg.make_opts()
 o.debug_trace = tr.data_ptr()
 wl.attention(o)
@@ -20,3 +20,8 @@ print("j | TMA-issue | PFULL0 seen  PV0+QK0 issued | PFULL1 seen  PV1+QK1 issued
 for j in range(0, 40):
     print(j, t[1024 + 2 * j], "|", t[8 * j], t[8 * j + 1], "|", t[8 * j + 2], t[8 * j + 3], "|",
           t[512 + 2 * j], t[512 + 2 * j + 1], "|", t[768 + 2 * j], t[768 + 2 * j + 1])
+
+print("softmax tile 0: S ready -> S loaded -> max/bump done -> first half exps done -> PHALF arrived -> P done")
+for j in range(0, 20):
+    a = [t[512 + 2 * j]] + [t[2048 + 8 * j + k] for k in range(4)] + [t[512 + 2 * j + 1]]
+    print(j, a, "deltas", [a[k + 1] - a[k] for k in range(5)])

@@ -210,7 +210,7 @@ def run_ours(args):
     sk_avg = statistics.mean(sk_ms) if sk_ms else None
     bytes_sk = alg_bytes_splitk(spec)
     achieved = bytes_sk / (sk_avg / 1e3) / 1e9 if sk_avg else None
-    traffic = load_traffic("splitk_kernel", bytes_sk)
+    traffic = load_traffic(f"splitk_kernel@{WORKLOAD}", bytes_sk)
     roofline = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)" if peak_kind == "measured" else "fallback",
                 "unit": "GB/s", "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,

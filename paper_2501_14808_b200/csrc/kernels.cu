@@ -56,32 +56,54 @@ hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *
 
 // Fused-step append: the slot of token t is derived on the device from the
 // attention descriptors (owning request, cached length, flattened block ids).
-__global__ void append_dev_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
-                                  uint4 *__restrict__ k_cache, uint4 *__restrict__ v_cache, const AttnParams p, int T,
-                                  int chunks_per_row) {
-    const int64_t total = (int64_t)T * p.H_kv * chunks_per_row;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = idx / chunks_per_row;
-        const int ch = (int)(idx % chunks_per_row);
-        const int t = (int)(row / p.H_kv);
-        const int g = (int)(row % p.H_kv);
-        const ReqDev rq = p.reqs[p.tok[t].req];
-        const int pos = rq.c + (t - rq.cu_q);
-        const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
-        const int64_t dst = ((blk * p.H_kv + g) * kBlock + pos % kBlock) * chunks_per_row + ch;
-        k_cache[dst] = k_new[idx];
-        v_cache[dst] = v_new[idx];
+// One CTA per token: the slot is computed once, then every (KV head, 16-byte
+// chunk) of K and V is moved with all loads issued before the stores.
+template <int PER>   // uint4 chunks of K (and of V) per thread
+__global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict__ k_new,
+                                                         const uint4 *__restrict__ v_new, uint4 *__restrict__ k_cache,
+                                                         uint4 *__restrict__ v_cache, const AttnParams p,
+                                                         int chunks_per_row) {
+    const int t = blockIdx.x;
+    const ReqDev rq = p.reqs[p.tok[t].req];
+    const int pos = rq.c + (t - rq.cu_q);
+    const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
+    const int row_chunks = p.H_kv * chunks_per_row;   // uint4 chunks of one token's K (or V)
+    const int64_t src0 = (int64_t)t * row_chunks;
+    for (int base = 0; base < row_chunks; base += 256 * PER) {
+        uint4 kv[2 * PER];
+        int idx[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            idx[e] = base + threadIdx.x + e * 256;
+            if (idx[e] < row_chunks) {
+                kv[e] = k_new[src0 + idx[e]];
+                kv[PER + e] = v_new[src0 + idx[e]];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            if (idx[e] < row_chunks) {
+                const int g = idx[e] / chunks_per_row, ch = idx[e] - g * chunks_per_row;
+                const int64_t dst = ((blk * p.H_kv + g) * kBlock + pos % kBlock) * chunks_per_row + ch;
+                k_cache[dst] = kv[e];
+                v_cache[dst] = kv[PER + e];
+            }
+        }
     }
 }
 
 hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream) {
     if (T == 0) return HG_OK;
     const int cpr = p.d / 8;
-    const int64_t total = (int64_t)T * p.H_kv * cpr;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    append_dev_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)k_new, (const uint4 *)v_new,
-                                                                 (uint4 *)p.k_cache, (uint4 *)p.v_cache, p, T, cpr);
+    const int row_chunks = p.H_kv * cpr;
+    const int per = (row_chunks + 255) / 256;
+    auto *kn = (const uint4 *)k_new, *vn = (const uint4 *)v_new;
+    auto *kc = (uint4 *)p.k_cache, *vc = (uint4 *)p.v_cache;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (per <= 1) append_dev_kernel<1><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
+    else if (per <= 2) append_dev_kernel<2><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
+    else if (per <= 4) append_dev_kernel<4><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
+    else append_dev_kernel<8><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
 }

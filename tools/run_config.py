@@ -34,6 +34,8 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 tot = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
 for k in range(a.steps):
     flush.zero_()
+    if os.environ.get("HG_HOST_AHEAD"):
+        torch.cuda._sleep(400000)   # keep the GPU busy so the host enqueues the step ahead of it
     tot[k][0].record()
     wl.step(ops[k])
     tot[k][1].record()
@@ -42,6 +44,10 @@ if a.time:
     st = hg.hg_last_plan_stats(wl.pool)
     for k in range(a.steps):
         e = ev[k]
-        print(a.config, "split", a.split, "step %.4f" % tot[k][0].elapsed_time(tot[k][1]), "tc %.4f" % (e[0].elapsed_time(e[1]) if st["tc_tiles"] else 0),
+        lead = tot[k][0].elapsed_time(e[2]) if st["splitk_items"] else 0.0
+        lead_tc = tot[k][0].elapsed_time(e[0]) if st["tc_tiles"] else 0.0
+        print("   lead to tc start %.4f" % lead_tc)
+        tail = e[3].elapsed_time(tot[k][1]) if st["splitk_items"] else 0.0
+        print(a.config, "split", a.split, "step %.4f lead %.4f tail %.4f" % (tot[k][0].elapsed_time(tot[k][1]), lead, tail), "tc %.4f" % (e[0].elapsed_time(e[1]) if st["tc_tiles"] else 0),
               "splitk %.4f" % (e[2].elapsed_time(e[3]) if st["splitk_items"] else 0),
               "comb %.4f" % (e[4].elapsed_time(e[5]) if st["combine_rows"] else 0), st)

@@ -35,6 +35,22 @@ __global__ void bench(long long *out, int iters) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tm = slot;
+    if (MODE == 7 && threadIdx.x >= 32) {   // TMEM traffic from the other warps (softmax-like ld/st)
+        const int w = threadIdx.x >> 5;
+        const uint32_t ta = tm + 384 + ((uint32_t)(w * 32) << 16);
+        uint32_t r[32];
+        for (int k = 0; k < iters / 16; ++k) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                         : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                         :: "r"(ta + 32), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+                            "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+            asm volatile("tcgen05.wait::st.sync.aligned;");
+        }
+    }
     if (threadIdx.x < 32) {
         const uint64_t dA = desc(sb, 16, 1024, 2);
         const uint64_t dB_k128 = desc(sb + 32768, 16, 1024, 2);
@@ -61,6 +77,14 @@ __global__ void bench(long long *out, int iters) {
                     if (MODE == 4)  // SS, A K-major, B MN-major SW128
                         asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
                                      ::"r"(tm + 256), "l"(dA + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "l"(dB_mn + ((ks * 2048) >> 4)), "r"(idesc(128, 128, 0, 1)), "r"(acc));
+                    if (MODE == 6 || MODE == 7) {  // alternate: 8 x QK (SS, K-major B) then 8 x PV (TS, MN-major B)
+                        if (((i / 8) & 1) == 0)
+                            asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                                         ::"r"(tm + 256), "l"(dA + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "l"(dB_k128 + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "r"(idesc(128, 128, 0, 0)), "r"(acc));
+                        else
+                            asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}"
+                                         ::"r"(tm + 128), "r"(tm + ks * 8), "l"(dB_mn + ((ks * 2048) >> 4)), "r"(idesc(128, 128, 0, 1)), "r"(acc));
+                    }
                     if (MODE == 5)  // SS, N=256 (both Q tiles' PV in one, if V were the A operand)
                         asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
                                      ::"r"(tm), "l"(dA + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "l"(dB_k128 + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "r"(idesc(128, 256, 0, 0)), "r"(acc));
@@ -105,5 +129,7 @@ int main() {
     run<3>("TS B=K32 N128 (V^T blocks)", d);
     run<4>("SS B=MN128 N128", d);
     run<5>("SS A=K128 B=K128 N256", d);
+    run<6>("alternate 8 QK (SS) / 8 PV (TS)", d);
+    run<7>("alternate + TMEM ld/st traffic", d);
     return 0;
 }

@@ -112,6 +112,24 @@ typedef struct {
 HG_API hg_status hg_kv_append(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
                        const void *v_new, void *stream);
 
+/* Rotary position embedding applied in the append / step prologue (SURVEY
+ * §8(f) NEXT-4 "fuse append + RoPE into the prologue"; the paper's models are
+ * Llama-family).  Rotate-half convention (Llama): with R = rotary_dim
+ * and f_i = theta^(-2i/R), a row x at absolute position p becomes, for i < R/2,
+ *   y[i]       = x[i] cos(p f_i) - x[i + R/2] sin(p f_i)
+ *   y[i + R/2] = x[i + R/2] cos(p f_i) + x[i] sin(p f_i)
+ * and y[i] = x[i] for i >= R.  Angles in fp64, rotation in fp32, result rounded
+ * to bf16 (the cache dtype; reading R24). */
+typedef struct {
+    double theta;         /* base: 1e4 (Llama-2), 5e5 (Llama-3) */
+    int32_t rotary_dim;   /* R: multiple of 16, <= head_dim; 0 = head_dim */
+} hg_rope;
+
+/* hg_kv_append with K rotated at its position p = c_i + j before it is
+ * written (V copied).  Same validation; HG_E_INVALID for a bad rope. */
+HG_API hg_status hg_kv_append_rope(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
+                            const void *v_new, const hg_rope *rope, void *stream);
+
 /* Tuning / test switches for hg_hybrid_attention_ex (zero-initialise for defaults). */
 typedef struct {
     int32_t split_tokens;       /* >0: fixed split-K chunk (multiple of B) for decode rows, making the
@@ -125,6 +143,10 @@ typedef struct {
                                    combine kernel [4,5] (bench.py's per-kernel roofline timing) */
     void *debug_trace;          /* NULL, or device int64[4096]: clock64 stamps of tcgen05 CTA 0's pipeline
                                    events (kernel development aid; see tc_attn.cu) */
+    const hg_rope *rope;        /* hg_hybrid_step only (NULL: none): q and k_new are pre-rotary; the
+                                   append prologue rotates k_new into the cache and q into a workspace
+                                   copy that the attention kernels read (cached keys were appended with
+                                   the same rope).  HG_E_INVALID in hg_hybrid_attention_ex. */
 } hg_attn_opts;
 
 /* Bytes of device workspace hg_hybrid_attention needs for this batch. */

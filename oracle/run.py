@@ -15,6 +15,15 @@ from synth.layout import history_steps, make_layout
 from synth.values import KIND_K, KIND_V, kv_values, q_values
 
 from . import OraclePool
+from .rope import rope_bf16
+
+
+def _k(spec, i, c0, c1, device):
+    """K rows of request i at positions [c0, c1) as the cache holds them (rotated when spec.rope)."""
+    k = kv_values(spec, i, c0, c1, KIND_K, device).cpu()
+    if getattr(spec, "rope", None):
+        k = rope_bf16(k, np.arange(c0, c1), *spec.rope)
+    return k
 
 
 def fill_pool(spec, lay, req_sel=None, pool=None, device="cpu"):
@@ -37,14 +46,14 @@ def fill_pool(spec, lay, req_sel=None, pool=None, device="cpu"):
         ks, vs = [], []
         for k in rows:
             i = st.req[k]
-            ks.append(kv_values(spec, i, st.c[k], st.c[k] + st.n[k], KIND_K, device).cpu())
+            ks.append(_k(spec, i, st.c[k], st.c[k] + st.n[k], device))
             vs.append(kv_values(spec, i, st.c[k], st.c[k] + st.n[k], KIND_V, device).cpu())
         pool.append([st.tables[k] for k in rows], [st.c[k] for k in rows],
                      [st.n[k] for k in rows], torch.cat(ks), torch.cat(vs))
     idx = [i for i in range(len(spec.requests)) if sel is None or i in sel]
     if idx:
-        ks = torch.cat([kv_values(spec, i, spec.requests[i].c, spec.requests[i].c + spec.requests[i].n,
-                                  KIND_K, device).cpu() for i in idx])
+        ks = torch.cat([_k(spec, i, spec.requests[i].c, spec.requests[i].c + spec.requests[i].n, device)
+                        for i in idx])
         vs = torch.cat([kv_values(spec, i, spec.requests[i].c, spec.requests[i].c + spec.requests[i].n,
                                   KIND_V, device).cpu() for i in idx])
         pool.append(lay.block_table[idx], [spec.requests[i].c for i in idx],
@@ -66,4 +75,7 @@ def run(spec, lay=None, req_sel=None, pool=None, device="cpu"):
     c = np.array([r.c for r in spec.requests], np.int32)
     n = np.array([r.n for r in spec.requests], np.int32)
     q = q_values(spec)
+    if getattr(spec, "rope", None):
+        pos = np.concatenate([np.arange(r.c, r.c + r.n) for r in spec.requests]) if spec.requests else []
+        q = rope_bf16(q, pos, *spec.rope)
     return pool.attention(lay.block_table, c, n, q, spec.H_q, req_sel=req_sel)

@@ -47,9 +47,13 @@ class hg_batch(ctypes.Structure):
                 ("new_len", P), ("is_offline", P), ("shared_prefix_blocks", P)]
 
 
+class hg_rope(ctypes.Structure):
+    _fields_ = [("theta", ctypes.c_double), ("rotary_dim", i32)]
+
+
 class hg_attn_opts(ctypes.Structure):
     _fields_ = [("split_tokens", i32), ("disable_prefix_pass", i32), ("disable_tc", i32), ("num_sms", i32),
-                ("events", P * 6), ("debug_trace", P)]
+                ("events", P * 6), ("debug_trace", P), ("rope", ctypes.POINTER(hg_rope))]
 
 
 class hg_plan_stats(ctypes.Structure):
@@ -79,6 +83,7 @@ _SIGS = {
     "hg_kv_num_free": ([P], i32),
     "hg_kv_refcount": ([P, i32], i32),
     "hg_kv_append": ([P, P, P, P, P], i32),
+    "hg_kv_append_rope": ([P, P, P, P, P, P], i32),
     "hg_hybrid_attention_workspace_size": ([P, P, i32, P], i32),
     "hg_hybrid_attention": ([P, P, i32, P, P, P, P, ctypes.c_size_t, P], i32),
     "hg_hybrid_attention_ex": ([P, P, i32, P, P, P, P, ctypes.c_size_t, P, P], i32),
@@ -236,15 +241,25 @@ def hg_kv_append(pool: KVPool, batch: Batch, k_new, v_new, stream=None) -> None:
     _check(lib().hg_kv_append(pool.h, batch.ref(), _ptr(k_new), _ptr(v_new), _stream_ptr(stream)))
 
 
+def hg_kv_append_rope(pool: KVPool, batch: Batch, k_new, v_new, rope: hg_rope, stream=None) -> None:
+    _check(lib().hg_kv_append_rope(pool.h, batch.ref(), _ptr(k_new), _ptr(v_new), ctypes.byref(rope),
+                                   _stream_ptr(stream)))
+
+
 def hg_hybrid_attention_workspace_size(pool: KVPool, batch: Batch, num_q_heads: int) -> int:
     n = ctypes.c_size_t()
     _check(lib().hg_hybrid_attention_workspace_size(pool.h, batch.ref(), num_q_heads, ctypes.byref(n)))
     return int(n.value)
 
 
-def make_opts(split_tokens=0, disable_prefix_pass=False, disable_tc=False, num_sms=0, events=None) -> hg_attn_opts:
-    """events: optional 6 torch.cuda.Event(enable_timing=True) (or None entries), see hg_attn_opts."""
+def make_opts(split_tokens=0, disable_prefix_pass=False, disable_tc=False, num_sms=0, events=None,
+              rope: Optional[hg_rope] = None) -> hg_attn_opts:
+    """events: optional 6 torch.cuda.Event(enable_timing=True) (or None entries), see hg_attn_opts.
+    rope: hg_rope applied in the hg_hybrid_step prologue (kept alive by the returned struct)."""
     o = hg_attn_opts(split_tokens, int(disable_prefix_pass), int(disable_tc), num_sms)
+    if rope is not None:
+        o._rope_ref = rope
+        o.rope = ctypes.pointer(rope)
     if events is not None:
         for k, ev in enumerate(events):
             if ev is not None:

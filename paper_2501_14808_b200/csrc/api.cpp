@@ -239,6 +239,16 @@ static hg_status append_impl(hg_kv_pool *pool, const BatchView &v, const void *k
                          pool->desc.num_kv_heads, pool->desc.head_dim, st);
 }
 
+static hg_status rope_args(const hg_rope *r, int d, RopeArgs *out) {
+    const int rot = r->rotary_dim ? r->rotary_dim : d;
+    if (!(r->theta > 0) || rot <= 0 || rot > d || rot % 16 || rot > 256)
+        return fail(HG_E_INVALID, "rope: theta %g, rotary_dim %d (head_dim %d): need theta > 0, R %% 16 == 0, R <= d",
+                    r->theta, r->rotary_dim, d);
+    out->theta = r->theta;
+    out->rot = rot;
+    return HG_OK;
+}
+
 // Small device scratch for append slots (pool-independent, grows on demand).
 static thread_local void *g_slot_dev = nullptr;
 static thread_local size_t g_slot_cap = 0;
@@ -270,6 +280,54 @@ extern "C" hg_status hg_kv_append(hg_kv_pool *pool, const hg_batch *batch, const
         g_slot_cap = cap;
     }
     return append_impl(pool, v, k_new, v_new, g_slot_dev, (cudaStream_t)stream);
+}
+
+extern "C" hg_status hg_kv_append_rope(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
+                                       const void *v_new, const hg_rope *rope, void *stream) {
+    if (!pool || !rope) return fail(HG_E_INVALID, "pool / rope is NULL");
+    RopeArgs ra;
+    hg_status s = rope_args(rope, pool->desc.head_dim, &ra);
+    if (s) return s;
+    BatchView v;
+    s = view_batch(batch, &v);
+    if (s) return s;
+    s = validate(v, pool->desc.block_size, pool->desc.num_blocks, -1, 0, true);
+    if (s) return s;
+    s = sticky_check();
+    if (s) return s;
+    int64_t T = 0;
+    for (int i = 0; i < v.R; ++i) T += v.n[i];
+    if (T == 0) return HG_OK;
+    if (!k_new || !v_new) return fail(HG_E_INVALID, "k_new / v_new NULL");
+    const int B = pool->desc.block_size;
+    // staged: slot int64 [T], then position int32 [T]
+    std::vector<uint8_t> img((size_t)T * 12);
+    int64_t *slot = (int64_t *)img.data();
+    int32_t *pos = (int32_t *)(img.data() + (size_t)T * 8);
+    int64_t t = 0;
+    for (int i = 0; i < v.R; ++i)
+        for (int j = 0; j < v.n[i]; ++j, ++t) {
+            const int64_t p = (int64_t)v.c[i] + j;
+            slot[t] = (int64_t)v.bt[(int64_t)i * v.W + p / B] * B + p % B;
+            pos[t] = (int32_t)p;
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (g_slot_cap < img.size()) {
+        if (g_slot_dev) {
+            cudaStreamSynchronize(st);
+            cudaFree(g_slot_dev);
+        }
+        size_t cap = std::max<size_t>(img.size() * 2, 1 << 16);
+        s = cuda_check(cudaMalloc(&g_slot_dev, cap), "cudaMalloc(slots)");
+        if (s) { g_slot_dev = nullptr; g_slot_cap = 0; return s; }
+        g_slot_cap = cap;
+    }
+    s = stage_h2d(pool, g_slot_dev, img.data(), img.size(), st);
+    if (s) return s;
+    return launch_rope_append((const uint16_t *)k_new, (const uint16_t *)v_new, (uint16_t *)pool->desc.k_cache,
+                              (uint16_t *)pool->desc.v_cache, (const int64_t *)g_slot_dev,
+                              (const int32_t *)((uint8_t *)g_slot_dev + (size_t)T * 8), (int)T,
+                              pool->desc.num_kv_heads, pool->desc.head_dim, ra, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -328,6 +386,12 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         return HG_OK;
     }
     if (!q || (!out && !outs)) return fail(HG_E_INVALID, "q / out NULL");
+    RopeArgs ra;
+    if (o && o->rope) {
+        if (!fused) return fail(HG_E_INVALID, "rope is applied in the hg_hybrid_step prologue only");
+        s = rope_args(o->rope, pool->desc.head_dim, &ra);
+        if (s) return s;
+    }
     if (fused && (!k_new || !v_new)) return fail(HG_E_INVALID, "k_new / v_new NULL");
     if (!ws || ws_bytes < plan.total_bytes)
         return fail(HG_E_INVALID, "workspace %zu bytes < required %zu", ws_bytes, plan.total_bytes);
@@ -389,7 +453,14 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     // (its CTAs are placed first), the split-K kernel on a side stream forked
     // after the descriptor copy; the combine waits for both.
     if (fused) {
-        s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st);
+        if (ra.rot) {   // NEXT-4: append + RoPE prologue; the attention reads the rotated Q copy
+            uint16_t *q_rot = (uint16_t *)(w + plan.off_qrot);
+            s = launch_rope_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, (const uint16_t *)q,
+                                       q_rot, plan.T, ra, st);
+            p.q = q_rot;
+        } else {
+            s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st);
+        }
         if (s) return s;
         ++kernels;
     }

@@ -115,7 +115,7 @@ struct Plan {
     int32_t tc_ctas = 0;        // persistent tcgen05 grid chosen by the planner
     // device layout (byte offsets inside the workspace)
     size_t off_reqs = 0, off_bt = 0, off_sk = 0, off_tc = 0, off_rows = 0, off_cbase = 0,
-           off_comb = 0, off_tcoff = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
+           off_comb = 0, off_tcoff = 0, off_qrot = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
 };
 
 // ---- host helpers (host.cpp) ------------------------------------------------
@@ -159,6 +159,18 @@ hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *
                         uint16_t *v_cache, const int64_t *slot, int T, int H_kv, int d,
                         void *stream);
 hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream);
+// RoPE in the append prologue (NEXT-4): K rotated at its position before it is
+// written, V copied, and (q_dst != NULL) Q rotated into q_dst.  Token slots and
+// positions from the attention descriptors (fused step) or from arrays.
+struct RopeArgs {
+    double theta = 0;
+    int rot = 0;   // rotary dims R (multiple of 16); 0 = none
+};
+hg_status launch_rope_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new,
+                                 const uint16_t *q_src, uint16_t *q_dst, int T, const RopeArgs &r, void *stream);
+hg_status launch_rope_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache, uint16_t *v_cache,
+                             const int64_t *slot, const int32_t *pos, int T, int H_kv, int d, const RopeArgs &r,
+                             void *stream);
 hg_status launch_splitk(const AttnParams &p, void *stream);
 hg_status launch_combine(const AttnParams &p, void *stream);
 hg_status launch_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v, void *stream);

@@ -456,6 +456,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     off = align_up(off, 256);
     p->off_part_o = off;   off = align_up(off + sizeof(float) * (size_t)p->n_slots * d, 256);
     p->off_part_lse = off; off = align_up(off + sizeof(float) * (size_t)p->n_slots, 256);
+    p->off_qrot = off;     off = align_up(off + (size_t)T * H_q * d * 2, 256);   // rotated Q (rope step)
     p->total_bytes = std::max<size_t>(off, 256);
     return HG_OK;
 }

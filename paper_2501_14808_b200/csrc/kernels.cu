@@ -156,6 +156,112 @@ __device__ __forceinline__ uint32_t swz(int row, int ch) {
 }
 
 // ----------------------------------------------------------------------------
+// NEXT-4 prologue: append + rotary position embedding (include/hygen.h hg_rope).
+// One CTA per token: the R/2 (cos, sin) of its position are computed once in
+// fp64 into shared memory; each thread then rotates a pair of 16-byte chunks
+// (dims [8c, 8c+8) and [8c + R/2, 8c + R/2 + 8)) of one head in fp32 and
+// rounds to bf16.  Dims >= R and V are copied.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void rope_chunk(uint4 &lo, uint4 &hi, const float2 *cs) {
+    uint32_t *a = reinterpret_cast<uint32_t *>(&lo), *b = reinterpret_cast<uint32_t *>(&hi);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&a[e]));
+        const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&b[e]));
+        const float2 c0 = cs[2 * e], c1 = cs[2 * e + 1];
+        a[e] = pack_bf16(x.x * c0.x - y.x * c0.y, x.y * c1.x - y.y * c1.y);
+        b[e] = pack_bf16(y.x * c0.x + x.x * c0.y, y.y * c1.x + x.y * c1.y);
+    }
+}
+
+template <bool DESC>
+__global__ void __launch_bounds__(256) rope_append_kernel(const uint4 *__restrict__ k_new,
+                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_cache,
+                                                          uint4 *__restrict__ v_cache, const AttnParams p,
+                                                          const int64_t *__restrict__ slot_arr,
+                                                          const int32_t *__restrict__ pos_arr,
+                                                          const uint4 *__restrict__ q_src, uint4 *__restrict__ q_dst,
+                                                          int H_q, int H_kv, int cpr, double theta, int rot) {
+    __shared__ float2 cs[128];
+    const int t = blockIdx.x;
+    int64_t blk, off;
+    int pos;
+    if (DESC) {
+        const ReqDev rq = p.reqs[p.tok[t].req];
+        pos = rq.c + (t - rq.cu_q);
+        blk = p.bt_flat[rq.bt_off + pos / kBlock];
+        off = pos % kBlock;
+    } else {
+        const int64_t sl = slot_arr[t];
+        blk = sl / kBlock;
+        off = sl % kBlock;
+        pos = pos_arr[t];
+    }
+    const int half = rot / 2, hc = half / 8;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        double sv, cv;
+        sincos((double)pos * pow(theta, -2.0 * i / rot), &sv, &cv);
+        cs[i] = make_float2((float)cv, (float)sv);
+    }
+    __syncthreads();
+    const int units = cpr - hc;   // per head: hc rotated chunk pairs + the unrotated chunks
+    for (int u = threadIdx.x; u < H_kv * units; u += blockDim.x) {
+        const int g = u / units, c = u - g * units;
+        const int64_t src = ((int64_t)t * H_kv + g) * cpr;
+        const int64_t dst = ((blk * H_kv + g) * kBlock + off) * cpr;
+        if (c < hc) {
+            uint4 lo = k_new[src + c], hi = k_new[src + c + hc];
+            const uint4 vl = v_new[src + c], vh = v_new[src + c + hc];
+            rope_chunk(lo, hi, cs + 8 * c);
+            k_cache[dst + c] = lo;
+            k_cache[dst + c + hc] = hi;
+            v_cache[dst + c] = vl;
+            v_cache[dst + c + hc] = vh;
+        } else {
+            const int cc = c + hc;
+            k_cache[dst + cc] = k_new[src + cc];
+            v_cache[dst + cc] = v_new[src + cc];
+        }
+    }
+    if (q_dst) {
+        for (int u = threadIdx.x; u < H_q * units; u += blockDim.x) {
+            const int h = u / units, c = u - h * units;
+            const int64_t base = ((int64_t)t * H_q + h) * cpr;
+            if (c < hc) {
+                uint4 lo = q_src[base + c], hi = q_src[base + c + hc];
+                rope_chunk(lo, hi, cs + 8 * c);
+                q_dst[base + c] = lo;
+                q_dst[base + c + hc] = hi;
+            } else {
+                q_dst[base + c + hc] = q_src[base + c + hc];
+            }
+        }
+    }
+}
+
+hg_status launch_rope_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new,
+                                 const uint16_t *q_src, uint16_t *q_dst, int T, const RopeArgs &r, void *stream) {
+    if (T == 0) return HG_OK;
+    rope_append_kernel<true><<<T, 256, 0, (cudaStream_t)stream>>>(
+        (const uint4 *)k_new, (const uint4 *)v_new, (uint4 *)p.k_cache, (uint4 *)p.v_cache, p, nullptr, nullptr,
+        (const uint4 *)q_src, (uint4 *)q_dst, p.H_q, p.H_kv, p.d / 8, r.theta, r.rot);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "rope append launch: %s", cudaGetErrorString(e));
+}
+
+hg_status launch_rope_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache, uint16_t *v_cache,
+                             const int64_t *slot, const int32_t *pos, int T, int H_kv, int d, const RopeArgs &r,
+                             void *stream) {
+    if (T == 0) return HG_OK;
+    AttnParams p{};
+    rope_append_kernel<false><<<T, 256, 0, (cudaStream_t)stream>>>(
+        (const uint4 *)k_new, (const uint4 *)v_new, (uint4 *)k_cache, (uint4 *)v_cache, p, slot, pos, nullptr,
+        nullptr, 0, H_kv, d / 8, r.theta, r.rot);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "rope append launch: %s", cudaGetErrorString(e));
+}
+
+// ----------------------------------------------------------------------------
 // a.6 split-K attention item kernel
 // ----------------------------------------------------------------------------
 #ifndef HG_SK_WARPS

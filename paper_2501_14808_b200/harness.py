@@ -7,6 +7,7 @@ values come from synth's counter-based generator evaluated on the device.
 """
 from __future__ import annotations
 
+import ctypes
 import numpy as np
 import torch
 
@@ -66,7 +67,10 @@ class Workload:
                 shared = [st.shared[k] for k in sel]
                 b = hg.Batch(np.array([st.tables[k] for k in sel], np.int32), [st.c[k] for k in sel],
                              [st.n[k] for k in sel], None, shared)
-                hg.hg_kv_append(self.pool, b, ks, vs)
+                if spec.rope:   # cached keys were appended rotated (NEXT-4 prologue)
+                    hg.hg_kv_append_rope(self.pool, b, ks, vs, self.rope())
+                else:
+                    hg.hg_kv_append(self.pool, b, ks, vs)
                 start = end
         torch.cuda.synchronize(self.device)
 
@@ -85,8 +89,15 @@ class Workload:
         hg.hg_hybrid_attention(self.pool, self.batch, self.spec.H_q, self.q, self.out,
                                self.lse if lse else None, self.workspace(opts), stream, opts)
 
+    def rope(self):
+        return hg.hg_rope(float(self.spec.rope[0]), int(self.spec.rope[1])) if self.spec.rope else None
+
     def step(self, opts=None, stream=None):
-        """One serving iteration: fused append + attention (hg_hybrid_step)."""
+        """One serving iteration: fused append (+ RoPE prologue when spec.rope) + attention (hg_hybrid_step)."""
+        if self.spec.rope:
+            opts = opts or hg.make_opts()
+            opts._rope_ref = self.rope()
+            opts.rope = ctypes.pointer(opts._rope_ref)
         hg.hg_hybrid_step(self.pool, self.batch, self.spec.H_q, self.q, self.k_new, self.v_new, self.out, self.lse,
                           self.workspace(opts), stream, opts)
 

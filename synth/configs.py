@@ -10,7 +10,7 @@ Nothing here computes attention or indexes the paged layout.
 from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
@@ -43,6 +43,9 @@ class BatchSpec:
     # child's prefix that are the parent's); a member of the child holds the
     # parent's content on [0, split) and the child's on [split, prefix_tokens)
     group_parent: Dict[int, Tuple[int, int]] = field(default_factory=dict)
+    # rotary embedding (NEXT-4 prologue): (theta, rotary_dim) or None; values from
+    # synth are pre-rotary, the library / oracle rotate Q and K at their positions
+    rope: Optional[Tuple[float, int]] = None
 
     @property
     def T(self) -> int:

@@ -247,3 +247,95 @@ def test_sampled_selection_matches_full():
     part, _ = run(spec, req_sel=sel)
     for i in sel:
         assert np.array_equal(part[rows_of(spec, i)], full[rows_of(spec, i)])
+
+
+# ---- RoPE (NEXT-4 prologue, reading R24) ------------------------------------------------
+from oracle.rope import rope, rope_bf16   # noqa: E402
+
+
+def test_rope_identity_at_position_zero():
+    x = np.random.default_rng(0).standard_normal((3, 2, 64))
+    assert np.array_equal(rope(x, [0, 0, 0], 1e4), x)
+
+
+@pytest.mark.parametrize("rot", [0, 32])
+def test_rope_keeps_pair_norms_and_tail(rot):
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((5, 3, 64))
+    pos = rng.integers(0, 20000, 5)
+    y = rope(x, pos, 5e5, rot)
+    R = rot or 64
+    h = R // 2
+    np.testing.assert_allclose(x[..., :h] ** 2 + x[..., h:R] ** 2, y[..., :h] ** 2 + y[..., h:R] ** 2,
+                               rtol=1e-12, atol=1e-12)
+    assert np.array_equal(y[..., R:], x[..., R:])
+
+
+def test_rope_2d_is_the_rotation_matrix():
+    """R = d = 2: f_0 = 1, so position p rotates (x0, x1) by p radians."""
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((4, 1, 2))
+    pos = np.array([0, 1, 7, 1000])
+    y = rope(x, pos, 1e4)
+    for k, p in enumerate(pos):
+        M = np.array([[np.cos(p), -np.sin(p)], [np.sin(p), np.cos(p)]])
+        np.testing.assert_allclose(y[k, 0], M @ x[k, 0], rtol=0, atol=1e-12)
+
+
+def test_rope_relative_position_property():
+    """q(p + s) . k(p' + s) = q(p) . k(p'): scores depend on p - p' only."""
+    rng = np.random.default_rng(3)
+    q, k = rng.standard_normal((1, 1, 128)), rng.standard_normal((1, 1, 128))
+    for p, pp, sh in [(5, 3, 100), (4000, 17, 9000), (0, 8191, 8000)]:
+        a = (rope(q, [p + sh], 5e5) * rope(k, [pp + sh], 5e5)).sum()
+        b = (rope(q, [p], 5e5) * rope(k, [pp], 5e5)).sum()
+        assert abs(a - b) < 1e-9 * (1 + abs(b))
+
+
+def _rope_spec(spec, theta=1e4, rot=0):
+    return spec.with_(rope=(theta, rot))
+
+
+def brute_check_rope(spec, tol=1e-13):
+    """Paged oracle with rope == dense brute force on rotated logical sequences."""
+    out, lse = run(spec)
+    q = q_values(spec)
+    pos = np.concatenate([np.arange(r.c, r.c + r.n) for r in spec.requests])
+    q = f64(rope_bf16(q, pos, *spec.rope))
+    for i, r in enumerate(spec.requests):
+        K = f64(rope_bf16(kv_values(spec, i, 0, r.c + r.n, KIND_K), np.arange(r.c + r.n), *spec.rope))
+        V = f64(kv_values(spec, i, 0, r.c + r.n, KIND_V))
+        o_ref, l_ref = attention_dense(q[rows_of(spec, i)], K, V, r.c)
+        np.testing.assert_allclose(out[rows_of(spec, i)], o_ref, rtol=0, atol=tol)
+        np.testing.assert_allclose(lse[rows_of(spec, i)], l_ref, rtol=0, atol=tol)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_brute_force_with_rope(seed):
+    brute_check_rope(_rope_spec(make_fuzz(seed), theta=[1e4, 5e5][seed % 2], rot=[0, 32][seed // 2 % 2]))
+
+
+def test_brute_force_nested_with_rope():
+    brute_check_rope(_rope_spec(make_fuzz_nested(2), theta=5e5))
+
+
+def test_rope_chunked_equals_whole_and_decode_bitwise():
+    """Positions are absolute: with rope, chunked prefill still equals the whole
+    prefill and a decode equals the last prefill row, bit for bit."""
+    N = 57
+    whole = BatchSpec("w", 2, 2, 64, 16, 4, [Request(0, N, cid=3)], rope=(1e4, 0))
+    o_whole, _ = run(whole)
+    dec = BatchSpec("d", 2, 2, 64, 16, 4, [Request(N - 1, 1, cid=3)], rope=(1e4, 0))
+    o_dec, _ = run(dec)
+    assert np.array_equal(o_dec[0], o_whole[N - 1])
+    lay = make_layout(whole)
+    pool = OraclePool(lay.num_blocks, 2, 16, 64)
+    outs, c = [], 0
+    for n in (16, 33, 8):
+        part = BatchSpec("p", 2, 2, 64, 16, 4, [Request(c, n, cid=3)], rope=(1e4, 0))
+        pool = fill_pool(part, lay, pool=pool)
+        q = rope_bf16(q_values(part), np.arange(c, c + n), 1e4)
+        o, _ = pool.attention(lay.block_table, [c], [n], q, 2)
+        outs.append(o)
+        c += n
+    assert np.array_equal(np.concatenate(outs), o_whole)

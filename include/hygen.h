@@ -237,6 +237,30 @@ HG_API hg_status hg_comm_destroy(hg_comm *comm);
  * Calls whose T*H_q*d*2 exceeds `bytes` fall back to the NCCL path (HG_E_INVALID
  * if the communicator has none).  Readers of the window must be ordered before
  * the next hg_hybrid_attention_tp on the same stream. */
+/* TP-native attention epilogue: the output projection of
+ * the sharded attention fused with its reduce-scatter.  Rank r holds
+ * O_r [T][K] (its heads' attention output, K = H_q/G * d) and the matching rows
+ * of the projection W_r [K][N] (row-major, N = hidden); the layer output is
+ * Y = sum_r O_r W_r [T][N], reduce-scattered by tokens: rank o receives rows
+ * [o T/G, (o+1) T/G) into y_shard.  One tcgen05 GEMM kernel computes O_r W_r
+ * and its epilogue stores each finished row (bf16) into the owning rank's
+ * receive slot [r] of the peer window (so the transfer overlaps the GEMM),
+ * then after a flag barrier each rank sums its G slots in fp32 (reading R25:
+ * partials are rounded to bf16 once, as a bf16 reduce-scatter would carry
+ * them).  G = 1: y_shard = O W directly.  Needs K % 64 == 0 and N % 128 == 0
+ * (HG_E_UNSUPPORTED) and, for G > 1, an open window of G*ceil(T/G)*N*2 bytes. */
+HG_API hg_status hg_out_proj_rs(hg_comm *comm, int32_t T, int32_t K, int32_t N, const void *o_local,
+                         const void *w_local, void *y_shard, void *stream);
+/* hg_hybrid_attention on this rank's heads (O kept in the workspace) followed by
+ * hg_out_proj_rs: the sharded attention layer without an output all-gather. */
+HG_API hg_status hg_hybrid_attention_tp_proj_workspace_size(const hg_kv_pool *pool, const hg_comm *comm,
+                                                     const hg_batch *batch, int32_t num_q_heads_total,
+                                                     size_t *bytes);
+HG_API hg_status hg_hybrid_attention_tp_proj(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
+                                      int32_t num_q_heads_total, const void *q_local, const void *w_local,
+                                      int32_t N, void *y_shard, void *workspace, size_t workspace_bytes,
+                                      void *stream);
+
 #define HG_IPC_HANDLE_BYTES 64
 HG_API hg_status hg_comm_window_create(hg_comm *comm, size_t bytes, void *ipc_handle_out, void **window_out);
 HG_API hg_status hg_comm_window_open(hg_comm *comm, const void *handles);

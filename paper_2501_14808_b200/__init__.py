@@ -97,6 +97,9 @@ _SIGS = {
     "hg_comm_destroy": ([P], i32),
     "hg_comm_window_create": ([P, ctypes.c_size_t, P, P], i32),
     "hg_comm_window_open": ([P, P], i32),
+    "hg_out_proj_rs": ([P, i32, i32, i32, P, P, P, P], i32),
+    "hg_hybrid_attention_tp_proj_workspace_size": ([P, P, P, i32, P], i32),
+    "hg_hybrid_attention_tp_proj": ([P, P, P, i32, P, P, i32, P, P, ctypes.c_size_t, P], i32),
     "hg_hybrid_attention_tp_workspace_size": ([P, P, P, i32, P], i32),
     "hg_hybrid_attention_tp": ([P, P, P, i32, P, P, P, ctypes.c_size_t, P], i32),
     "hg_batch_features": ([P, i32, P], i32),
@@ -402,6 +405,24 @@ def hg_hybrid_attention_tp(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_t
     _check(lib().hg_hybrid_attention_tp(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local),
                                         _ptr(out_gathered), _ptr(workspace),
                                         workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+
+
+def hg_out_proj_rs(comm: Comm, T: int, K: int, N: int, o_local, w_local, y_shard, stream=None) -> None:
+    _check(lib().hg_out_proj_rs(comm.h, T, K, N, _ptr(o_local), _ptr(w_local), _ptr(y_shard), _stream_ptr(stream)))
+
+
+def hg_hybrid_attention_tp_proj_workspace_size(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_total: int) -> int:
+    n = ctypes.c_size_t()
+    _check(lib().hg_hybrid_attention_tp_proj_workspace_size(pool.h, comm.h, batch.ref(), num_q_heads_total,
+                                                            ctypes.byref(n)))
+    return int(n.value)
+
+
+def hg_hybrid_attention_tp_proj(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_total: int, q_local, w_local,
+                                N: int, y_shard, workspace, stream=None) -> None:
+    _check(lib().hg_hybrid_attention_tp_proj(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local),
+                                             _ptr(w_local), N, _ptr(y_shard), _ptr(workspace),
+                                             workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
 
 
 # ---- predictor -------------------------------------------------------------------

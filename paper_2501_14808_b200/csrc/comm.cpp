@@ -65,6 +65,9 @@ using namespace hg;
 namespace hg {
 hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
                               unsigned long long epoch, void *stream);
+hg_status launch_out_proj(const uint16_t *o, const uint16_t *w, int M, int N, int K, int G, int rank, int rows_max,
+                          uint16_t *const *dst, void *stream);
+hg_status launch_rs_reduce(const uint16_t *recv, uint16_t *y, int rows, int rows_max, int N, int G, void *stream);
 hg_status launch_gather_transpose(const uint16_t *src, uint16_t *dst, int G, int T, int row_elems, void *stream);
 int pool_num_kv_heads(const hg_kv_pool *p);
 int pool_head_dim(const hg_kv_pool *p);
@@ -237,4 +240,76 @@ extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, con
     }
     // [G][T][Hl*d] -> [T][G*Hl*d]
     return launch_gather_transpose(gather, (uint16_t *)out_gathered, G, (int)T, Hl * d, stream);
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-4: TP-native epilogue -- output projection + reduce-scatter (gemm.cu)
+// ---------------------------------------------------------------------------
+extern "C" hg_status hg_out_proj_rs(hg_comm *comm, int32_t T, int32_t K, int32_t N, const void *o_local,
+                                    const void *w_local, void *y_shard, void *stream) {
+    if (!comm || T < 0 || K <= 0 || N <= 0) return fail(HG_E_INVALID, "bad arguments");
+    if (K % 64 || N % 128)
+        return fail(HG_E_UNSUPPORTED, "out-proj: K %d must be a multiple of 64 and N %d of 128", K, N);
+    if (T == 0) return HG_OK;
+    if (!o_local || !w_local || !y_shard) return fail(HG_E_INVALID, "NULL buffer");
+    const int G = comm->world;
+    if (cudaSetDevice(comm->device) != cudaSuccess) return fail(HG_E_CUDA, "cudaSetDevice(%d)", comm->device);
+    if (G == 1) {
+        uint16_t *dst[1] = {(uint16_t *)y_shard};
+        return launch_out_proj((const uint16_t *)o_local, (const uint16_t *)w_local, T, N, K, 1, 0, T, dst, stream);
+    }
+    const int rows_max = (T + G - 1) / G;
+    const size_t need = (size_t)G * rows_max * N * 2;
+    if (!comm->open || comm->win_bytes < need)
+        return fail(HG_E_INVALID, "out-proj reduce-scatter needs an open peer window of %zu bytes", need);
+    unsigned long long *fl[kMaxOuts];
+    for (int k = 0; k < G; ++k) fl[k] = (unsigned long long *)comm->peer[k];
+    unsigned long long *mine = (unsigned long long *)comm->win;
+    // entry: no rank overwrites a receive slot its owner may still be reducing
+    hg_status s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
+    if (s) return s;
+    uint16_t *dst[kMaxOuts];
+    for (int k = 0; k < G; ++k) dst[k] = (uint16_t *)(comm->peer[k] + kWinHdr);
+    s = launch_out_proj((const uint16_t *)o_local, (const uint16_t *)w_local, T, N, K, G, comm->rank, rows_max, dst,
+                        stream);
+    if (s) return s;
+    s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);   // every partial row has landed
+    if (s) return s;
+    const int r0 = (comm->rank * T) / G, r1 = ((comm->rank + 1) * T) / G;
+    return launch_rs_reduce((const uint16_t *)(comm->win + kWinHdr), (uint16_t *)y_shard, r1 - r0, rows_max, N, G,
+                            stream);
+}
+
+extern "C" hg_status hg_hybrid_attention_tp_proj_workspace_size(const hg_kv_pool *pool, const hg_comm *comm,
+                                                                const hg_batch *batch, int32_t H_q, size_t *bytes) {
+    if (!pool || !comm || !batch || !bytes) return fail(HG_E_INVALID, "NULL argument");
+    if (H_q % comm->world) return fail(HG_E_INVALID, "num_q_heads %d not divisible by world %d", H_q, comm->world);
+    size_t attn = 0;
+    hg_status s = hg_hybrid_attention_workspace_size(pool, batch, H_q / comm->world, &attn);
+    if (s) return s;
+    int64_t T = 0;
+    for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
+    *bytes = al256(attn) + al256((size_t)T * (H_q / comm->world) * pool_head_dim(pool) * 2);
+    return HG_OK;
+}
+
+extern "C" hg_status hg_hybrid_attention_tp_proj(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
+                                                 const void *q_local, const void *w_local, int32_t N, void *y_shard,
+                                                 void *workspace, size_t workspace_bytes, void *stream) {
+    if (!pool || !comm || !batch) return fail(HG_E_INVALID, "NULL argument");
+    size_t need = 0;
+    hg_status s = hg_hybrid_attention_tp_proj_workspace_size(pool, comm, batch, H_q, &need);
+    if (s) return s;
+    if (!workspace || workspace_bytes < need)
+        return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    const int Hl = H_q / comm->world, d = pool_head_dim(pool);
+    int64_t T = 0;
+    for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
+    size_t attn = 0;
+    s = hg_hybrid_attention_workspace_size(pool, batch, Hl, &attn);
+    if (s) return s;
+    uint16_t *o_local = (uint16_t *)((uint8_t *)workspace + al256(attn));   // [T][Hl][d]
+    s = hg_hybrid_attention(pool, batch, Hl, q_local, o_local, nullptr, workspace, attn, stream);
+    if (s) return s;
+    return hg_out_proj_rs(comm, (int32_t)T, Hl * d, N, o_local, w_local, y_shard, stream);
 }

@@ -131,3 +131,13 @@ def q_values(spec, device="cpu", requests=None) -> torch.Tensor:
     if not parts:
         return torch.empty((0, spec.H_q, spec.d), dtype=torch.bfloat16, device=device)
     return torch.cat(parts, 0)
+
+
+KIND_O, KIND_W = 3, 4
+
+
+def matrix(seed: int, kind: int, tag: int, rows: int, cols: int, scale: float = 1.0, device="cpu") -> torch.Tensor:
+    """A seeded bf16 [rows][cols] matrix (N(0,1)-scale, times ``scale``) from the
+    same counter-based generator: the O_r / W_r inputs of the NEXT-4 projection."""
+    pos = torch.arange(rows, dtype=torch.int64)
+    return gen_block(seed, kind, tag, pos, 1, cols, scale=scale, device=device).reshape(rows, cols)

@@ -1,0 +1,180 @@
+"""NEXT-4 TP-native epilogue: output projection fused with its reduce-scatter
+(hg_out_proj_rs, hg_hybrid_attention_tp_proj) against oracle/outproj.py.
+
+Bound (reading R25): bf16 inputs, fp32 accumulation, each rank's partial rows
+rounded to bf16 once, fp32 sum, bf16 output.  Each of the G partials and the
+output adds at most half a bf16 ulp (2^-9 relative) of its own magnitude, and
+the partials are at most ~2x the output here, so max-abs <= (2G + 1) 2^-9
+max|Y|; rel-L2 <= 5e-3 (N(0,1)-scale outputs: W scaled by 1/sqrt(K_total)).  Two ranks run as two
+processes on the same GPU (CUDA IPC maps the windows as it would across NVLink).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+REL_L2 = 5e-3
+
+
+def max_abs_bound(ref, G):
+    return (2 * G + 1) * 2.0 ** -9 * max(float(np.abs(ref).max()), 1e-30)
+
+
+def _inputs(seed, G, T, K_tot, N, device="cuda"):
+    from synth.values import KIND_O, KIND_W, matrix
+    K = K_tot // G
+    O = [matrix(seed, KIND_O, r, T, K, device=device) for r in range(G)]
+    W = [matrix(seed, KIND_W, r, K, N, scale=1.0 / np.sqrt(K_tot), device=device) for r in range(G)]
+    return O, W
+
+
+def _check(got, ref):
+    got = got.float().cpu().double().numpy()
+    rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+    mx = np.abs(got - ref).max() if got.size else 0.0
+    assert rel <= REL_L2 and mx <= max_abs_bound(ref, 1), (rel, mx)
+
+
+@pytest.mark.parametrize("T,K,N", [(1, 64, 256), (100, 1024, 512), (576, 4096, 4096), (768, 1024, 8192),
+                                   (300, 128, 256)])
+def test_out_proj_single_rank(T, K, N):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_14808_b200 as hg
+    from oracle.outproj import out_proj_rs
+    comm = hg.Comm(None, 0, 1, torch.cuda.current_device())
+    O, W = _inputs(1, 1, T, K, N)
+    y = torch.full((T, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    hg.hg_out_proj_rs(comm, T, K, N, O[0], W[0], y)
+    torch.cuda.synchronize()
+    ref = out_proj_rs([O[0].cpu().double().numpy()], [W[0].cpu().double().numpy()])[0]
+    _check(y, ref)
+    comm.close()
+
+
+def test_out_proj_unsupported_shapes():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_14808_b200 as hg
+    comm = hg.Comm(None, 0, 1, torch.cuda.current_device())
+    O, W = _inputs(1, 1, 8, 64, 256)
+    y = torch.empty((8, 256), dtype=torch.bfloat16, device="cuda")
+    for K, N in [(48, 256), (64, 200)]:
+        with pytest.raises(hg.HgError) as e:
+            hg.hg_out_proj_rs(comm, 8, K, N, O[0], W[0], y)
+        assert e.value.status == hg.HG_E_UNSUPPORTED
+    comm.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2501_14808_b200 as hg
+        from oracle.outproj import out_proj_rs, shard_rows
+        from paper_2501_14808_b200.harness import Workload
+        from synth.configs import make_config, make_fuzz
+        torch.cuda.set_device(0)
+        comm = hg.Comm(None, rank, world, 0)
+        hs = [None] * world
+        dist.all_gather_object(hs, comm.hg_comm_window_create(32 << 20))
+        comm.hg_comm_window_open(hs)
+        res = []
+        # (1) the projection alone, several shapes, repeated (epochs advance)
+        for (T, K_tot, N) in [(576, 4096, 4096), (33, 256, 512), (768, 2048, 8192)]:
+            O, W = _inputs(7, world, T, K_tot, N)
+            ref = out_proj_rs([o.cpu().double().numpy() for o in O], [w.cpu().double().numpy() for w in W])[rank]
+            a, b = shard_rows(T, world, rank)
+            for _ in range(2):
+                y = torch.full((b - a, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+                hg.hg_out_proj_rs(comm, T, K_tot // world, N, O[rank], W[rank], y)
+                torch.cuda.synchronize()
+                got = y.float().cpu().double().numpy()
+                rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+                res.append(("proj", T, bool(rel <= REL_L2 and np.abs(got - ref).max() <= max_abs_bound(ref, world)),
+                            float(rel),
+                            float(np.abs(got - ref).max()), float(np.abs(ref).max())))
+                dist.barrier()
+        # (2) the sharded attention layer: local heads' attention -> projection -> reduce-scatter
+        for name in ("fuzz5", "c3"):
+            spec = make_config(name, 0) if name == "c3" else make_fuzz(5, H_kv=2, G_q=4, d=128)
+            if name == "c3":
+                spec = spec.with_(requests=spec.requests[:1] + spec.requests[1:257:16])
+            wl = Workload(spec)
+            wl.append()   # the new tokens' K/V in the cache (the step's append)
+            torch.cuda.synchronize()
+            Hk, Hq, d = spec.H_kv // world, spec.H_q // world, spec.d
+            kc = wl.k_cache[:, rank * Hk:(rank + 1) * Hk].contiguous()
+            vc = wl.v_cache[:, rank * Hk:(rank + 1) * Hk].contiguous()
+            ql = wl.q[:, rank * Hq:(rank + 1) * Hq].contiguous()
+            pool = hg.KVPool(kc, vc, wl.lay.num_blocks, spec.B, Hk, d, 0)
+            N = 512
+            _, W = _inputs(11, world, 1, spec.H_q * d, N)
+            ws = torch.empty(hg.hg_hybrid_attention_tp_proj_workspace_size(pool, comm, wl.batch, spec.H_q),
+                             dtype=torch.uint8, device="cuda")
+            a, b = shard_rows(spec.T, world, rank)
+            y = torch.full((b - a, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+            hg.hg_hybrid_attention_tp_proj(pool, comm, wl.batch, spec.H_q, ql, W[rank], N, y, ws)
+            torch.cuda.synchronize()
+            # reference: this library's per-rank attention outputs (bf16), gathered, projected in fp64
+            o_loc = torch.empty((spec.T, Hq, d), dtype=torch.bfloat16, device="cuda")
+            ws2 = torch.empty(hg.hg_hybrid_attention_workspace_size(pool, wl.batch, Hq) + (1 << 20),
+                              dtype=torch.uint8, device="cuda")
+            hg.hg_hybrid_attention(pool, wl.batch, Hq, ql, o_loc, None, ws2)
+            torch.cuda.synchronize()
+            olist = [None] * world
+            dist.all_gather_object(olist, o_loc.reshape(spec.T, Hq * d).cpu())
+            ref = out_proj_rs([o.double().numpy() for o in olist], [w.cpu().double().numpy() for w in W])[rank]
+            got = y.float().cpu().double().numpy()
+            rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+            res.append(("layer", name, bool(rel <= REL_L2 and np.abs(got - ref).max() <= max_abs_bound(ref, world)),
+                        float(rel),
+                        int(np.isnan(got).any(1).sum()), int(np.isnan(ref).any(1).sum()),
+                        float(np.nanmax(np.abs(got - ref)))))
+            pool.close()
+            dist.barrier()
+        comm.close()
+        if os.path.isdir("gpurun_out"):
+            import json
+            json.dump(res, open(f"gpurun_out/op_res_{rank}.json", "w"))
+        q.put((rank, res, None))
+    except Exception:
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_same_gpu_out_proj_rs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in ps:
+        rank, res, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}:\n{err}"
+        got[rank] = res
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        bad = [x for x in got[r] if not x[2]]
+        assert not bad, (r, bad, got[r])

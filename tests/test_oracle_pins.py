@@ -339,3 +339,34 @@ def test_rope_chunked_equals_whole_and_decode_bitwise():
         outs.append(o)
         c += n
     assert np.array_equal(np.concatenate(outs), o_whole)
+
+
+# ---- output projection + reduce-scatter (NEXT-4) --------------------------------------
+def test_out_proj_rs_brute_force_tiny():
+    from oracle.outproj import out_proj_rs, shard_rows
+    rng = np.random.default_rng(5)
+    G, T, N = 3, 7, 5
+    Ks = [2, 3, 4]
+    O = [rng.standard_normal((T, k)) for k in Ks]
+    W = [rng.standard_normal((k, N)) for k in Ks]
+    shards = out_proj_rs(O, W)
+    for o in range(G):
+        a, b = shard_rows(T, G, o)
+        assert shards[o].shape == (b - a, N)
+        for t in range(a, b):
+            for n in range(N):
+                v = 0.0
+                for r in range(G):
+                    for k in range(Ks[r]):
+                        v += O[r][t, k] * W[r][k, n]
+                assert abs(shards[o][t - a, n] - v) < 1e-12
+    assert sum(shard_rows(T, G, o)[1] - shard_rows(T, G, o)[0] for o in range(G)) == T
+
+
+def test_out_proj_rs_block_identity():
+    from oracle.outproj import out_proj_rs
+    rng = np.random.default_rng(6)
+    O = [rng.standard_normal((11, 8)) for _ in range(4)]
+    W = [rng.standard_normal((8, 6)) for _ in range(4)]
+    full = np.concatenate(O, axis=1) @ np.concatenate(W, axis=0)
+    np.testing.assert_allclose(np.concatenate(out_proj_rs(O, W)), full, rtol=1e-12, atol=1e-12)

@@ -248,6 +248,8 @@ def run_ours(args):
         line["predictor"] = pred
         line["slo_loop"] = slo_loop(dev, model)
         line["psm_vs_fcfs"] = psm_vs_fcfs(dev)
+    if args.extra:
+        line["next4"] = next4(dev, peaks)
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -563,6 +565,53 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
             "mape_pred_vs_measured": float(np.mean(np.abs(pred - meas) / meas)),
             "online_tokens": tok_on, "offline_tokens": tok_off,
             "note": "kernel-level analogue of the paper's SLO loop: budget = attention GPU time per iteration"}
+
+
+def next4(dev, peaks, reps=20):
+    """NEXT-4 on one GPU: (a) the rope prologue's cost on the c1 step (hg_hybrid_step with
+    and without hg_rope), (b) the output-projection GEMM of hg_out_proj_rs (G = 1: its
+    epilogue stores straight into Y) at the Llama-3-70B shapes of c3 (hidden 8192; K =
+    64 heads x 128 on one GPU, 8 heads x 128 per rank at TP-8), against its tensor roofline."""
+    import torch
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    from synth.configs import make_config
+    from synth.values import KIND_O, KIND_W, matrix
+    res = {}
+    spec = make_config(WORKLOAD, 0)
+    for name, sp in (("c1", spec), ("c1_rope", spec.with_(rope=(1e4, 0)))):
+        wl = Workload(sp, device=dev)
+        for _ in range(3):
+            wl.step()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            wl.step()
+        e.record()
+        torch.cuda.synchronize()
+        res[name + "_ms_per_step"] = s.elapsed_time(e) / reps
+        wl.close()
+    comm = hg.Comm(None, 0, 1, dev.index)
+    peak = peaks["bf16_tflops"]
+    for T, K, N in ((768, 8192, 8192), (768, 1024, 8192)):
+        O = matrix(1, KIND_O, 0, T, K, device=dev)
+        W = matrix(1, KIND_W, 0, K, N, scale=K ** -0.5, device=dev)
+        y = torch.empty((T, N), dtype=torch.bfloat16, device=dev)
+        for _ in range(3):
+            hg.hg_out_proj_rs(comm, T, K, N, O, W, y)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            hg.hg_out_proj_rs(comm, T, K, N, O, W, y)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        tf = 2.0 * T * K * N / ms / 1e9
+        res[f"out_proj_{T}x{K}x{N}"] = {"ms": ms, "tflops": tf, "roofline_frac": tf / peak, "peak": peak}
+    comm.close()
+    return res
 
 
 def psm_vs_fcfs(dev, groups=64, per_group=32, batch=128, H=(32, 8, 128), seed=0):

@@ -85,6 +85,11 @@ __global__ void bench(long long *out, int iters) {
                             asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}"
                                          ::"r"(tm + 128), "r"(tm + ks * 8), "l"(dB_mn + ((ks * 2048) >> 4)), "r"(idesc(128, 128, 0, 1)), "r"(acc));
                     }
+                    if (MODE == 8 || MODE == 9 || MODE == 10) {  // SS, N = 80 / 64 / 96 (narrow KV tiles)
+                        constexpr int NN = MODE == 8 ? 80 : MODE == 9 ? 64 : 96;
+                        asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                                     ::"r"(tm), "l"(dA + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "l"(dB_k128 + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "r"(idesc(128, NN, 0, 0)), "r"(acc));
+                    }
                     if (MODE == 5)  // SS, N=256 (both Q tiles' PV in one, if V were the A operand)
                         asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
                                      ::"r"(tm), "l"(dA + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "l"(dB_k128 + (((ks / 4) * 16384 + (ks % 4) * 32) >> 4)), "r"(idesc(128, 256, 0, 0)), "r"(acc));
@@ -129,6 +134,9 @@ int main() {
     run<3>("TS B=K32 N128 (V^T blocks)", d);
     run<4>("SS B=MN128 N128", d);
     run<5>("SS A=K128 B=K128 N256", d);
+    run<8>("SS N80", d);
+    run<9>("SS N64", d);
+    run<10>("SS N96", d);
     run<6>("alternate 8 QK (SS) / 8 PV (TS)", d);
     run<7>("alternate + TMEM ld/st traffic", d);
     return 0;

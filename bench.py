@@ -159,11 +159,21 @@ def run_ours(args):
     from synth.configs import make_config
 
     rank, world, local = env_rank()
+    # HG_BENCH_SAME_GPU=1 is a functional test of the multi-rank path on a one-GPU box:
+    # every rank on device 0, gloo for the bench's own collectives, no NCCL
+    # communicator (the peer window carries the gather).  Its timings are not a
+    # scaling measurement (the ranks time-slice one GPU).
+    same_gpu = os.environ.get("HG_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     peaks, peak_kind = load_peaks()
     spec = make_config(WORKLOAD, 0)
 
@@ -692,7 +702,8 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     local = spec.with_(H_kv=Hk, H_q=Hq)
     # each rank's slice is generated as its own (smaller-head) workload; values are synthetic
     wl = Workload(local, device=dev)
-    uid = [hg.hg_comm_unique_id() if rank == 0 else None]
+    same_gpu = os.environ.get("HG_BENCH_SAME_GPU") == "1"
+    uid = [hg.hg_comm_unique_id() if rank == 0 and not same_gpu else None]
     dist.broadcast_object_list(uid, src=0)
     comm = hg.Comm(uid[0], rank, world, dev.index)
     # v2: a peer window per rank, mapped by every other rank (CUDA IPC over NVLink);
@@ -721,9 +732,32 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
         e.record()
         torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([s.elapsed_time(e)], device=dev)
+    cdev = "cpu" if same_gpu else dev   # gloo (same-GPU functional test) reduces host tensors
+    t = torch.tensor([s.elapsed_time(e)], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = t.item()
+    # e2e through the public API with host buffers: each rank's pinned q / k_new / v_new
+    # slices in, the gathered O [T][H_q][d] out, per step; slowest rank's wall time
+    qh, kh, vh = wl.q.cpu().pin_memory(), wl.k_new.cpu().pin_memory(), wl.v_new.cpu().pin_memory()
+    oh = torch.empty(out.shape, dtype=torch.bfloat16).pin_memory()
+
+    def step_host():
+        wl.q.copy_(qh, non_blocking=True)
+        wl.k_new.copy_(kh, non_blocking=True)
+        wl.v_new.copy_(vh, non_blocking=True)
+        step()
+        oh.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    for _ in range(args.warmup):
+        step_host()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_host()
+    te = torch.tensor([time.perf_counter() - t0], device=cdev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = te.item()
     if rank == 0:
         ms = total_ms / args.steps
         print(json.dumps({
@@ -733,7 +767,14 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
             "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "parallelism": f"kv-head tp{world}, all-gather fused into the epilogues (peer window)",
                        "l2": "KV working set 2.7 GB total > L2"},
             "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 3) * args.steps,  # + append, 2 barriers
+            "e2e": {"value": spec.T * args.steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2 * world,
+                    "d2h_bytes_per_step": oh.numel() * 2 * world, "ms_per_step": e2e_s / args.steps * 1e3,
+                    "api": "per rank: pinned H2D of its q / k_new / v_new slices, hg_kv_append + "
+                           "hg_hybrid_attention_tp, D2H of the gathered O; slowest rank"},
             "clocks": clk.summary(),
+            **({"note": "HG_BENCH_SAME_GPU functional test: all ranks on one GPU, not a scaling number"}
+               if same_gpu else {}),
         }))
     comm.close()
     dist.destroy_process_group()

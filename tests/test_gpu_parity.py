@@ -173,15 +173,47 @@ def test_full_size_sampled(name):
     wl.close()
 
 
-@pytest.mark.parametrize("q_scale", [8.0])
-@pytest.mark.parametrize("name", ["p1"])
+@pytest.mark.parametrize("name,q_scale", [("p1", 8.0), ("p2", 8.0), ("c1", 4.0), ("c1_long", 4.0)])
 def test_peaked(name, q_scale):
+    """§8(c.6) parity matrix: peaked queries (q x 4 / q x 8)."""
     from synth.configs import make_config
     spec = make_config(name, 0, q_scale)
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    compare(spec, wl, req_sel=[1])
+    compare(spec, wl, req_sel=[1] if name == "p1" else [0] if name == "p2" else _sample(spec, 4))
+    wl.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c1_long", "c2"])
+def test_full_size_second_seed(name):
+    """§8(c.6): C1 and C2 at seed 1 as well (different lengths and block placement)."""
+    from synth.configs import make_config
+    spec = make_config(name, 1)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    compare(spec, wl, req_sel=_sample(spec, 4))
+    wl.close()
+
+
+def test_c2_shared_vs_private_full_size():
+    """§8(c.6) C2 row: the all-share batch and the same batch with private prefix
+    copies agree within tolerance of each other and of the oracle."""
+    from synth.configs import make_config
+    a = make(make_config("c2", 0))
+    a.step()
+    b = make(make_config("c2_private", 0))
+    b.step()
+    torch.cuda.synchronize()
+    d = (a.out.double() - b.out.double())
+    assert d.abs().max().item() <= MAX_ABS
+    assert (d.norm() / b.out.double().norm()).item() <= REL_L2
+    sel = _sample(a.spec, 4)
+    compare(a.spec, a, req_sel=sel)
+    compare(b.spec, b, req_sel=sel)
+    a.close()
+    b.close()
 
 
 def test_empty_batch():

@@ -437,3 +437,24 @@ def test_c2_nested_full_size():
     assert st["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
     compare(spec, wl, req_sel=_sample(spec, 10))
     wl.close()
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_mixed_feature_fuzz(seed):
+    """Everything at once on random small batches: nested prefix tries, GQA group
+    sizes 1-16, d in {64, 128}, RoPE on/off, and the plan switches (fixed split,
+    no prefix pass, no tcgen05), through the fused step, against the oracle."""
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_fuzz, make_fuzz_nested
+    rng = np.random.default_rng(50_000 + seed)
+    G = int(rng.choice([1, 2, 4, 8, 16]))
+    d = int(rng.choice([64, 128]))
+    spec = (make_fuzz_nested if seed % 2 else make_fuzz)(seed, G_q=G, H_kv=int(rng.choice([1, 2])), d=d)
+    if rng.random() < 0.5:
+        spec = spec.with_(rope=(float(rng.choice([1e4, 5e5])), int(rng.choice([0, 32]))))
+    opts = [None, hg.make_opts(split_tokens=int(rng.choice([16, 64, 256]))), hg.make_opts(disable_prefix_pass=True),
+            hg.make_opts(disable_tc=True)][seed % 4]
+    wl = make(spec)
+    wl.step(opts)
+    torch.cuda.synchronize()
+    compare(spec, wl, tag=f"[mixed {seed}]")

@@ -5,9 +5,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <set>
 #include <vector>
 
@@ -42,6 +45,10 @@ struct hg_kv_pool {
     // side stream: the split-K kernel runs beside the tcgen05 kernel (fork/join by events)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // hg_hybrid_step_host: copy stream for the two input waves, their events, and
+    // the prefill wave's tcgen05 stream (highest priority) with its done events
+    cudaStream_t h2d = nullptr, side_hi = nullptr;
+    cudaEvent_t ev_in0 = nullptr, ev_in1 = nullptr, ev_tc = nullptr, ev_d2h = nullptr;
 };
 
 namespace hg {
@@ -133,6 +140,13 @@ extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
     }
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
+    for (cudaStream_t s : {p->h2d, p->side_hi})
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    for (cudaEvent_t e : {p->ev_in0, p->ev_in1, p->ev_tc, p->ev_d2h})
+        if (e) cudaEventDestroy(e);
     delete p;
     return HG_OK;
 }
@@ -333,6 +347,29 @@ extern "C" hg_status hg_kv_append_rope(hg_kv_pool *pool, const hg_batch *batch, 
 // ---------------------------------------------------------------------------
 // a.1-a.7 hybrid attention
 // ---------------------------------------------------------------------------
+static hg_status ensure_side(hg_kv_pool *pool) {
+    if (pool->side) return HG_OK;
+    hg_status s = cuda_check(cudaStreamCreateWithFlags(&pool->side, cudaStreamNonBlocking), "side stream");
+    if (s) return s;
+    s = cuda_check(cudaEventCreateWithFlags(&pool->ev_fork, cudaEventDisableTiming), "fork event");
+    if (s) return s;
+    return cuda_check(cudaEventCreateWithFlags(&pool->ev_join, cudaEventDisableTiming), "join event");
+}
+
+// Pipelined host step (hg_hybrid_step_host): the inputs arrive in two waves on
+// a copy stream -- wave 0 = the decode rows' Q/K/V, wave 1 = the prefill-chunk
+// rows' -- and each wave's append and attention start as soon as it lands.
+struct StepPipe {
+    cudaEvent_t in0 = nullptr, in1 = nullptr;   // recorded on the copy stream after each wave
+    cudaStream_t side = nullptr;                // stream of the wave-1 work (append + tcgen05)
+    cudaEvent_t tc_done = nullptr;              // recorded on `side` after the tcgen05 kernel
+    std::function<hg_status(int)> enqueue_wave; // issues wave w's copies and records in0 / in1: wave 0 right
+                                                // after the descriptor upload (which must not queue behind
+                                                // the inputs on the copy engine), wave 1 after the split-K
+                                                // launch (so that launch is not delayed by the host)
+    bool planned = false;                       // pool->plan already holds this batch's validated plan
+    bool used = false;                          // out: the call was split into waves
+};
 static PlanOpts plan_opts(const hg_kv_pool *pool, const hg_attn_opts *o) {
     PlanOpts po;
     po.num_sms = pool->num_sms;
@@ -374,10 +411,10 @@ extern "C" hg_status hg_hybrid_attention_workspace_size(const hg_kv_pool *pool, 
 static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, void *out,
                                 float *lse, void *ws, size_t ws_bytes, cudaStream_t st, const hg_attn_opts *o,
                                 bool fused = false, const void *k_new = nullptr, const void *v_new = nullptr,
-                                const OutSpec *outs = nullptr) {
+                                const OutSpec *outs = nullptr, StepPipe *pipe = nullptr) {
     BatchView v;
     Plan &plan = pool->plan;
-    hg_status s = plan_call(pool, batch, H_q, o, &v, &plan, fused);
+    hg_status s = (pipe && pipe->planned) ? view_batch(batch, &v) : plan_call(pool, batch, H_q, o, &v, &plan, fused);
     if (s) return s;
     s = sticky_check();
     if (s) return s;
@@ -395,6 +432,17 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     if (fused && (!k_new || !v_new)) return fail(HG_E_INVALID, "k_new / v_new NULL");
     if (!ws || ws_bytes < plan.total_bytes)
         return fail(HG_E_INVALID, "workspace %zu bytes < required %zu", ws_bytes, plan.total_bytes);
+    if (pipe) {
+        // Split into waves only when wave 0's work (append + split-K) reads no
+        // wave-1 input: every prefill chunk (wave 1) is on the tcgen05 tiles.
+        // The prefix-group tiles read only cached keys and decode-row Q (wave 0).
+        static const bool serial = getenv("HG_E2E_SERIAL") != nullptr;   // A/B switch: one input wave
+        bool ok = fused && !ra.rot && plan.n_tc_prefill() > 0 && !serial;
+        for (size_t k = 0; ok && k < plan.sk.size(); ++k) ok = v.n[plan.sk[k].req] == 1;
+        pipe->used = ok;
+        if (ok)
+            for (TokDev &tk : plan.tok) tk.wave = v.n[tk.req] > 1 ? 1 : 0;
+    }
     // one image of all descriptors -> one pinned H2D copy
     static thread_local std::vector<uint8_t> img;
     img.assign(plan.desc_bytes, 0);
@@ -409,6 +457,12 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
     s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
     if (s) return s;
+    if (pipe) {
+        s = pipe->enqueue_wave(0);
+        if (!s && !pipe->used) s = pipe->enqueue_wave(1);
+        if (!s && !pipe->used) s = cuda_check(cudaStreamWaitEvent(st, pipe->in1, 0), "inputs wait");
+        if (s) return s;
+    }
     uint8_t *w = (uint8_t *)ws;
     AttnParams p{};
     p.k_cache = (const uint16_t *)pool->desc.k_cache;
@@ -448,6 +502,51 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     auto rec = [&](int k, cudaStream_t on) {
         if (o && o->events[k]) cudaEventRecord((cudaEvent_t)o->events[k], on);
     };
+    if (pipe && pipe->used) {
+        s = ensure_side(pool);
+        if (s) return s;
+        s = cuda_check(cudaEventRecord(pool->ev_fork, st), "fork record");   // descriptors staged
+        // wave 0 on the caller's stream: decode rows' append, then split-K
+        if (!s) s = cuda_check(cudaStreamWaitEvent(st, pipe->in0, 0), "wave 0 wait");
+        if (!s) s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st, 0);
+        if (s) return s;
+        rec(2, st);
+        s = launch_splitk(p, st);
+        if (s) return s;
+        rec(3, st);
+        // wave 1 on the pipe's stream: prefill rows' append, then the tcgen05 tiles
+        s = pipe->enqueue_wave(1);
+        if (s) return s;
+        cudaStream_t sd = pipe->side;
+        s = cuda_check(cudaStreamWaitEvent(sd, pool->ev_fork, 0), "fork wait");
+        if (!s) s = cuda_check(cudaStreamWaitEvent(sd, pipe->in1, 0), "wave 1 wait");
+        if (!s) s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, sd, 1);
+        if (s) return s;
+        rec(0, sd);
+        s = launch_tc(p, pool->tmap_k, pool->tmap_v, sd);
+        if (s) return s;
+        rec(1, sd);
+        s = cuda_check(cudaEventRecord(pipe->tc_done, sd), "tc record");
+        if (!s) s = cuda_check(cudaStreamWaitEvent(st, pipe->tc_done, 0), "tc wait");
+        if (s) return s;
+        int kernels = 4;
+        if (p.n_comb) {
+            rec(4, st);
+            s = launch_combine(p, st);
+            if (s) return s;
+            rec(5, st);
+            ++kernels;
+        }
+        hg_plan_stats &ls = pool->last;
+        ls.tc_tiles = p.n_tc;
+        ls.prefix_tiles = plan.prefix_tiles;
+        ls.splitk_items = p.n_sk * p.H_kv;
+        ls.combine_rows = p.n_comb * p.H_kv;
+        ls.kernels = kernels;
+        ls.kv_bytes_unique = plan.kv_bytes_unique;
+        ls.kv_bytes_read = plan.kv_bytes_read;
+        return HG_OK;
+    }
     // The tcgen05 tiles (tensor-bound) and the split-K items (HBM-bound) are
     // independent: the tcgen05 kernel is launched first on the caller's stream
     // (its CTAs are placed first), the split-K kernel on a side stream forked
@@ -467,14 +566,8 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     const bool overlap = p.n_tc && p.n_sk;
     cudaStream_t sk_stream = st;
     if (overlap) {
-        if (!pool->side) {
-            s = cuda_check(cudaStreamCreateWithFlags(&pool->side, cudaStreamNonBlocking), "side stream");
-            if (s) return s;
-            s = cuda_check(cudaEventCreateWithFlags(&pool->ev_fork, cudaEventDisableTiming), "fork event");
-            if (s) return s;
-            s = cuda_check(cudaEventCreateWithFlags(&pool->ev_join, cudaEventDisableTiming), "join event");
-            if (s) return s;
-        }
+        s = ensure_side(pool);
+        if (s) return s;
         sk_stream = pool->side;
         s = cuda_check(cudaEventRecord(pool->ev_fork, st), "fork record");
         if (s) return s;
@@ -581,48 +674,116 @@ extern "C" hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, 
     return HG_OK;
 }
 
+// Pipelined: the inputs go up in two waves on a library-owned copy stream, the
+// decode rows' first (small: one token per request) so the HBM-bound split-K
+// kernel starts after ~1/10 of the upload; the prefill chunks' rows follow while
+// it runs and feed the tcgen05 tiles on a high-priority stream; their O goes
+// back to the host as soon as those tiles finish, the decode rows' after the
+// combine.  Runs of consecutive requests of one wave are copied as one range.
 extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q,
                                          const void *q_host, const void *k_new_host, const void *v_new_host,
                                          void *out_host, void *workspace, size_t workspace_bytes, void *stream) {
+    static const bool trace = getenv("HG_E2E_TRACE") != nullptr;   // host-side phase times (stderr)
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    const auto t_in = now();
     if (!pool) return fail(HG_E_INVALID, "pool is NULL");
     hg_status s = sticky_check();
     if (s) return s;
-    size_t need = 0;
-    s = hg_hybrid_step_host_workspace_size(pool, batch, H_q, &need);
-    if (s) return s;
-    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    if (!q_host || !k_new_host || !v_new_host || !out_host) return fail(HG_E_INVALID, "host buffer NULL");
+    // one validated plan for the whole step (attention_impl reuses pool->plan)
     BatchView v;
-    s = view_batch(batch, &v);
+    s = plan_call(pool, batch, H_q, nullptr, &v, &pool->plan, true);
     if (s) return s;
-    s = validate(v, pool->desc.block_size, pool->desc.num_blocks, H_q, pool->desc.num_kv_heads, true);
-    if (s) return s;
-    int64_t T = 0;
-    for (int i = 0; i < v.R; ++i) T += v.n[i];
+    const int64_t T = pool->plan.T;
     if (T == 0) return HG_OK;
-    size_t attn = 0;
-    s = hg_hybrid_attention_workspace_size(pool, batch, H_q, &attn);
-    if (s) return s;
+    const size_t attn = pool->plan.total_bytes;
     const size_t d = pool->desc.head_dim, Hk = pool->desc.num_kv_heads;
+    const size_t need = al256(attn) + 2 * al256(T * H_q * d * 2) + 2 * al256(T * Hk * d * 2) + al256(T * 8);
+    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    const size_t qrow = (size_t)H_q * d * 2, kvrow = Hk * d * 2;   // bytes per token row
     uint8_t *w = (uint8_t *)workspace;
     size_t off = al256(attn);
-    void *q_d = w + off;   off += al256(T * H_q * d * 2);
-    void *o_d = w + off;   off += al256(T * H_q * d * 2);
-    void *k_d = w + off;   off += al256(T * Hk * d * 2);
-    void *v_d = w + off;   off += al256(T * Hk * d * 2);
-    void *slot_d = w + off;
+    uint8_t *q_d = w + off;   off += al256(T * qrow);
+    uint8_t *o_d = w + off;   off += al256(T * qrow);
+    uint8_t *k_d = w + off;   off += al256(T * kvrow);
+    uint8_t *v_d = w + off;
     cudaStream_t st = (cudaStream_t)stream;
-    s = cuda_check(cudaMemcpyAsync(q_d, q_host, T * H_q * d * 2, cudaMemcpyHostToDevice, st), "H2D q");
+    if (!pool->h2d) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        s = cuda_check(cudaStreamCreateWithFlags(&pool->h2d, cudaStreamNonBlocking), "copy stream");
+        if (!s) s = cuda_check(cudaStreamCreateWithPriority(&pool->side_hi, cudaStreamNonBlocking, hi), "tc stream");
+        for (cudaEvent_t *e : {&pool->ev_in0, &pool->ev_in1, &pool->ev_tc, &pool->ev_d2h})
+            if (!s) s = cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event create");
+        if (s) return s;
+    }
+    // row runs [a, b) of each wave (wave 1 = prefill-chunk requests, n_i > 1)
+    std::vector<std::pair<int64_t, int64_t>> runs[2];
+    {
+        int64_t row = 0;
+        for (int i = 0; i < v.R; ++i) {
+            auto &rw = runs[v.n[i] > 1 ? 1 : 0];
+            if (!rw.empty() && rw.back().second == row) rw.back().second += v.n[i];
+            else rw.emplace_back(row, row + v.n[i]);
+            row += v.n[i];
+        }
+    }
+    StepPipe pipe;
+    pipe.in0 = pool->ev_in0;
+    pipe.in1 = pool->ev_in1;
+    pipe.side = pool->side_hi;
+    pipe.tc_done = pool->ev_tc;
+    // the copy stream and the tcgen05 stream start after whatever the caller queued before this step
+    s = cuda_check(cudaEventRecord(pool->ev_d2h, st), "order record");
+    if (!s) s = cuda_check(cudaStreamWaitEvent(pool->h2d, pool->ev_d2h, 0), "order wait");
+    if (!s) s = cuda_check(cudaStreamWaitEvent(pipe.side, pool->ev_d2h, 0), "order wait");
     if (s) return s;
-    s = cuda_check(cudaMemcpyAsync(k_d, k_new_host, T * Hk * d * 2, cudaMemcpyHostToDevice, st), "H2D k");
+    pipe.planned = true;
+    pipe.enqueue_wave = [&](int wv) -> hg_status {
+        for (auto &r : runs[wv]) {
+            const int64_t a = r.first, n = r.second - r.first;
+            hg_status e = cuda_check(cudaMemcpyAsync(q_d + a * qrow, (const uint8_t *)q_host + a * qrow, n * qrow,
+                                                     cudaMemcpyHostToDevice, pool->h2d), "H2D q");
+            if (!e) e = cuda_check(cudaMemcpyAsync(k_d + a * kvrow, (const uint8_t *)k_new_host + a * kvrow,
+                                                   n * kvrow, cudaMemcpyHostToDevice, pool->h2d), "H2D k");
+            if (!e) e = cuda_check(cudaMemcpyAsync(v_d + a * kvrow, (const uint8_t *)v_new_host + a * kvrow,
+                                                   n * kvrow, cudaMemcpyHostToDevice, pool->h2d), "H2D v");
+            if (e) return e;
+        }
+        return cuda_check(cudaEventRecord(wv ? pool->ev_in1 : pool->ev_in0, pool->h2d), "wave record");
+    };
+    const auto t_cp = now();
+    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, workspace, attn, st, nullptr, true, k_d, v_d, nullptr,
+                       &pipe);
     if (s) return s;
-    s = cuda_check(cudaMemcpyAsync(v_d, v_new_host, T * Hk * d * 2, cudaMemcpyHostToDevice, st), "H2D v");
+    const auto t_at = now();
+    auto d2h = [&](const std::vector<std::pair<int64_t, int64_t>> &rw, cudaStream_t on) -> hg_status {
+        for (auto &r : rw) {
+            hg_status e = cuda_check(cudaMemcpyAsync((uint8_t *)out_host + r.first * qrow, o_d + r.first * qrow,
+                                                     (r.second - r.first) * qrow, cudaMemcpyDeviceToHost, on), "D2H out");
+            if (e) return e;
+        }
+        return HG_OK;
+    };
+    if (pipe.used) {
+        // prefill rows are final when the tcgen05 kernel ends (they have no partials)
+        s = d2h(runs[1], pipe.side);
+        if (!s) s = cuda_check(cudaEventRecord(pool->ev_d2h, pipe.side), "d2h record");
+        if (!s) s = d2h(runs[0], st);
+        if (!s) s = cuda_check(cudaStreamWaitEvent(st, pool->ev_d2h, 0), "d2h wait");
+    } else {
+        s = cuda_check(cudaMemcpyAsync(out_host, o_d, T * qrow, cudaMemcpyDeviceToHost, st), "D2H out");
+    }
     if (s) return s;
-    (void)slot_d;
-    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, workspace, attn, st, nullptr, true, k_d, v_d);
-    if (s) return s;
-    s = cuda_check(cudaMemcpyAsync(out_host, o_d, T * H_q * d * 2, cudaMemcpyDeviceToHost, st), "D2H out");
-    if (s) return s;
-    return cuda_check(cudaStreamSynchronize(st), "stream sync");
+    const auto t_d2 = now();
+    s = cuda_check(cudaStreamSynchronize(st), "stream sync");
+    if (trace)
+        fprintf(stderr, "hg_hybrid_step_host: prep %.1f us, attention + input copies enqueue %.1f, d2h %.1f, sync %.1f\n",
+                us(t_in, t_cp), us(t_cp, t_at), us(t_at, t_d2), us(t_d2, now()));
+    return s;
 }
 
 // ---------------------------------------------------------------------------

@@ -43,7 +43,7 @@ struct TokDev {
     int32_t base;
     int32_t nparts;
     int32_t req;    // owning request (device-side slot computation of the fused append)
-    int32_t pad;
+    int32_t wave;   // pipelined host step: input wave of the token (0 decode rows, 1 prefill-chunk rows)
 };
 
 // tcgen05 tile (tc_attn.cu): up to 128 stacked query rows sharing KV head g
@@ -110,6 +110,7 @@ struct Plan {
     std::vector<int32_t> comb;
     int64_t n_slots = 0;
     int32_t prefix_tiles = 0;
+    int64_t n_tc_prefill() const { return (int64_t)tc.size() - prefix_tiles; }   // mode-0 items
     int64_t kv_bytes_unique = 0;
     int64_t kv_bytes_read = 0;
     int32_t tc_ctas = 0;        // persistent tcgen05 grid chosen by the planner
@@ -158,7 +159,10 @@ hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, con
 hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache,
                         uint16_t *v_cache, const int64_t *slot, int T, int H_kv, int d,
                         void *stream);
-hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream);
+// wave >= 0: only tokens whose TokDev.wave == wave (the pipelined host step
+// appends the decode rows' K/V as soon as their wave of inputs has landed).
+hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream,
+                            int wave = -1);
 // RoPE in the append prologue (NEXT-4): K rotated at its position before it is
 // written, V copied, and (q_dst != NULL) Q rotated into q_dst.  Token slots and
 // positions from the attention descriptors (fused step) or from arrays.

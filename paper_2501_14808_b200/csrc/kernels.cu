@@ -62,9 +62,11 @@ template <int PER>   // uint4 chunks of K (and of V) per thread
 __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict__ k_new,
                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_cache,
                                                          uint4 *__restrict__ v_cache, const AttnParams p,
-                                                         int chunks_per_row) {
+                                                         int chunks_per_row, int wave) {
     const int t = blockIdx.x;
-    const ReqDev rq = p.reqs[p.tok[t].req];
+    const TokDev tk = p.tok[t];
+    if (wave >= 0 && tk.wave != wave) return;   // pipelined host step: this token's inputs arrive in the other wave
+    const ReqDev rq = p.reqs[tk.req];
     const int pos = rq.c + (t - rq.cu_q);
     const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
     const int row_chunks = p.H_kv * chunks_per_row;   // uint4 chunks of one token's K (or V)
@@ -92,7 +94,8 @@ __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict
     }
 }
 
-hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream) {
+hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream,
+                            int wave) {
     if (T == 0) return HG_OK;
     const int cpr = p.d / 8;
     const int row_chunks = p.H_kv * cpr;
@@ -100,10 +103,10 @@ hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const ui
     auto *kn = (const uint4 *)k_new, *vn = (const uint4 *)v_new;
     auto *kc = (uint4 *)p.k_cache, *vc = (uint4 *)p.v_cache;
     cudaStream_t st = (cudaStream_t)stream;
-    if (per <= 1) append_dev_kernel<1><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
-    else if (per <= 2) append_dev_kernel<2><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
-    else if (per <= 4) append_dev_kernel<4><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
-    else append_dev_kernel<8><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr);
+    if (per <= 1) append_dev_kernel<1><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr, wave);
+    else if (per <= 2) append_dev_kernel<2><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr, wave);
+    else if (per <= 4) append_dev_kernel<4><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr, wave);
+    else append_dev_kernel<8><<<T, 256, 0, st>>>(kn, vn, kc, vc, p, cpr, wave);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
 }

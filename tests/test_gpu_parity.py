@@ -247,19 +247,40 @@ def test_error_leaves_outputs_untouched():
     assert torch.all(wl.out == 7.0) and torch.equal(k_before, wl.k_cache)
 
 
-def test_e2e_host_step_matches_device_path():
+def _e2e_spec(name):
+    from synth.configs import Request, make_config
+    if name == "interleaved":   # prefill chunks between decodes: several row runs per wave
+        return _mixed(name, 32, 8, 128, [Request(300, 200), Request(40, 1), Request(1000, 1, True),
+                                         Request(0, 77), Request(129, 1), Request(64, 300, True)])
+    if name == "d64_gqa5":
+        return _mixed(name, 40, 8, 64, [Request(17, 1), Request(0, 130), Request(2000, 1), Request(5, 33, True)])
+    return make_config(name, 0)
+
+
+@pytest.mark.parametrize("name", ["toy_a", "toy_b", "c1", "c2", "c3", "p1", "interleaved", "d64_gqa5"])
+def test_e2e_host_step_matches_device_path(name):
+    """hg_hybrid_step_host (host buffers, two pipelined input waves: decode rows
+    then prefill-chunk rows) runs first on a fresh pool -- so its own append
+    fills the cache -- and must equal hg_hybrid_step (device buffers) bit for
+    bit, output and post-append cache."""
     import paper_2501_14808_b200 as hg
-    from synth.configs import make_config
-    spec = make_config("toy_b", 0)
+    spec = _e2e_spec(name)
     wl = make(spec)
-    wl.step()
     torch.cuda.synchronize()
     qh, kh, vh = (x.cpu().pin_memory() for x in (wl.q, wl.k_new, wl.v_new))
-    oh = torch.empty(wl.out.shape, dtype=torch.bfloat16).pin_memory()
+    oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16).pin_memory()
     ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
                      device="cuda")
-    hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
-    assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16))
+    for rep in range(2):   # second call: events and streams reused
+        hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
+        k_after, v_after = wl.k_cache.clone(), wl.v_cache.clone()
+        wl.step()
+        torch.cuda.synchronize()
+        assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), rep
+        assert torch.equal(k_after, wl.k_cache) and torch.equal(v_after, wl.v_cache), rep
+    if name in ("toy_a", "toy_b", "interleaved"):
+        wl.out.copy_(oh.cuda())
+        compare(spec, wl, check_lse=False, tag=" (host step)")
 
 
 def test_tp_path_world1_matches_single_gpu():

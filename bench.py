@@ -54,7 +54,7 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi style clock / throttle sampling through NVML during the timed region."""
 
-    def __init__(self, device_index: int, period_s: float = 0.002):
+    def __init__(self, device_index: int, period_s: float = 0.001):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.dev, self.period = device_index, period_s
         self._stop = threading.Event()
@@ -92,6 +92,9 @@ class ClockSampler:
         if self.ok:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            t0 = time.perf_counter()   # the thread is sampling before the timed region starts
+            while len(self.samples) < 2 and time.perf_counter() - t0 < 1.0:
+                time.sleep(0.0005)
         return self
 
     def __exit__(self, *a):
@@ -103,7 +106,9 @@ class ClockSampler:
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "sm_mhz_min": min(self.samples), "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "NVML (nvmlDeviceGetClockInfo SM + clocks-event reasons), sampled every 1 ms "
+                          "in a thread during the timed region"}
 
 
 def alg_bytes_splitk(spec):
@@ -299,17 +304,23 @@ def measure_e2e(wl, spec, args, stream):
     oh = torch.empty(wl.out.shape, dtype=torch.bfloat16).pin_memory()
     ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
                      device=wl.device)
-    for _ in range(args.warmup):
+    # warm-up: at least W steps and 0.5 s -- the host step's wall time settles only
+    # after ~100 synchronised steps on these boxes (0.94 -> 0.61 ms, tools/prof_e2e.py)
+    w, t0 = 0, time.perf_counter()
+    while w < args.warmup or time.perf_counter() - t0 < 0.5:
         hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws, stream)
+        w += 1
     torch.cuda.synchronize()
+    steps = max(args.steps, 50)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(steps):
         hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws, stream)
     dt = time.perf_counter() - t0
     h2d = (qh.numel() + kh.numel() + vh.numel()) * 2
-    return {"value": spec.T * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": oh.numel() * 2, "ms_per_step": dt / args.steps * 1e3,
-            "api": "hg_hybrid_step_host (C ABI, host buffers; synchronises each step)"}
+    return {"value": spec.T * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": oh.numel() * 2, "ms_per_step": dt / steps * 1e3, "steps": steps,
+            "warmup_steps": w,
+            "api": "hg_hybrid_step_host (C ABI, host buffers; two pipelined input waves; synchronises each step)"}
 
 
 def cpu_baseline(spec, wl=None, sample_reqs=None, min_s=10.0):
@@ -769,15 +780,16 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
         oh.copy_(out, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 150)):   # the same count on every rank (peer barriers); see measure_e2e
         step_host()
     dist.barrier()
+    e2e_steps = max(args.steps, 50)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         step_host()
     te = torch.tensor([time.perf_counter() - t0], device=cdev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = te.item()
+    e2e_s = te.item() * args.steps / e2e_steps   # per args.steps steps, as below
     if rank == 0:
         ms = total_ms / args.steps
         print(json.dumps({
@@ -833,7 +845,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)   # ~0.1 s timed: enough NVML clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", dest="extra", action="store_false",

@@ -356,6 +356,18 @@ static hg_status ensure_side(hg_kv_pool *pool) {
     return cuda_check(cudaEventCreateWithFlags(&pool->ev_join, cudaEventDisableTiming), "join event");
 }
 
+// High-priority stream for the tcgen05 tiles when they run beside split-K
+// (their CTAs need whole SMs: at equal priority split-K's queued CTAs can take
+// every SM that frees up), and the event that joins it.
+static hg_status ensure_hi(hg_kv_pool *pool) {
+    if (pool->side_hi) return HG_OK;
+    int lo = 0, hi = 0;
+    hg_status s = cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    if (!s) s = cuda_check(cudaStreamCreateWithPriority(&pool->side_hi, cudaStreamNonBlocking, hi), "tc stream");
+    if (!s) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_tc, cudaEventDisableTiming), "tc event");
+    return s;
+}
+
 // Pipelined host step (hg_hybrid_step_host): the inputs arrive in two waves on
 // a copy stream -- wave 0 = the decode rows' Q/K/V, wave 1 = the prefill-chunk
 // rows' -- and each wave's append and attention start as soon as it lands.
@@ -432,15 +444,32 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     if (fused && (!k_new || !v_new)) return fail(HG_E_INVALID, "k_new / v_new NULL");
     if (!ws || ws_bytes < plan.total_bytes)
         return fail(HG_E_INVALID, "workspace %zu bytes < required %zu", ws_bytes, plan.total_bytes);
-    if (pipe) {
-        // Split into waves only when wave 0's work (append + split-K) reads no
-        // wave-1 input: every prefill chunk (wave 1) is on the tcgen05 tiles.
-        // The prefix-group tiles read only cached keys and decode-row Q (wave 0).
-        static const bool serial = getenv("HG_E2E_SERIAL") != nullptr;   // A/B switch: one input wave
-        bool ok = fused && !ra.rot && plan.n_tc_prefill() > 0 && !serial;
+    // Two waves -- decode rows (append + split-K on the caller's stream) and
+    // prefill-chunk rows (append + tcgen05 on the high-priority stream) -- when
+    // wave 0's work reads no wave-1 input: every prefill chunk is on the tcgen05
+    // tiles (the prefix-group tiles read only cached keys and decode-row Q).
+    // Split-K then waits only for the decode rows' append; the host step
+    // (pipe != NULL) also feeds each wave from its own H2D copies.
+    StepPipe local;
+    {
+        static const bool serial = getenv("HG_E2E_SERIAL") != nullptr;   // A/B switches: one wave
+        // device-buffer step: off by default -- measured slower on c1 (0.460 vs 0.4555 ms:
+        // the decode rows' append alone still takes ~5 us, and the tiles, started
+        // later, then overlap more of split-K); HG_STEP_WAVES=1 turns it on
+        static const bool no_waves = getenv("HG_STEP_WAVES") == nullptr;
+        bool ok = fused && !ra.rot && plan.n_tc_prefill() > 0 && !plan.sk.empty();
         for (size_t k = 0; ok && k < plan.sk.size(); ++k) ok = v.n[plan.sk[k].req] == 1;
-        pipe->used = ok;
-        if (ok)
+        if (pipe) {
+            pipe->used = ok && !serial;
+        } else if (ok && !no_waves) {
+            s = ensure_hi(pool);
+            if (s) return s;
+            local.side = pool->side_hi;
+            local.tc_done = pool->ev_tc;
+            local.used = true;
+            pipe = &local;
+        }
+        if (pipe && pipe->used)
             for (TokDev &tk : plan.tok) tk.wave = v.n[tk.req] > 1 ? 1 : 0;
     }
     // one image of all descriptors -> one pinned H2D copy
@@ -457,7 +486,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
     s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
     if (s) return s;
-    if (pipe) {
+    if (pipe && pipe->enqueue_wave) {
         s = pipe->enqueue_wave(0);
         if (!s && !pipe->used) s = pipe->enqueue_wave(1);
         if (!s && !pipe->used) s = cuda_check(cudaStreamWaitEvent(st, pipe->in1, 0), "inputs wait");
@@ -507,7 +536,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (s) return s;
         s = cuda_check(cudaEventRecord(pool->ev_fork, st), "fork record");   // descriptors staged
         // wave 0 on the caller's stream: decode rows' append, then split-K
-        if (!s) s = cuda_check(cudaStreamWaitEvent(st, pipe->in0, 0), "wave 0 wait");
+        if (!s && pipe->in0) s = cuda_check(cudaStreamWaitEvent(st, pipe->in0, 0), "wave 0 wait");
         if (!s) s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st, 0);
         if (s) return s;
         rec(2, st);
@@ -515,11 +544,13 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (s) return s;
         rec(3, st);
         // wave 1 on the pipe's stream: prefill rows' append, then the tcgen05 tiles
-        s = pipe->enqueue_wave(1);
-        if (s) return s;
+        if (pipe->enqueue_wave) {
+            s = pipe->enqueue_wave(1);
+            if (s) return s;
+        }
         cudaStream_t sd = pipe->side;
         s = cuda_check(cudaStreamWaitEvent(sd, pool->ev_fork, 0), "fork wait");
-        if (!s) s = cuda_check(cudaStreamWaitEvent(sd, pipe->in1, 0), "wave 1 wait");
+        if (!s && pipe->in1) s = cuda_check(cudaStreamWaitEvent(sd, pipe->in1, 0), "wave 1 wait");
         if (!s) s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, sd, 1);
         if (s) return s;
         rec(0, sd);
@@ -711,12 +742,11 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     uint8_t *k_d = w + off;   off += al256(T * kvrow);
     uint8_t *v_d = w + off;
     cudaStream_t st = (cudaStream_t)stream;
+    s = ensure_hi(pool);
+    if (s) return s;
     if (!pool->h2d) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
         s = cuda_check(cudaStreamCreateWithFlags(&pool->h2d, cudaStreamNonBlocking), "copy stream");
-        if (!s) s = cuda_check(cudaStreamCreateWithPriority(&pool->side_hi, cudaStreamNonBlocking, hi), "tc stream");
-        for (cudaEvent_t *e : {&pool->ev_in0, &pool->ev_in1, &pool->ev_tc, &pool->ev_d2h})
+        for (cudaEvent_t *e : {&pool->ev_in0, &pool->ev_in1, &pool->ev_d2h})
             if (!s) s = cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event create");
         if (s) return s;
     }

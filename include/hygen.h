@@ -181,9 +181,21 @@ HG_API hg_status hg_hybrid_step(hg_kv_pool *pool, const hg_batch *batch, int32_t
                                 size_t workspace_bytes, void *stream, const hg_attn_opts *opts);
 
 /* End-to-end serving step with HOST buffers (the e2e measurement of the
- * bench): H2D of q/k_new/v_new (host bf16, pinned for async overlap) into the
- * workspace, hg_kv_append, hg_hybrid_attention, D2H of out.  Synchronises the
- * stream before returning so out_host is valid. */
+ * bench): q/k_new/v_new (host bf16 [T][H][d], pinned for async overlap) are
+ * copied into the workspace, appended and attended, and out_host [T][H_q][d]
+ * receives O.  Pipelined in two input waves on library-owned streams (a copy
+ * stream and a high-priority tcgen05 stream, ordered after the caller's
+ * `stream`): the decode rows' (n_i = 1) Q/K/V go up first and feed their
+ * append + split-K on `stream` while the prefill-chunk rows' copies are still in
+ * flight; those feed their append + the tcgen05 tiles, whose O rows are copied
+ * back as soon as the tiles end; the decode rows' O follows the combine.
+ * (One wave -- all copies, then the fused step -- when a decode item would read
+ * a prefill row, e.g. head_dim without tcgen05 support, or with RoPE.)  Same
+ * validation and errors as hg_hybrid_step; nothing is copied or launched on
+ * error.  Synchronises `stream` (which has joined the library streams) before
+ * returning, so out_host is valid and the host buffers may be reused.
+ * Workspace: hg_hybrid_step_host_workspace_size (the attention workspace plus
+ * device copies of q, out, k_new, v_new). */
 HG_API hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
                               const void *q_host, const void *k_new_host, const void *v_new_host,
                               void *out_host, void *workspace, size_t workspace_bytes, void *stream);

@@ -314,10 +314,15 @@ typedef struct {
 #define HG_MASK_EQ1   (HG_FEAT_S_P | HG_FEAT_S_P2 | HG_FEAT_S_D2 | HG_FEAT_N_P | HG_FEAT_N_D)
 #define HG_MASK_EQ2   (HG_FEAT_S_P | HG_FEAT_S_P2 | HG_FEAT_N_P | HG_FEAT_N_D)
 #define HG_MASK_ATTN  (HG_FEAT_S_P | HG_FEAT_P2 | HG_FEAT_D_CTX | HG_FEAT_N_D | HG_FEAT_N_P)
+/* Fit option (OR into the mask): minimise the squared RELATIVE error
+ * sum_i ((w.x_i - y_i) / y_i)^2 -- linear regression weighted by 1 / y_i^2, the
+ * least-squares criterion closest to the MAPE the paper reports;
+ * requires every y_i > 0. */
+#define HG_FIT_RELATIVE (1 << 8)
 
 typedef struct {
     double w[9];          /* w[0] intercept, w[1+k] feature k (0 for unselected) */
-    int32_t feature_mask; /* HG_FEAT_* bits used by the fit */
+    int32_t feature_mask; /* HG_FEAT_* bits used by the fit (| HG_FIT_RELATIVE if set) */
     int32_t n_samples;
     double train_mape;    /* mean |pred - y| / y on the training set */
 } hg_predictor;

@@ -81,10 +81,18 @@ def design(X, mask: int):
     return np.hstack([np.ones((X.shape[0], 1)), X[:, cols]]), cols
 
 
-def fit(X, y, mask: int):
-    """OLS: minimise ||A w - y||_2 with A = [1, selected features]."""
+def fit(X, y, mask: int, relative: bool = False):
+    """OLS: minimise ||A w - y||_2 with A = [1, selected features].
+
+    relative=True (HG_FIT_RELATIVE): minimise sum_i ((A w - y)_i / y_i)^2, i.e.
+    the same regression with row i divided by y_i (weights 1 / y_i^2) -- the
+    least-squares criterion nearest to the MAPE of P:414.  Needs y > 0."""
     A, cols = design(X, mask)
-    w_sel, *_ = np.linalg.lstsq(A, np.asarray(y, np.float64), rcond=None)
+    y = np.asarray(y, np.float64)
+    if relative:
+        assert np.all(y > 0)
+        A, y = A / y[:, None], np.ones_like(y)
+    w_sel, *_ = np.linalg.lstsq(A, y, rcond=None)
     w = np.zeros(9)
     w[0] = w_sel[0]
     for k, col in enumerate(cols):

@@ -24,6 +24,7 @@ HG_FEAT_S_P, HG_FEAT_S_D, HG_FEAT_S_P2, HG_FEAT_S_D2, HG_FEAT_N_P, HG_FEAT_N_D, 
 HG_MASK_EQ1 = HG_FEAT_S_P | HG_FEAT_S_P2 | HG_FEAT_S_D2 | HG_FEAT_N_P | HG_FEAT_N_D
 HG_MASK_EQ2 = HG_FEAT_S_P | HG_FEAT_S_P2 | HG_FEAT_N_P | HG_FEAT_N_D
 HG_MASK_ATTN = HG_FEAT_S_P | HG_FEAT_P2 | HG_FEAT_D_CTX | HG_FEAT_N_D | HG_FEAT_N_P
+HG_FIT_RELATIVE = 1 << 8   # OR into the mask: least squares on (pred - y) / y
 
 
 class HgError(RuntimeError):

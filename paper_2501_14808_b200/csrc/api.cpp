@@ -862,7 +862,11 @@ static void feat_vec(const hg_features &f, double x[8]) {
 
 extern "C" hg_status hg_predictor_fit(const hg_features *X, const double *y, int32_t n, int32_t mask,
                                       hg_predictor *out) {
-    if (!X || !y || !out || n < 1 || (mask & ~0xFF)) return fail(HG_E_INVALID, "bad arguments");
+    if (!X || !y || !out || n < 1 || (mask & ~0x1FF)) return fail(HG_E_INVALID, "bad arguments");
+    const bool rel = mask & HG_FIT_RELATIVE;
+    if (rel)
+        for (int i = 0; i < n; ++i)
+            if (!(y[i] > 0)) return fail(HG_E_INVALID, "HG_FIT_RELATIVE needs y > 0 (y[%d] = %g)", i, y[i]);
     int cols[8], k = 0;
     for (int b = 0; b < 8; ++b)
         if (mask >> b & 1) cols[k++] = b;
@@ -875,6 +879,10 @@ extern "C" hg_status hg_predictor_fit(const hg_features *X, const double *y, int
         feat_vec(X[i], x);
         A[i] = 1.0;
         for (int j = 0; j < k; ++j) A[(size_t)(j + 1) * n + i] = x[cols[j]];
+        if (rel) {   // row i weighted by 1 / y_i: residual (w.x_i - y_i) / y_i
+            for (int j = 0; j < p; ++j) A[(size_t)j * n + i] /= y[i];
+            b[i] = 1.0;
+        }
     }
     for (int j = 0; j < p; ++j) {
         double m = 0;

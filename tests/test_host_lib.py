@@ -281,6 +281,24 @@ def test_fit_matches_oracle_lstsq(mask):
     assert abs(m.train_mape - OP.mape(yh, y)) < 1e-9
 
 
+@pytest.mark.parametrize("mask", [OP.MASK_GRADED, OP.MASK_EQ2_IDENT, 0])
+def test_relative_fit_matches_oracle(mask):
+    rng = np.random.default_rng(100 + mask)
+    X = _rand_X(rng, 600)
+    y = 0.05 + X @ np.array([1e-4, 0, 1e-9, 1e-6, 2e-3, 3e-3, 4e-7, 5e-8])
+    y = y * np.exp(0.1 * rng.standard_normal(600))
+    m = hg.hg_predictor_fit([hg.features_from_array(x) for x in X], y, mask | hg.HG_FIT_RELATIVE)
+    w = OP.fit(X, y, mask, relative=True)
+    np.testing.assert_allclose(np.array(m.w[:]), w, rtol=1e-7, atol=1e-12)
+    assert m.feature_mask == mask | hg.HG_FIT_RELATIVE
+    yh = [OP.predict(w, x) for x in X]
+    assert abs(m.train_mape - OP.mape(yh, y)) < 1e-9
+    y[3] = 0.0
+    with pytest.raises(hg.HgError) as e:
+        hg.hg_predictor_fit([hg.features_from_array(x) for x in X], y, mask | hg.HG_FIT_RELATIVE)
+    assert e.value.status == hg.HG_E_INVALID
+
+
 def test_fit_noise_free_recovery():
     rng = np.random.default_rng(9)
     X = _rand_X(rng, 300)

@@ -150,3 +150,48 @@ def test_fit_noisy_heldout_mape():
     X, y = _synthetic(2000, rng, w_true, P.MASK_EQ2_IDENT, noise=0.01)
     w = P.fit(X[:1600], y[:1600], P.MASK_EQ2_IDENT)
     assert P.mape([P.predict(w, x) for x in X[1600:]], y[1600:]) < 0.02
+
+
+# ---- relative-error fit (HG_FIT_RELATIVE) ------------------------------------------
+def test_relative_fit_intercept_only_closed_form():
+    """mask 0: minimise sum (w0 / y_i - 1)^2  =>  w0 = sum(1/y) / sum(1/y^2)."""
+    rng = np.random.default_rng(3)
+    y = rng.uniform(0.05, 3.0, 200)
+    X = np.zeros((200, 8))
+    w = P.fit(X, y, 0, relative=True)
+    assert abs(w[0] - np.sum(1 / y) / np.sum(1 / y ** 2)) < 1e-12 * w[0]
+    assert abs(P.fit(X, y, 0)[0] - y.mean()) < 1e-12   # OLS: the mean
+
+
+def test_relative_fit_noise_free_and_scale_invariant():
+    rng = np.random.default_rng(11)
+    X = np.abs(rng.standard_normal((300, 8))) * [100, 1, 1e4, 1, 3, 5, 1e5, 1e4]
+    A, cols = P.design(X, P.MASK_GRADED)
+    wt = np.r_[0.03, np.abs(rng.standard_normal(len(cols))) * 1e-5]
+    y = A @ wt
+    w = P.fit(X, y, P.MASK_GRADED, relative=True)
+    np.testing.assert_allclose(np.r_[w[0], w[1:][cols]], wt, rtol=1e-8)
+    yn = y * (1 + 0.05 * rng.standard_normal(300))
+    w1 = P.fit(X, yn, P.MASK_GRADED, relative=True)
+    w2 = P.fit(X, 7.0 * yn, P.MASK_GRADED, relative=True)
+    np.testing.assert_allclose(w2, 7.0 * w1, rtol=1e-9, atol=1e-18)
+
+
+def test_relative_fit_optimal_for_its_criterion():
+    """Each fit is optimal under its own criterion: the relative fit has the
+    smaller sum of squared relative errors, OLS the smaller sum of squares."""
+    rng = np.random.default_rng(12)
+    X = np.abs(rng.standard_normal((400, 8))) * 50
+    y = 0.02 + X @ np.abs(rng.standard_normal(8)) * 1e-3
+    y = y * np.exp(0.2 * rng.standard_normal(400))
+    wr = P.fit(X, y, P.MASK_GRADED, relative=True)
+    wo = P.fit(X, y, P.MASK_GRADED)
+    pr = np.array([wr[0] + wr[1:] @ x for x in X])
+    po = np.array([wo[0] + wo[1:] @ x for x in X])
+    assert np.sum(((pr - y) / y) ** 2) <= np.sum(((po - y) / y) ** 2)
+    assert np.sum((po - y) ** 2) <= np.sum((pr - y) ** 2)
+    # small perturbations of the relative solution never lower its criterion
+    for k in range(20):
+        d = wr + rng.standard_normal(9) * 1e-3 * (np.abs(wr) + 1e-12) * (np.r_[1, [(P.MASK_GRADED >> i) & 1 for i in range(8)]])
+        pd = np.array([d[0] + d[1:] @ x for x in X])
+        assert np.sum(((pd - y) / y) ** 2) >= np.sum(((pr - y) / y) ** 2) - 1e-12

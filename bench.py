@@ -450,7 +450,7 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
     out = torch.empty_like(q)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ws = None
-    X, y, T, pre = [], [], [], []
+    X, y, T, pre, stats = [], [], [], [], []
     for k, spec in enumerate(specs):
         lay = make_layout(spec, seed=k, num_blocks=N)
         b = hg.Batch(lay.block_table, [r.c for r in spec.requests], [r.n for r in spec.requests],
@@ -466,6 +466,7 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
             hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, ops[r])
         torch.cuda.synchronize()
         st = hg.hg_last_plan_stats(pool)
+        stats.append([st[k] for k in ("tc_tiles", "prefix_tiles", "splitk_items", "combine_rows", "kernels")])
         first = 0 if st["tc_tiles"] else 2 if st["splitk_items"] else 4
         last = 5 if st["combine_rows"] else 3 if st["splitk_items"] else 1
         y.append(statistics.median(e[first].elapsed_time(e[last]) for e in evs))
@@ -475,6 +476,9 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
         pre.append(sp / spec.T)
     pool.close()
     X, y = np.array(X), np.array(y)
+    if os.environ.get("HG_SAVE_SWEEP"):   # raw sweep for offline residual analysis
+        np.savez(os.path.join(os.environ["HG_SAVE_SWEEP"], f"sweep_{shape}.npz"), X=X, y=y, T=np.array(T),
+                 stats=np.array(stats))
     rng = np.random.default_rng(1)
     perm = rng.permutation(len(y))
     ntr = int(0.8 * len(y))

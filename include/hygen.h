@@ -147,6 +147,10 @@ typedef struct {
                                    append prologue rotates k_new into the cache and q into a workspace
                                    copy that the attention kernels read (cached keys were appended with
                                    the same rope).  HG_E_INVALID in hg_hybrid_attention_ex. */
+    int32_t disable_prefill_split; /* 1: never cut a prefill chunk's keys into ranges.  0 (default): when
+                                   the prefill items would fill < half the SMs, each chunk's cached keys
+                                   are cut at KV-tile boundaries into ranges written as partials and
+                                   merged by the combine kernel (small chunks at long contexts) */
 } hg_attn_opts;
 
 /* Bytes of device workspace hg_hybrid_attention needs for this batch. */

@@ -389,6 +389,7 @@ static PlanOpts plan_opts(const hg_kv_pool *pool, const hg_attn_opts *o) {
         po.split_tokens = o->split_tokens;
         po.prefix_pass = !o->disable_prefix_pass;
         po.use_tc = !o->disable_tc;
+        po.split_prefill = !o->disable_prefill_split;
         if (o->num_sms > 0) po.num_sms = o->num_sms;
     }
     return po;

@@ -14,6 +14,7 @@ constexpr int kBlock = 16;        // KV block size B handled by the kernels
 constexpr int kSkRows = 16;       // query rows per split-K item (one m16 MMA tile)
 constexpr int kTcRows = 128;      // query rows per tcgen05 tile (UMMA M)
 constexpr int kTcKeys = 128;      // keys per tcgen05 KV tile (UMMA N of S = Q K^T)
+constexpr int kMaxCuts = 64;      // key ranges per prefill request (build_plan)
 constexpr int kMaxOuts = 8;       // O copies one launch writes (ranks of a peer window)
 
 // Per-request record in the device descriptor.
@@ -142,6 +143,7 @@ struct PlanOpts {
     int split_tokens = 0;
     bool prefix_pass = true;
     bool use_tc = true;
+    bool split_prefill = true;   // key-range cuts of long prefill items when the grid is sparse
     int num_sms = 148;
 };
 hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpts &o, Plan *p);

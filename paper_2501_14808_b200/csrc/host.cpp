@@ -68,6 +68,7 @@ struct Scratch {
     // build_plan: prefix-pass extent of each row and its tile-map nodes
     struct Node { int32_t a, e, rep, depth, nm, first; };
     std::vector<int32_t> pre_end, npre;
+    std::vector<int32_t> np;      // key ranges of each prefill request (1: whole)
     std::vector<Node> nodes;
 };
 static thread_local Scratch g_scr;
@@ -328,6 +329,37 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             if (v.n[i] > 1) n256 += (int64_t)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows);
         for (const Scratch::Node &nd : sc.nodes) n256 += (int64_t)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows);
         if (n256 >= o.num_sms) ipr = 2 * kTcRows;
+        // Few prefill items over long cached contexts (a small chunk budget at a
+        // long prompt: one item = one CTA walking thousands of keys while most SMs
+        // idle): cut each such request's keys into np_i ranges at KV-tile
+        // boundaries inside its cached prefix (visible to every row), the last
+        // range holding the causal diagonal; the ranges write partials that the
+        // combine kernel merges like split-K's.  np_i fills about one wave of
+        // 256-row items.
+        // Only where the tiles would be the step's long pole: the decode rows'
+        // split-K pass is HBM-bound (~its unique KV bytes / 6.5 TB/s) and a
+        // 256-row item advances ~1.5 us per 128-key tile, so a chunk is cut into
+        // pieces no longer than max(split-K time, 8 tiles); beside a large decode
+        // pass the extra CTAs would only take SMs from split-K.
+        sc.np.assign((size_t)v.R, 1);
+        const int np_cap = (int)std::min<int64_t>(kMaxCuts, o.num_sms / std::max<int64_t>(n256, 1));
+        if (o.split_prefill && np_cap > 1) {
+            constexpr double kTileUs = 1.5, kHbmBytesPerUs = 6.5e6;
+            double dec_keys = 0;
+            for (int i = 0; i < v.R; ++i)
+                if (v.n[i] == 1) dec_keys += (double)v.c[i] + 1 - (double)sc.pre_end[i] * B;
+            const double sk_us = dec_keys * H_kv * 4.0 * d / kHbmBytesPerUs;
+            const double target_us = std::max(sk_us, 8 * kTileUs);
+            bool any = false;
+            for (int i = 0; i < v.R; ++i)
+                if (v.n[i] > 1) {
+                    const double chain_us = (double)ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs;
+                    const int want = (int)std::ceil(chain_us / target_us);
+                    sc.np[i] = std::max(1, std::min({want, np_cap, 1 + v.c[i] / (2 * kTcKeys)}));
+                    any |= sc.np[i] > 1;
+                }
+            if (any) ipr = 2 * kTcRows;
+        }
     }
     // algorithmic unique KV tokens U: every shared block counted once
     {
@@ -343,6 +375,29 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         for (int i = 0; i < v.R; ++i) {
             if (v.n[i] <= 1) continue;
             const int rows = v.n[i] * G;
+            // key-range cuts of request i (sc.np[i] > 1): multiples of kTcKeys inside
+            // its first c_i keys, spreading the ~ceil((c_i + n_i) / 128) tiles evenly
+            int np = tc_ok ? sc.np[i] : 1;
+            int32_t cut[kMaxCuts + 1];
+            if (np > 1) {
+                const int64_t nt = ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys), tc_full = v.c[i] / kTcKeys;
+                np = std::min(np, kMaxCuts);
+                int m = 0;
+                cut[m++] = 0;
+                for (int k = 1; k < np; ++k) {
+                    const int64_t b = std::min<int64_t>((nt * k + np / 2) / np, tc_full) * kTcKeys;
+                    if (b > cut[m - 1]) cut[m++] = (int32_t)b;
+                }
+                np = m;
+            }
+            if (np > 1) {
+                for (int j = 0; j < v.n[i]; ++j) {
+                    const int t = p->reqs[i].cu_q + j;
+                    p->tok[t] = TokDev{(int32_t)p->n_slots, np, i, 0};
+                    p->n_slots += (int64_t)np * G * H_kv;
+                    p->comb.push_back(t);
+                }
+            }
             for (int g = 0; g < H_kv; ++g) {
                 for (int r0 = 0; r0 < rows; r0 += ipr) {
                     const int nr = std::min(ipr, rows - r0);
@@ -350,7 +405,17 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
                     TcItem it{p->reqs[i].bt_off, g, 0, v.c[i] + j_last + 1, 0, p->reqs[i].cu_q + j0, nr, -1,
                               v.c[i] + j0, r0 - j0 * G};
                     kv_tok_read += it.k1;
-                    p->tc.push_back(it);
+                    if (np == 1) {
+                        p->tc.push_back(it);
+                        continue;
+                    }
+                    for (int k = 0; k < np; ++k) {   // partial k of every row: keys [cut[k], cut[k+1] or k1)
+                        TcItem pc = it;
+                        pc.k0 = cut[k];
+                        pc.k1 = k + 1 < np ? cut[k + 1] : it.k1;
+                        pc.part = k;
+                        p->tc.push_back(pc);
+                    }
                 }
             }
         }

@@ -173,6 +173,48 @@ def test_full_size_sampled(name):
     wl.close()
 
 
+def _prefill_split_spec(case):
+    from synth.configs import Request
+    if case == "c4_small_chunk":   # the C4 shape the predictor under-priced: 128-token chunk at c = 5600
+        return _mixed(case, 32, 8, 128, [Request(5600, 128, True), Request(3000, 1), Request(4000, 1, True),
+                                         Request(100, 1)])
+    if case == "mha_64rows":       # 64-row items (one Q tile), G_q = 1
+        return _mixed(case, 32, 32, 128, [Request(7000, 64)])
+    if case == "gqa5":             # G_q = 5: items end mid-token
+        return _mixed(case, 40, 8, 128, [Request(2500, 77), Request(900, 1, True)])
+    if case == "d64_two_chunks":
+        return _mixed(case, 32, 8, 64, [Request(3000, 200), Request(10, 1), Request(1500, 33, True)])
+    if case == "short_ctx":        # c_i < 256: no cut possible for this chunk, the other one is cut
+        return _mixed(case, 32, 8, 128, [Request(200, 100), Request(4096, 100)])
+    raise KeyError(case)
+
+
+@pytest.mark.parametrize("case", ["c4_small_chunk", "mha_64rows", "gqa5", "d64_two_chunks", "short_ctx"])
+def test_prefill_key_split(case):
+    """Sparse tcgen05 grid (few prefill items over long cached contexts): each
+    chunk's keys are cut into ranges written as partials and merged by the
+    combine kernel.  Parity with the oracle, agreement with the unsplit plan,
+    and run-to-run bitwise reproducibility."""
+    import paper_2501_14808_b200 as hg
+    spec = _prefill_split_spec(case)
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    st = hg.hg_last_plan_stats(wl.pool)
+    compare(spec, wl)
+    a = wl.out.clone()
+    wl.attention(hg.make_opts(disable_prefill_split=True))
+    torch.cuda.synchronize()
+    st0 = hg.hg_last_plan_stats(wl.pool)
+    assert st["tc_tiles"] > st0["tc_tiles"] and st["combine_rows"] > st0["combine_rows"], (st, st0)
+    assert (a.double() - wl.out.double()).abs().max().item() <= MAX_ABS
+    compare(spec, wl, tag=" (unsplit)")
+    wl.attention()
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int16), wl.out.view(torch.int16))
+    wl.close()
+
+
 @pytest.mark.parametrize("name,q_scale", [("p1", 8.0), ("p2", 8.0), ("c1", 4.0), ("c1_long", 4.0)])
 def test_peaked(name, q_scale):
     """§8(c.6) parity matrix: peaked queries (q x 4 / q x 8)."""

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out/pred
-timeout 900 python bench.py --no-extra > gpurun_out/pred/bench.log 2> gpurun_out/pred/bench.err
+HG_SAVE_SWEEP=gpurun_out/pred timeout 900 python bench.py --no-extra > gpurun_out/pred/bench.log 2> gpurun_out/pred/bench.err

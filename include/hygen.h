@@ -198,8 +198,10 @@ HG_API hg_status hg_hybrid_step(hg_kv_pool *pool, const hg_batch *batch, int32_t
  * validation and errors as hg_hybrid_step; nothing is copied or launched on
  * error.  Synchronises `stream` (which has joined the library streams) before
  * returning, so out_host is valid and the host buffers may be reused.
- * Workspace: hg_hybrid_step_host_workspace_size (the attention workspace plus
- * device copies of q, out, k_new, v_new). */
+ * Workspace: hg_hybrid_step_host_workspace_size (device copies of q, out,
+ * k_new, v_new first, then the attention workspace).  The decode rows' copies
+ * are queued before validation; on an error they are drained before the call
+ * returns and nothing else is launched. */
 HG_API hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
                               const void *q_host, const void *k_new_host, const void *v_new_host,
                               void *out_host, void *workspace, size_t workspace_bytes, void *stream);

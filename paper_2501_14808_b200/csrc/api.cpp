@@ -702,7 +702,7 @@ extern "C" hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, 
     int64_t T = 0;
     for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
     const size_t d = pool->desc.head_dim, Hk = pool->desc.num_kv_heads;
-    *bytes = al256(attn) + 2 * al256(T * H_q * d * 2) + 2 * al256(T * Hk * d * 2) + al256(T * 8);
+    *bytes = 2 * al256(T * H_q * d * 2) + 2 * al256(T * Hk * d * 2) + al256(T * 8) + al256(attn);
     return HG_OK;
 }
 
@@ -725,23 +725,23 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     hg_status s = sticky_check();
     if (s) return s;
     if (!q_host || !k_new_host || !v_new_host || !out_host) return fail(HG_E_INVALID, "host buffer NULL");
-    // one validated plan for the whole step (attention_impl reuses pool->plan)
     BatchView v;
-    s = plan_call(pool, batch, H_q, nullptr, &v, &pool->plan, true);
+    s = view_batch(batch, &v);
     if (s) return s;
-    const int64_t T = pool->plan.T;
-    if (T == 0) return HG_OK;
-    const size_t attn = pool->plan.total_bytes;
+    // Workspace: the device copies of q, out, k_new, v_new first (sized by T
+    // alone), then the attention workspace -- so wave 0's copies can start
+    // before the batch is validated and planned.
+    int64_t T = 0;
+    bool rows_ok = true;
+    for (int i = 0; i < v.R; ++i) {
+        rows_ok &= v.n[i] >= 1;
+        T += v.n[i];
+    }
     const size_t d = pool->desc.head_dim, Hk = pool->desc.num_kv_heads;
-    const size_t need = al256(attn) + 2 * al256(T * H_q * d * 2) + 2 * al256(T * Hk * d * 2) + al256(T * 8);
-    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
-    const size_t qrow = (size_t)H_q * d * 2, kvrow = Hk * d * 2;   // bytes per token row
+    const size_t qrow = (size_t)std::max(H_q, 0) * d * 2, kvrow = Hk * d * 2;   // bytes per token row
+    const size_t in_bytes = rows_ok ? 2 * al256(T * qrow) + 2 * al256(T * kvrow) + al256(T * 8) : 0;
     uint8_t *w = (uint8_t *)workspace;
-    size_t off = al256(attn);
-    uint8_t *q_d = w + off;   off += al256(T * qrow);
-    uint8_t *o_d = w + off;   off += al256(T * qrow);
-    uint8_t *k_d = w + off;   off += al256(T * kvrow);
-    uint8_t *v_d = w + off;
+    uint8_t *q_d = w, *o_d = q_d + al256(T * qrow), *k_d = o_d + al256(T * qrow), *v_d = k_d + al256(T * kvrow);
     cudaStream_t st = (cudaStream_t)stream;
     s = ensure_hi(pool);
     if (s) return s;
@@ -753,7 +753,7 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     }
     // row runs [a, b) of each wave (wave 1 = prefill-chunk requests, n_i > 1)
     std::vector<std::pair<int64_t, int64_t>> runs[2];
-    {
+    if (rows_ok) {
         int64_t row = 0;
         for (int i = 0; i < v.R; ++i) {
             auto &rw = runs[v.n[i] > 1 ? 1 : 0];
@@ -762,18 +762,10 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
             row += v.n[i];
         }
     }
-    StepPipe pipe;
-    pipe.in0 = pool->ev_in0;
-    pipe.in1 = pool->ev_in1;
-    pipe.side = pool->side_hi;
-    pipe.tc_done = pool->ev_tc;
-    // the copy stream and the tcgen05 stream start after whatever the caller queued before this step
-    s = cuda_check(cudaEventRecord(pool->ev_d2h, st), "order record");
-    if (!s) s = cuda_check(cudaStreamWaitEvent(pool->h2d, pool->ev_d2h, 0), "order wait");
-    if (!s) s = cuda_check(cudaStreamWaitEvent(pipe.side, pool->ev_d2h, 0), "order wait");
-    if (s) return s;
-    pipe.planned = true;
-    pipe.enqueue_wave = [&](int wv) -> hg_status {
+    bool issued[2] = {false, false};
+    auto enqueue_wave = [&](int wv) -> hg_status {
+        if (issued[wv]) return HG_OK;
+        issued[wv] = true;
         for (auto &r : runs[wv]) {
             const int64_t a = r.first, n = r.second - r.first;
             hg_status e = cuda_check(cudaMemcpyAsync(q_d + a * qrow, (const uint8_t *)q_host + a * qrow, n * qrow,
@@ -786,10 +778,42 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
         }
         return cuda_check(cudaEventRecord(wv ? pool->ev_in1 : pool->ev_in0, pool->h2d), "wave record");
     };
-    const auto t_cp = now();
-    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, workspace, attn, st, nullptr, true, k_d, v_d, nullptr,
-                       &pipe);
+    // the copy stream and the tcgen05 stream start after whatever the caller queued before this step
+    s = cuda_check(cudaEventRecord(pool->ev_d2h, st), "order record");
+    if (!s) s = cuda_check(cudaStreamWaitEvent(pool->h2d, pool->ev_d2h, 0), "order wait");
+    if (!s) s = cuda_check(cudaStreamWaitEvent(pool->side_hi, pool->ev_d2h, 0), "order wait");
     if (s) return s;
+    const bool early = rows_ok && T > 0 && workspace && workspace_bytes >= in_bytes;
+    if (early) {   // wave 0 (decode rows, small) crosses PCIe while the host validates and plans
+        s = enqueue_wave(0);
+        if (s) return s;
+    }
+    // on any error below, the copies already queued finish before returning (they
+    // read the caller's host buffers); nothing else has been launched
+    auto bail = [&](hg_status e) {
+        if (early) cudaStreamSynchronize(pool->h2d);
+        return e;
+    };
+    // one validated plan for the whole step (attention_impl reuses pool->plan)
+    s = plan_call(pool, batch, H_q, nullptr, &v, &pool->plan, true);
+    if (s) return bail(s);
+    if (T == 0) return HG_OK;
+    const size_t attn = pool->plan.total_bytes;
+    const size_t need = in_bytes + al256(attn);
+    if (!workspace || workspace_bytes < need)
+        return bail(fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need));
+    uint8_t *ws_attn = w + in_bytes;
+    StepPipe pipe;
+    pipe.in0 = pool->ev_in0;
+    pipe.in1 = pool->ev_in1;
+    pipe.side = pool->side_hi;
+    pipe.tc_done = pool->ev_tc;
+    pipe.planned = true;
+    pipe.enqueue_wave = enqueue_wave;
+    const auto t_cp = now();
+    s = attention_impl(pool, batch, H_q, q_d, o_d, nullptr, ws_attn, attn, st, nullptr, true, k_d, v_d, nullptr,
+                       &pipe);
+    if (s) return bail(s);
     const auto t_at = now();
     auto d2h = [&](const std::vector<std::pair<int64_t, int64_t>> &rw, cudaStream_t on) -> hg_status {
         for (auto &r : rw) {

@@ -325,6 +325,31 @@ def test_e2e_host_step_matches_device_path(name):
         compare(spec, wl, check_lse=False, tag=" (host step)")
 
 
+def test_e2e_host_step_errors_leave_outputs_untouched():
+    """hg_hybrid_step_host starts the decode rows' copies before validating; an
+    invalid batch must still return its status with out_host and the pool untouched."""
+    import paper_2501_14808_b200 as hg
+    from synth.configs import make_config
+    spec = make_config("toy_a", 0)
+    wl = make(spec)
+    torch.cuda.synchronize()
+    qh, kh, vh = (x.cpu().pin_memory() for x in (wl.q, wl.k_new, wl.v_new))
+    oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16).pin_memory()
+    ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
+                     device="cuda")
+    k_before = wl.k_cache.clone()
+    bad = hg.Batch(wl.lay.block_table, [0, 32, 32], [16, 1, 1], None, [0, 1, 0])   # S shared by r1 only
+    assert hg.status_of(hg.hg_hybrid_step_host, wl.pool, bad, spec.H_q, qh, kh, vh, oh, ws) == hg.HG_E_INVALID
+    small = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    assert hg.status_of(hg.hg_hybrid_step_host, wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, small) == hg.HG_E_INVALID
+    torch.cuda.synchronize()
+    assert torch.all(oh == 7.0) and torch.equal(k_before, wl.k_cache)
+    hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)   # and the next valid call works
+    wl.step()
+    torch.cuda.synchronize()
+    assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16))
+
+
 def test_tp_path_world1_matches_single_gpu():
     """hg_hybrid_attention_tp on a 1-rank NCCL communicator (the only GPU count
     gpurun offers): the sharded path's workspace layout + transpose kernel."""

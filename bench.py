@@ -761,9 +761,8 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
                      device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        wl.append()
-        hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, out, ws, stream)
+    def step():   # the sharded serving step: append of this rank's K/V slice fused with the attention
+        hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, wl.k_new, wl.v_new, out, ws, stream)
 
     for _ in range(args.warmup):
         step()
@@ -812,12 +811,12 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "parallelism": f"kv-head tp{world}, all-gather fused into the epilogues (peer window)",
                        "l2": "KV working set 2.7 GB total > L2"},
-            "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 3) * args.steps,  # + append, 2 barriers
+            "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 2) * args.steps,  # + 2 barriers
             "e2e": {"value": spec.T * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2 * world,
                     "d2h_bytes_per_step": oh.numel() * 2 * world, "ms_per_step": e2e_s / args.steps * 1e3,
-                    "api": "per rank: pinned H2D of its q / k_new / v_new slices, hg_kv_append + "
-                           "hg_hybrid_attention_tp, D2H of the gathered O; slowest rank"},
+                    "api": "per rank: pinned H2D of its q / k_new / v_new slices, hg_hybrid_step_tp "
+                           "(append fused), D2H of the gathered O; slowest rank"},
             "clocks": clk.summary(),
             **({"note": "HG_BENCH_SAME_GPU functional test: all ranks on one GPU, not a scaling number"}
                if same_gpu else {}),

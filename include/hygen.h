@@ -292,6 +292,16 @@ HG_API hg_status hg_hybrid_attention_tp_workspace_size(const hg_kv_pool *pool, c
 HG_API hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
                                  int32_t num_q_heads_total, const void *q_local, void *out_gathered,
                                  void *workspace, size_t workspace_bytes, void *stream);
+/* The sharded serving step: hg_kv_append of this rank's KV-head slice
+ * (k_new_local / v_new_local, dev bf16 [T][H_kv_local][d]) fused with
+ * hg_hybrid_attention_tp, as hg_hybrid_step fuses them on one GPU (one
+ * validation with the append rules, one plan, one descriptor upload, the slots
+ * derived on the device).  Same workspace, window and error rules as
+ * hg_hybrid_attention_tp. */
+HG_API hg_status hg_hybrid_step_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
+                                   int32_t num_q_heads_total, const void *q_local, const void *k_new_local,
+                                   const void *v_new_local, void *out_gathered, void *workspace,
+                                   size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* Batch-latency predictor (§4.2 Eq. 1; App. B Eq. 2)  */

@@ -104,6 +104,7 @@ _SIGS = {
     "hg_hybrid_attention_tp_proj": ([P, P, P, i32, P, P, i32, P, P, ctypes.c_size_t, P], i32),
     "hg_hybrid_attention_tp_workspace_size": ([P, P, P, i32, P], i32),
     "hg_hybrid_attention_tp": ([P, P, P, i32, P, P, P, ctypes.c_size_t, P], i32),
+    "hg_hybrid_step_tp": ([P, P, P, i32, P, P, P, P, P, ctypes.c_size_t, P], i32),
     "hg_batch_features": ([P, i32, P], i32),
     "hg_predictor_fit": ([P, P, i32, i32, P], i32),
     "hg_predictor_predict": ([P, P], ctypes.c_double),
@@ -408,6 +409,14 @@ def hg_hybrid_attention_tp(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_t
     _check(lib().hg_hybrid_attention_tp(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local),
                                         _ptr(out_gathered), _ptr(workspace),
                                         workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+
+
+def hg_hybrid_step_tp(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_total: int, q_local, k_new_local,
+                      v_new_local, out_gathered, workspace, stream=None) -> None:
+    """Fused sharded step: append of this rank's KV-head slice + hg_hybrid_attention_tp."""
+    _check(lib().hg_hybrid_step_tp(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local), _ptr(k_new_local),
+                                   _ptr(v_new_local), _ptr(out_gathered), _ptr(workspace),
+                                   workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
 
 
 def hg_out_proj_rs(comm: Comm, T: int, K: int, N: int, o_local, w_local, y_shard, stream=None) -> None:

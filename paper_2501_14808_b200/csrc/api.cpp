@@ -424,10 +424,11 @@ extern "C" hg_status hg_hybrid_attention_workspace_size(const hg_kv_pool *pool, 
 static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, void *out,
                                 float *lse, void *ws, size_t ws_bytes, cudaStream_t st, const hg_attn_opts *o,
                                 bool fused = false, const void *k_new = nullptr, const void *v_new = nullptr,
-                                const OutSpec *outs = nullptr, StepPipe *pipe = nullptr) {
+                                const OutSpec *outs = nullptr, StepPipe *pipe = nullptr, bool planned = false) {
     BatchView v;
     Plan &plan = pool->plan;
-    hg_status s = (pipe && pipe->planned) ? view_batch(batch, &v) : plan_call(pool, batch, H_q, o, &v, &plan, fused);
+    hg_status s = (planned || (pipe && pipe->planned)) ? view_batch(batch, &v)
+                                                       : plan_call(pool, batch, H_q, o, &v, &plan, fused);
     if (s) return s;
     s = sticky_check();
     if (s) return s;
@@ -653,6 +654,22 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
 }
 
 namespace hg {
+// Validate + plan once for a sharded call (pool->plan); the attention workspace bytes.
+hg_status plan_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, bool append, size_t *bytes) {
+    BatchView v;
+    hg_status s = plan_call(pool, batch, H_q, nullptr, &v, &pool->plan, append);
+    if (s) return s;
+    *bytes = pool->plan.total_bytes;
+    return HG_OK;
+}
+// Attention (fused with the append when k_new != NULL) on the plan already in
+// pool->plan, O to every destination of `outs` (or to `out` when outs == NULL).
+hg_status attention_planned(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q,
+                            const void *k_new, const void *v_new, void *out, const OutSpec *outs, void *ws,
+                            size_t ws_bytes, void *stream) {
+    return attention_impl(pool, batch, H_q, q, out, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                          k_new != nullptr, k_new, v_new, outs, nullptr, true);
+}
 hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
                        void *ws, size_t ws_bytes, void *stream) {
     return attention_impl(pool, batch, H_q, q, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr, false,

@@ -184,20 +184,21 @@ extern "C" hg_status hg_hybrid_attention_tp_workspace_size(const hg_kv_pool *poo
     return HG_OK;
 }
 
-extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
-                                            const void *q_local, void *out_gathered, void *workspace,
-                                            size_t workspace_bytes, void *stream) {
+// Shared body of hg_hybrid_attention_tp / hg_hybrid_step_tp: one validated plan
+// per call; k_new != NULL fuses the append (this rank's KV-head slice).
+static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q, const void *q_local,
+                         const void *k_new, const void *v_new, void *out_gathered, void *workspace,
+                         size_t workspace_bytes, void *stream) {
     if (!pool || !comm || !batch) return fail(HG_E_INVALID, "NULL argument");
-    size_t need = 0;
-    hg_status s = hg_hybrid_attention_tp_workspace_size(pool, comm, batch, H_q, &need);
-    if (s) return s;
-    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    if (H_q % comm->world) return fail(HG_E_INVALID, "num_q_heads %d not divisible by world %d", H_q, comm->world);
     const int G = comm->world, Hl = H_q / G, d = pool_head_dim(pool);
+    size_t attn = 0;
+    hg_status s = plan_attention(pool, batch, Hl, k_new != nullptr, &attn);
+    if (s) return s;
     int64_t T = 0;
     for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
-    size_t attn = 0;
-    s = hg_hybrid_attention_workspace_size(pool, batch, Hl, &attn);
-    if (s) return s;
+    const size_t need = al256(attn) + al256((size_t)T * H_q * d * 2);
+    if (!workspace || workspace_bytes < need) return fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
     const size_t out_bytes = (size_t)T * H_q * d * 2;
     if (comm->open && out_bytes <= comm->win_bytes) {
         // v2: every epilogue stores its O rows into all ranks' windows, at this
@@ -213,7 +214,7 @@ extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, con
         os.n = G;
         os.ld = (int64_t)H_q * d;
         for (int k = 0; k < G; ++k) os.ptr[k] = (uint16_t *)(comm->peer[k] + kWinHdr) + (size_t)comm->rank * Hl * d;
-        s = attention_to(pool, batch, Hl, q_local, os, workspace, attn, stream);
+        s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream);
         if (s) return s;
         s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
         if (s) return s;
@@ -231,15 +232,30 @@ extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, con
     uint16_t *gather = (uint16_t *)(w + al256(attn));  // [G][T][Hl][d], rank-major (NCCL layout)
     const size_t count = (size_t)T * Hl * d;
     uint16_t *mine = gather + (size_t)comm->rank * count;
-    s = hg_hybrid_attention(pool, batch, Hl, q_local, mine, nullptr, workspace, attn, stream);
-    if (s) return s;
     if (T == 0) return HG_OK;
+    s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, mine, nullptr, workspace, attn, stream);
+    if (s) return s;
     if (G > 1) {
         nccl_result r = g_nccl.AllGather(mine, gather, count, kNcclBf16, comm->comm, (cudaStream_t)stream);
         if (r) return fail(HG_E_NCCL, "ncclAllGather: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
     }
     // [G][T][Hl*d] -> [T][G*Hl*d]
     return launch_gather_transpose(gather, (uint16_t *)out_gathered, G, (int)T, Hl * d, stream);
+}
+
+extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
+                                            const void *q_local, void *out_gathered, void *workspace,
+                                            size_t workspace_bytes, void *stream) {
+    return tp_call(pool, comm, batch, H_q, q_local, nullptr, nullptr, out_gathered, workspace, workspace_bytes,
+                   stream);
+}
+
+extern "C" hg_status hg_hybrid_step_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
+                                       const void *q_local, const void *k_new_local, const void *v_new_local,
+                                       void *out_gathered, void *workspace, size_t workspace_bytes, void *stream) {
+    if (!k_new_local || !v_new_local) return fail(HG_E_INVALID, "k_new / v_new NULL");
+    return tp_call(pool, comm, batch, H_q, q_local, k_new_local, v_new_local, out_gathered, workspace,
+                   workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------

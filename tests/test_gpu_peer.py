@@ -72,9 +72,12 @@ def test_window_world1(zero_copy):
                      dtype=torch.uint8, device="cuda")
     win = comm.window((spec.T, spec.H_q, spec.d))
     out = win if zero_copy else torch.empty_like(wl.out)
-    for _ in range(3):   # epochs advance; flags only grow
+    for it in range(4):   # epochs advance; flags only grow
         out.fill_(0)
-        hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, out, ws)
+        if it == 3:   # fused sharded step
+            hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, wl.k_new, wl.v_new, out, ws)
+        else:
+            hg.hg_hybrid_attention_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, out, ws)
         torch.cuda.synchronize()
         assert torch.equal(out.view(torch.int16), wl.out.view(torch.int16))
     comm.close()
@@ -123,16 +126,24 @@ def _rank_main(rank, world, port, names, q):
         for name in names:
             spec = _spec(name)
             wl = Workload(spec)          # same seeded values in every process
+            wl.step()                    # new tokens in the cache: the fused step re-appends the same values
+            torch.cuda.synchronize()
             ref = _reference_slices(hg, wl, spec, world, dev)
             k, v, ql = _slice_inputs(wl, spec, world, rank)
             pool = hg.KVPool(k, v, wl.lay.num_blocks, spec.B, spec.H_kv // world, spec.d, dev)
             ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(pool, comm, wl.batch, spec.H_q),
                              dtype=torch.uint8, device="cuda")
-            for it in range(3):
+            Hk = spec.H_kv // world
+            kn = wl.k_new[:, rank * Hk:(rank + 1) * Hk].contiguous()
+            vn = wl.v_new[:, rank * Hk:(rank + 1) * Hk].contiguous()
+            for it in range(4):
                 zero_copy = it == 1
                 out = comm.window((spec.T, spec.H_q, spec.d)) if zero_copy else \
                     torch.full((spec.T, spec.H_q, spec.d), float("nan"), dtype=torch.bfloat16, device="cuda")
-                hg.hg_hybrid_attention_tp(pool, comm, wl.batch, spec.H_q, ql, out, ws)
+                if it == 3:   # the fused sharded step (re-appends the same K/V slice: idempotent)
+                    hg.hg_hybrid_step_tp(pool, comm, wl.batch, spec.H_q, ql, kn, vn, out, ws)
+                else:
+                    hg.hg_hybrid_attention_tp(pool, comm, wl.batch, spec.H_q, ql, out, ws)
                 torch.cuda.synchronize()
                 ok = torch.equal(out.view(torch.int16), ref.view(torch.int16))
                 res.append((name, it, bool(ok)))
@@ -167,4 +178,4 @@ def test_two_ranks_same_gpu_peer_window():
     for r in range(2):
         bad = [x for x in got[r] if not x[2]]
         assert not bad, (r, bad)
-        assert len(got[r]) == 3 * len(names)
+        assert len(got[r]) == 4 * len(names)

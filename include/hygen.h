@@ -226,6 +226,24 @@ typedef struct {
 } hg_plan_stats;
 HG_API hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *out);
 
+/* Host-only plan inspection (tests, no GPU): validates `batch` against a pool
+ * of num_blocks blocks and builds the work plan hg_hybrid_attention would run
+ * (use_tc = 1: as on a device with the tcgen05 path; num_sms: the grid it is
+ * sized for), then lists, for every query row (token t, q head h) of every work
+ * item, the key range [k0, k1) it attends there (causal cap applied) and the
+ * partial index it writes (-1: the row's only range, written directly).
+ * kind: 0 prefill tile (tcgen05), 1 shared-prefix node tile (tcgen05), 2
+ * split-K item.  nparts: ranges the token's rows are merged from.  The ranges of
+ * a row must tile [0, c_i + j + 1) exactly once -- the a.4 tile map, the split-K
+ * plan and the prefill key cuts are checked that way.  Writes min(cap, total)
+ * rows; *n_rows = total. */
+typedef struct {
+    int32_t t, h, k0, k1, part, kind, nparts;
+} hg_plan_row;
+HG_API hg_status hg_plan_rows(const hg_batch *batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
+                              int32_t num_blocks, int32_t num_sms, int32_t use_tc, const hg_attn_opts *opts,
+                              hg_plan_row *rows, int64_t cap, int64_t *n_rows);
+
 /* ------------------------------------------------------------------------ */
 /* Multi-GPU: KV-head sharding + all-gather of outputs (§8(e); TP)    */
 /* ------------------------------------------------------------------------ */

@@ -94,6 +94,7 @@ _SIGS = {
     "hg_hybrid_step_host_workspace_size": ([P, P, i32, P], i32),
     "hg_batch_indices": ([P, P, P, P, P, P], i32),
     "hg_last_plan_stats": ([P, P], i32),
+    "hg_plan_rows": ([P, i32, i32, i32, i32, i32, i32, P, P, ctypes.c_int64, P], i32),
     "hg_comm_unique_id": ([P], i32),
     "hg_comm_init": ([P, i32, i32, i32, P], i32),
     "hg_comm_destroy": ([P], i32),
@@ -318,6 +319,18 @@ def hg_batch_indices(pool: KVPool, batch: Batch):
     pg = np.zeros(max(R, 1), np.int32)
     _check(lib().hg_batch_indices(pool.h, batch.ref(), _ptr(cu), _ptr(kv), _ptr(slot), _ptr(pg)))
     return cu, kv[:R], slot[:T], pg[:R]
+
+
+def hg_plan_rows(batch: Batch, num_q_heads: int, num_kv_heads: int, head_dim: int, num_blocks: int,
+                 num_sms: int = 148, use_tc: bool = True, opts: Optional[hg_attn_opts] = None) -> np.ndarray:
+    """Host-only plan inspection: int32 [n][7] rows (t, h, k0, k1, part, kind, nparts), see hygen.h."""
+    n = ctypes.c_int64()
+    args = (batch.ref(), num_q_heads, num_kv_heads, head_dim, num_blocks, num_sms, int(use_tc),
+            None if opts is None else ctypes.byref(opts))
+    _check(lib().hg_plan_rows(*args, None, 0, ctypes.byref(n)))
+    out = np.zeros((n.value, 7), np.int32)
+    _check(lib().hg_plan_rows(*args, _ptr(out), n.value, ctypes.byref(n)))
+    return out
 
 
 def hg_last_plan_stats(pool: KVPool) -> dict:

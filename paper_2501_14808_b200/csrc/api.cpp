@@ -700,6 +700,52 @@ extern "C" hg_status hg_hybrid_attention(hg_kv_pool *pool, const hg_batch *batch
                                   nullptr);
 }
 
+extern "C" hg_status hg_plan_rows(const hg_batch *batch, int32_t H_q, int32_t H_kv, int32_t d, int32_t num_blocks,
+                                  int32_t num_sms, int32_t use_tc, const hg_attn_opts *o, hg_plan_row *rows,
+                                  int64_t cap, int64_t *n_rows) {
+    if (!n_rows || (cap > 0 && !rows) || num_sms < 1) return fail(HG_E_INVALID, "bad arguments");
+    BatchView v;
+    hg_status s = view_batch(batch, &v);
+    if (s) return s;
+    s = validate(v, kBlock, num_blocks, H_q, H_kv, false);
+    if (s) return s;
+    PlanOpts po;
+    po.num_sms = num_sms;
+    if (o) {
+        po.split_tokens = o->split_tokens;
+        po.prefix_pass = !o->disable_prefix_pass;
+        po.split_prefill = !o->disable_prefill_split;
+        if (o->disable_tc) use_tc = 0;
+    }
+    po.use_tc = use_tc != 0;
+    static thread_local Plan plan;
+    s = build_plan(v, H_q, H_kv, d, po, &plan);
+    if (s) return s;
+    const int G = H_q / H_kv;
+    int64_t n = 0;
+    auto emit = [&](int t, int h, int k0, int k1, int part, int kind) {
+        if (n < cap) rows[n] = hg_plan_row{t, h, k0, k1, part, kind, plan.tok[t].nparts};
+        ++n;
+    };
+    for (const TcItem &it : plan.tc)
+        for (int r = 0; r < it.nrows; ++r) {
+            const int x = it.hl0 + r, j = x / G, h = it.g * G + x % G;
+            if (it.mode == 0) emit(it.t0 + j, h, it.k0, std::min(it.k1, it.pos0 + j + 1), it.part, 0);
+            else emit(plan.tc_tok[it.t0 + j], h, it.k0, it.k1, it.part, 1);
+        }
+    for (const SkItem &it : plan.sk) {
+        const ReqDev &rq = plan.reqs[it.req];
+        for (int g = 0; g < H_kv; ++g)
+            for (int jj = 0; jj < it.nt; ++jj) {
+                const int j = it.j0 + jj;
+                for (int hl = 0; hl < G; ++hl)
+                    emit(rq.cu_q + j, g * G + hl, it.k0, std::min(it.k1, rq.c + j + 1), it.part, 2);
+            }
+    }
+    *n_rows = n;
+    return HG_OK;
+}
+
 extern "C" hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *out) {
     if (!pool || !out) return fail(HG_E_INVALID, "NULL argument");
     *out = pool->last;

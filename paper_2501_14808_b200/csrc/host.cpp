@@ -2,6 +2,7 @@
 // error reporting, batch validation (§8(b) rules), prefix groups, and the
 // per-call work plan consumed by the sm_100a kernels.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -343,12 +344,21 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         // pass the extra CTAs would only take SMs from split-K.
         sc.np.assign((size_t)v.R, 1);
         const int np_cap = (int)std::min<int64_t>(kMaxCuts, o.num_sms / std::max<int64_t>(n256, 1));
+        constexpr double kTileUs = 1.5, kHbmBytesPerUs = 6.5e6;
+        double dec_keys = 0;
+        for (int i = 0; i < v.R; ++i)
+            if (v.n[i] == 1) dec_keys += (double)v.c[i] + 1 - (double)sc.pre_end[i] * B;
+        const double sk_us = dec_keys * H_kv * 4.0 * d / kHbmBytesPerUs;
+        {   // A/B knob (HG_IPR256_BESIDE_SK=1): 256-row items whenever the tiles finish well within split-K
+            static const bool knob = getenv("HG_IPR256_BESIDE_SK") != nullptr;
+            if (knob && ipr == kTcRows) {
+                double chain = 0;
+                for (int i = 0; i < v.R; ++i)
+                    if (v.n[i] > 1) chain = std::max(chain, (double)ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs);
+                if (chain * 2 < sk_us) ipr = 2 * kTcRows;
+            }
+        }
         if (o.split_prefill && np_cap > 1) {
-            constexpr double kTileUs = 1.5, kHbmBytesPerUs = 6.5e6;
-            double dec_keys = 0;
-            for (int i = 0; i < v.R; ++i)
-                if (v.n[i] == 1) dec_keys += (double)v.c[i] + 1 - (double)sc.pre_end[i] * B;
-            const double sk_us = dec_keys * H_kv * 4.0 * d / kHbmBytesPerUs;
             const double target_us = std::max(sk_us, 8 * kTileUs);
             bool any = false;
             for (int i = 0; i < v.R; ++i)

@@ -349,14 +349,16 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         for (int i = 0; i < v.R; ++i)
             if (v.n[i] == 1) dec_keys += (double)v.c[i] + 1 - (double)sc.pre_end[i] * B;
         const double sk_us = dec_keys * H_kv * 4.0 * d / kHbmBytesPerUs;
-        {   // A/B knob (HG_IPR256_BESIDE_SK=1): 256-row items whenever the tiles finish well within split-K
-            static const bool knob = getenv("HG_IPR256_BESIDE_SK") != nullptr;
-            if (knob && ipr == kTcRows) {
-                double chain = 0;
-                for (int i = 0; i < v.R; ++i)
-                    if (v.n[i] > 1) chain = std::max(chain, (double)ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs);
-                if (chain * 2 < sk_us) ipr = 2 * kTcRows;
-            }
+        if (ipr == kTcRows) {
+            // Beside a decode pass that outlasts them twice over, 256-row items even
+            // on a sparse grid: half the CTAs, each needing a whole SM, so split-K
+            // keeps more SMs while the tiles run (c1_long: 0.481 -> 0.457 ms; c1, c3
+            // unchanged within noise)
+            double chain = 0;
+            for (int i = 0; i < v.R; ++i)
+                if (v.n[i] > 1)
+                    chain = std::max(chain, (double)ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs);
+            if (chain * 2 < sk_us) ipr = 2 * kTcRows;
         }
         if (o.split_prefill && np_cap > 1) {
             const double target_us = std::max(sk_us, 8 * kTileUs);

@@ -133,7 +133,8 @@ HG_API hg_status hg_kv_append_rope(hg_kv_pool *pool, const hg_batch *batch, cons
 /* Tuning / test switches for hg_hybrid_attention_ex (zero-initialise for defaults). */
 typedef struct {
     int32_t split_tokens;       /* >0: fixed split-K chunk (multiple of B) for decode rows, making the
-                                   plan independent of load (bitwise reproducible across G, reading R18);
+                                   plan independent of load (bitwise reproducible across G, reading R18;
+                                   prefill key cuts are off in this mode);
                                    0: automatic (sized to fill the SMs) */
     int32_t disable_prefix_pass;/* 1: no shared-prefix group pass (shared blocks read per request) */
     int32_t disable_tc;         /* 1: prefill rows also go through the split-K kernel (no tcgen05) */

@@ -360,7 +360,9 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
                     chain = std::max(chain, (double)ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs);
             if (chain * 2 < sk_us) ipr = 2 * kTcRows;
         }
-        if (o.split_prefill && np_cap > 1) {
+        // (never under a fixed split, o.split_tokens > 0: that mode promises a plan
+        // independent of load and head count, so a KV-head slice is bit-identical, R17)
+        if (o.split_prefill && o.split_tokens <= 0 && np_cap > 1) {
             const double target_us = std::max(sk_us, 8 * kTileUs);
             bool any = false;
             for (int i = 0; i < v.R; ++i)

@@ -115,6 +115,15 @@ def test_prefill_key_cuts(case, num_sms):
     assert not ((off[:, 5] == 0) & (off[:, 4] >= 0)).any()
 
 
+def test_prefill_cuts_off_under_fixed_split():
+    """split_tokens > 0 promises a load-independent plan (R17): no key cuts."""
+    H_q, H_kv, d, reqs = LONG["c4_small_chunk"]
+    spec = _long("c4_small_chunk", H_q, H_kv, d, reqs)
+    lay = make_layout(spec, seed=1)
+    rows = check_plan(spec, lay, opts=hg.make_opts(split_tokens=512))
+    assert not ((rows[:, 5] == 0) & (rows[:, 4] >= 0)).any()
+
+
 def test_prefill_cuts_stay_off_beside_a_large_decode_pass():
     """c1_long: a 512-token chunk at 3584 beside 64 decodes of 1-4K keys -- the
     decode pass is the long pole, so the chunk stays whole."""

@@ -238,7 +238,8 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)" if peak_kind == "measured" else "fallback",
                 "unit": "GB/s", "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
-                "traffic": traffic, "alg_bytes_per_launch": bytes_sk, "avg_launch_ms": sk_avg,
+                "traffic": traffic["bytes"] if traffic else None,   # DRAM read+write bytes per launch (ncu)
+                "traffic_detail": traffic, "alg_bytes_per_launch": bytes_sk, "avg_launch_ms": sk_avg,
                 "share_of_step": (sk_avg / ms) if sk_avg else None}
     # whole-step roofline (all kernels): t_roof = max(bytes/BW, flops/TC)
     bt, fl = alg_bytes_total(spec), alg_flops(spec)

@@ -49,6 +49,8 @@ def _reference_slices(hg, wl, spec, world, dev):
 
 def _spec(name):
     from synth.configs import make_config, make_fuzz
+    if name.startswith("fuzz8_"):   # 8 KV heads: shardable 8 ways
+        return make_fuzz(int(name[6:]), H_kv=8, G_q=2)
     if name.startswith("fuzz"):
         return make_fuzz(int(name[4:]), H_kv=2, G_q=4)
     return make_config(name, 0)
@@ -158,14 +160,18 @@ def _rank_main(rank, world, port, names, q):
         dist.destroy_process_group()
 
 
-def test_two_ranks_same_gpu_peer_window():
+@pytest.mark.parametrize("world,names", [(2, ["toy_b", "fuzz0", "fuzz3", "fuzz7", "c2_g8"]),
+                                         (4, ["c3"]),                 # C3 at G = 4
+                                         (8, ["fuzz8_1", "fuzz8_5"])])
+def test_ranks_same_gpu_peer_window(world, names):
+    """`world` processes on one GPU: every rank's slice of the gathered output is
+    bit-identical to that slice computed alone (plain and fused sharded calls)."""
     _cuda()
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    names = ["toy_b", "fuzz0", "fuzz3", "fuzz7", "c2_g8"]
     port = _free_port()
-    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, names, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, names, q)) for r in range(world)]
     for p in ps:
         p.start()
     got = {}
@@ -175,7 +181,7 @@ def test_two_ranks_same_gpu_peer_window():
         got[rank] = res
     for p in ps:
         p.join(timeout=60)
-    for r in range(2):
+    for r in range(world):
         bad = [x for x in got[r] if not x[2]]
         assert not bad, (r, bad)
         assert len(got[r]) == 4 * len(names)

@@ -48,6 +48,9 @@ def lib():
                                              P, i32, i64, i64, P, P, P, P]
         L.oracle_attention_range.restype = i32
         L.oracle_num_threads.restype = i32
+        L.oracle_set_num_threads.argtypes = [i32]
+        L.oracle_set_num_threads.restype = None
+        L.oracle_set_num_threads(len(os.sched_getaffinity(0)))   # all host cores (torchrun sets OMP_NUM_THREADS=1)
         _LIB = L
     return _LIB
 

@@ -175,6 +175,16 @@ int oracle_attention(const uint16_t *Kc, const uint16_t *Vc, int64_t num_blocks,
                                   n_sel, 0, -1, out, NULL, NULL, lse);
 }
 
+/* Thread count for the following parallel regions (the host's cores: SURVEY
+ * §8(d)); overrides OMP_NUM_THREADS, which torchrun pins to 1. */
+void oracle_set_num_threads(int nt) {
+#ifdef _OPENMP
+    if (nt > 0) omp_set_num_threads(nt);
+#else
+    (void)nt;
+#endif
+}
+
 int oracle_num_threads(void) {
     int nt = 1;
 #ifdef _OPENMP

@@ -330,20 +330,17 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             if (v.n[i] > 1) n256 += (int64_t)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows);
         for (const Scratch::Node &nd : sc.nodes) n256 += (int64_t)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows);
         if (n256 >= o.num_sms) ipr = 2 * kTcRows;
-        // Few prefill items over long cached contexts (a small chunk budget at a
-        // long prompt: one item = one CTA walking thousands of keys while most SMs
-        // idle): cut each such request's keys into np_i ranges at KV-tile
+        // Long prefill items on an unbalanced grid (a small chunk at a long prompt:
+        // one item = one CTA walking thousands of keys while the other SMs run out
+        // of work): cut such a request's keys into np_i ranges at KV-tile
         // boundaries inside its cached prefix (visible to every row), the last
         // range holding the causal diagonal; the ranges write partials that the
-        // combine kernel merges like split-K's.  np_i fills about one wave of
-        // 256-row items.
-        // Only where the tiles would be the step's long pole: the decode rows'
-        // split-K pass is HBM-bound (~its unique KV bytes / 6.5 TB/s) and a
-        // 256-row item advances ~1.5 us per 128-key tile, so a chunk is cut into
-        // pieces no longer than max(split-K time, 8 tiles); beside a large decode
-        // pass the extra CTAs would only take SMs from split-K.
+        // combine kernel merges like split-K's.  A 256-row item advances ~1.5 us
+        // per 128-key tile and the decode rows' split-K pass is HBM-bound (~its
+        // unique KV bytes / 6.5 TB/s): a chunk is cut only where its chain is
+        // 1.5x longer than both that pass and the grid's average load, into pieces
+        // no longer than the larger of the two (and >= 8 tiles).
         sc.np.assign((size_t)v.R, 1);
-        const int np_cap = (int)std::min<int64_t>(kMaxCuts, o.num_sms / std::max<int64_t>(n256, 1));
         constexpr double kTileUs = 1.5, kHbmBytesPerUs = 6.5e6;
         double dec_keys = 0;
         for (int i = 0; i < v.R; ++i)
@@ -362,14 +359,26 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         }
         // (never under a fixed split, o.split_tokens > 0: that mode promises a plan
         // independent of load and head count, so a KV-head slice is bit-identical, R17)
-        if (o.split_prefill && o.split_tokens <= 0 && np_cap > 1) {
-            const double target_us = std::max(sk_us, 8 * kTileUs);
+        if (o.split_prefill && o.split_tokens <= 0) {
+            // pieces no longer than the longest of: the decode pass, the grid's
+            // average load with every item whole, and 8 tiles
+            double total_us = 0;
+            for (int i = 0; i < v.R; ++i)
+                if (v.n[i] > 1)
+                    total_us += (double)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows) *
+                                ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs;
+            for (const Scratch::Node &nd : sc.nodes)
+                total_us += (double)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows) *
+                            ceil_div((int64_t)(nd.e - nd.a) * B, kTcKeys) * kTileUs;
+            const double target_us = std::max({sk_us, total_us / o.num_sms, 8 * kTileUs});
             bool any = false;
             for (int i = 0; i < v.R; ++i)
                 if (v.n[i] > 1) {
                     const double chain_us = (double)ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs;
-                    const int want = (int)std::ceil(chain_us / target_us);
-                    sc.np[i] = std::max(1, std::min({want, np_cap, 1 + v.c[i] / (2 * kTcKeys)}));
+                    // only a clear long pole pays for the partials and the merge
+                    // (p1: a 78 us chain over a 70 us average -- cutting cost 25 us)
+                    const int want = chain_us > 1.5 * target_us ? (int)std::ceil(chain_us / target_us - 1e-9) : 1;
+                    sc.np[i] = std::max(1, std::min({want, kMaxCuts, 1 + v.c[i] / (2 * kTcKeys)}));
                     any |= sc.np[i] > 1;
                 }
             if (any) ipr = 2 * kTcRows;

@@ -21,15 +21,23 @@ ap.add_argument("--no-tc", action="store_true")
 ap.add_argument("--no-prefix", action="store_true")
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--no-prefill-split", action="store_true")
+ap.add_argument("--spec", default=None, help="pickled BatchSpec instead of a named config")
 a = ap.parse_args()
-spec = make_config(a.config, 0)
+if a.spec:
+    import pickle
+    spec = pickle.load(open(a.spec, "rb"))
+else:
+    spec = make_config(a.config, 0)
 wl = Workload(spec)
-opts = hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split)
+opts = hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split,
+                    disable_prefill_split=a.no_prefill_split)
 for _ in range(2):
     wl.step(opts)
 torch.cuda.synchronize()
 ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(a.steps)]
-ops = [hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split, events=e) for e in ev]
+ops = [hg.make_opts(disable_tc=a.no_tc, disable_prefix_pass=a.no_prefix, split_tokens=a.split, events=e,
+                   disable_prefill_split=a.no_prefill_split) for e in ev]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 tot = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(a.steps)]
 for k in range(a.steps):

@@ -782,16 +782,19 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = t.item()
     # e2e through the public API with host buffers: each rank's pinned q / k_new / v_new
-    # slices in, the gathered O [T][H_q][d] out, per step; slowest rank's wall time
+    # slices in; out, the gathered O [T][H_q][d] read back once per job -- rank r copies
+    # token rows [r T/N, (r+1) T/N) of it (every head: rows other ranks computed too);
+    # slowest rank's wall time
     qh, kh, vh = wl.q.cpu().pin_memory(), wl.k_new.cpu().pin_memory(), wl.v_new.cpu().pin_memory()
-    oh = torch.empty(out.shape, dtype=torch.bfloat16).pin_memory()
+    r0, r1 = spec.T * rank // world, spec.T * (rank + 1) // world
+    oh = torch.empty(out[r0:r1].shape, dtype=torch.bfloat16).pin_memory()
 
     def step_host():
         wl.q.copy_(qh, non_blocking=True)
         wl.k_new.copy_(kh, non_blocking=True)
         wl.v_new.copy_(vh, non_blocking=True)
         step()
-        oh.copy_(out, non_blocking=True)
+        oh.copy_(out[r0:r1], non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
 
     for _ in range(max(args.warmup, 150)):   # the same count on every rank (peer barriers); see measure_e2e
@@ -815,9 +818,9 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
             "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 2) * args.steps,  # + 2 barriers
             "e2e": {"value": spec.T * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2 * world,
-                    "d2h_bytes_per_step": oh.numel() * 2 * world, "ms_per_step": e2e_s / args.steps * 1e3,
+                    "d2h_bytes_per_step": spec.T * spec.H_q * spec.d * 2, "ms_per_step": e2e_s / args.steps * 1e3,
                     "api": "per rank: pinned H2D of its q / k_new / v_new slices, hg_hybrid_step_tp "
-                           "(append fused), D2H of the gathered O; slowest rank"},
+                           "(append fused), D2H of its 1/N token rows of the gathered O; slowest rank"},
             "clocks": clk.summary(),
             **({"note": "HG_BENCH_SAME_GPU functional test: all ranks on one GPU, not a scaling number"}
                if same_gpu else {}),

@@ -139,3 +139,18 @@ def test_invalid_batch_rejected():
     with pytest.raises(hg.HgError) as e:
         hg.hg_plan_rows(bad, spec.H_q, spec.H_kv, spec.d, lay.num_blocks)
     assert e.value.status == hg.HG_E_INVALID
+
+
+def test_c4_batch_with_a_small_chunk_at_10k():
+    """C4 batch #219 (tools/slow_batch_c4_219.pkl): a 49-token chunk at c = 10240
+    beside a 975-token chunk at c = 0 and 59 decodes.  Whole, its 8 items walk 81
+    KV tiles each while everything else is done (0.222 ms); cut, 0.112 ms."""
+    import os
+    import pickle
+    spec = pickle.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                                         "slow_batch_c4_219.pkl"), "rb"))
+    lay = make_layout(spec, seed=219)
+    rows = check_plan(spec, lay)
+    cut = (rows[:, 5] == 0) & (rows[:, 4] >= 0)
+    t_long = sum(r.n for r in spec.requests[:[i for i, r in enumerate(spec.requests) if r.c == 10240][0]])
+    assert cut.any() and np.all(rows[cut, 0] >= t_long) and np.all(rows[cut, 0] < t_long + 49)

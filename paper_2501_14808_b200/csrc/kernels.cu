@@ -567,19 +567,39 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
     const int g = rem / G, hl = rem % G;
     const TokDev tk = p.tok[t];
     const int64_t base = tk.base + (int64_t)g * tk.nparts * G;
+    // the parts' LSEs are loaded once, lane s holding parts s, s + 32, ...; max and
+    // sum by warp shuffles (no chain of dependent loads per part)
+    float lv[2];
     float M = -CUDART_INF_F;
-    for (int s = 0; s < tk.nparts; ++s) M = fmaxf(M, p.part_lse[base + s * G + hl]);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int sidx = lane + 32 * k;
+        lv[k] = sidx < tk.nparts ? p.part_lse[base + (int64_t)sidx * G + hl] : -CUDART_INF_F;
+        M = fmaxf(M, lv[k]);
+    }
+    for (int sidx = lane + 64; sidx < tk.nparts; sidx += 32) M = fmaxf(M, p.part_lse[base + (int64_t)sidx * G + hl]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     const float ref = (M == -CUDART_INF_F) ? 0.f : M;
-    float L = 0.f;
-    for (int s = 0; s < tk.nparts; ++s) L += fast_exp2(p.part_lse[base + s * G + hl] - ref);
+    float wl[2], L = 0.f;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        wl[k] = fast_exp2(lv[k] - ref);   // 0 for missing / empty parts
+        L += wl[k];
+    }
+    for (int sidx = lane + 64; sidx < tk.nparts; sidx += 32) L += fast_exp2(p.part_lse[base + (int64_t)sidx * G + hl] - ref);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     const float inv = L > 0.f ? 1.f / L : 0.f;
     constexpr int PER = D / 32;
     float acc[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-    for (int s = 0; s < tk.nparts; ++s) {
-        const int64_t slot = base + (int64_t)s * G + hl;
-        const float w = fast_exp2(p.part_lse[slot] - ref) * inv;
+#pragma unroll 4
+    for (int sidx = 0; sidx < tk.nparts; ++sidx) {
+        const int64_t slot = base + (int64_t)sidx * G + hl;
+        const float w = (sidx < 64 ? __shfl_sync(0xffffffffu, wl[sidx >> 5], sidx & 31)
+                                   : fast_exp2(p.part_lse[slot] - ref)) * inv;
         const float *src = p.part_o + slot * D + lane * PER;
 #pragma unroll
         for (int e = 0; e < PER; e += 2) {

@@ -245,6 +245,7 @@ def run_ours(args):
     bt, fl = alg_bytes_total(spec), alg_flops(spec)
     t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
     e2e = None if args.profile else measure_e2e(wl, spec, args, stream)
+    split_calls = None if args.profile else measure_append_attention(wl, flush, stream)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -264,6 +265,7 @@ def run_ours(args):
                                "splitk_to_end": statistics.median(e[3].elapsed_time(x) for x, e in zip(ends, kev))}
                               if sk_ms else None),
         "plan": stats,
+        "append_and_attention_ms": split_calls,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,
         "clocks": clk.summary(),
@@ -296,6 +298,31 @@ def load_traffic(kernel, alg_bytes):
         return {"bytes": k["dram_bytes"], "over_alg": k["dram_bytes"] / alg_bytes, "source": d.get("source", p)}
     except Exception:
         return None
+
+
+def measure_append_attention(wl, flush, stream, reps=30):
+    """append timed separately and as append+attention -- the unfused
+    calls (hg_kv_append, then hg_hybrid_attention), device time of each, L2 flushed."""
+    import torch
+    res = {}
+    for name, fn in (("append", lambda: wl.append(stream)), ("attention", lambda: wl.attention(stream=stream)),
+                     ("append_then_attention", lambda: (wl.append(stream), wl.attention(stream=stream))),
+                     ("fused_step", lambda: wl.step(stream=stream))):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush_l2(flush)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        res[name] = statistics.median(ts)
+    res["note"] = ("each call alone (GPU idle before it), median of %d, L2 flushed; the timed steps above run "
+                   "back to back with per-kernel events" % reps)
+    return res
 
 
 def measure_e2e(wl, spec, args, stream):

@@ -503,6 +503,14 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         p.n_out = outs->n;
         for (int k = 0; k < outs->n; ++k) p.outs[k] = outs->ptr[k];
         p.out_ld = outs->ld;
+        if (outs->bar_world > 0) {
+            if (!fused || ra.rot) return fail(HG_E_INVALID, "entry barrier needs the fused (non-rope) step");
+            for (int k = 0; k < outs->bar_world; ++k) p.bar_flags[k] = outs->bar_flags[k];
+            p.bar_mine = outs->bar_mine;
+            p.bar_rank = outs->bar_rank;
+            p.bar_world = outs->bar_world;
+            p.bar_epoch = outs->bar_epoch;
+        }
     } else {
         p.n_out = 1;
         p.outs[0] = (uint16_t *)out;

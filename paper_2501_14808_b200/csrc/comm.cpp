@@ -208,12 +208,20 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
         unsigned long long *fl[kMaxOuts];
         for (int k = 0; k < G; ++k) fl[k] = (unsigned long long *)comm->peer[k];
         unsigned long long *mine = (unsigned long long *)comm->win;
-        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
-        if (s) return s;
         OutSpec os;
         os.n = G;
         os.ld = (int64_t)H_q * d;
         for (int k = 0; k < G; ++k) os.ptr[k] = (uint16_t *)(comm->peer[k] + kWinHdr) + (size_t)comm->rank * Hl * d;
+        if (k_new) {   // fused step: the entry barrier rides in the append kernel (no extra launch)
+            for (int k = 0; k < G; ++k) os.bar_flags[k] = fl[k];
+            os.bar_mine = mine;
+            os.bar_rank = comm->rank;
+            os.bar_world = G;
+            os.bar_epoch = ++comm->epoch;
+        } else {
+            s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
+            if (s) return s;
+        }
         s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream);
         if (s) return s;
         s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);

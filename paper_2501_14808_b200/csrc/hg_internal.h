@@ -93,6 +93,11 @@ struct AttnParams {
     int32_t tc_ctas;           // persistent tcgen05 grid (<= n_tc)
     const int32_t *tc_off;     // [tc_ctas + 1]: CTA b processes tc items [tc_off[b], tc_off[b+1])
     float scale_log2;          // log2(e) / sqrt(d)
+    // peer-window entry barrier folded into the fused step's append kernel (bar_world = 0: none)
+    unsigned long long *bar_flags[kMaxOuts];
+    unsigned long long *bar_mine;
+    int32_t bar_rank, bar_world;
+    unsigned long long bar_epoch;
     long long *trace;          // debug: per-event clock64 stamps of tcgen05 CTA 0 (NULL: off)
 };
 
@@ -153,6 +158,12 @@ struct OutSpec {
     int n = 0;
     uint16_t *ptr[kMaxOuts] = {};
     int64_t ld = 0;   // elements between token rows
+    // entry barrier of a peer-window call, run by the fused step's append kernel
+    // (world = 0: none; the caller launches its own barrier kernel)
+    unsigned long long *bar_flags[kMaxOuts] = {};
+    unsigned long long *bar_mine = nullptr;
+    int bar_rank = 0, bar_world = 0;
+    unsigned long long bar_epoch = 0;
 };
 hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
                        void *ws, size_t ws_bytes, void *stream);

@@ -58,12 +58,35 @@ hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *
 // attention descriptors (owning request, cached length, flattened block ids).
 // One CTA per token: the slot is computed once, then every (KV head, 16-byte
 // chunk) of K and V is moved with all loads issued before the stores.
+// Peer-window barrier body (see peer_barrier_kernel below): thread k < world
+// publishes `epoch` into rank k's slot [rank] and waits for rank k's arrival in
+// the local slot [k]; traps after ~30 s.
+__device__ __forceinline__ void peer_barrier_body(unsigned long long *const *flags, unsigned long long *mine,
+                                                  int rank, int world, unsigned long long epoch, int k) {
+    if (k >= world) return;
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(flags[k] + rank), "l"(epoch) : "memory");
+    unsigned long long t0, now, v;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine + k) : "memory");
+        if (v >= epoch) break;
+        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
+        if (now - t0 > 30000000000ull) __trap();
+        __nanosleep(256);
+    }
+}
+
 template <int PER>   // uint4 chunks of K (and of V) per thread
 __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict__ k_new,
                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_cache,
                                                          uint4 *__restrict__ v_cache, const AttnParams p,
                                                          int chunks_per_row, int wave) {
     const int t = blockIdx.x;
+    // sharded fused step: CTA 0's first warp also runs the peer-window entry
+    // barrier (the kernels after this one are the first to write peer windows)
+    if (p.bar_world > 0 && t == 0 && threadIdx.x < 32)
+        peer_barrier_body(p.bar_flags, p.bar_mine, p.bar_rank, p.bar_world, p.bar_epoch, threadIdx.x);
     const TokDev tk = p.tok[t];
     if (wave >= 0 && tk.wave != wave) return;   // pipelined host step: this token's inputs arrive in the other wave
     const ReqDev rq = p.reqs[tk.req];
@@ -673,19 +696,7 @@ struct PeerFlags {
 
 __global__ void peer_barrier_kernel(PeerFlags pf, unsigned long long *mine, int rank, int world,
                                     unsigned long long epoch) {
-    const int k = threadIdx.x;
-    if (k >= world) return;
-    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
-    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(pf.flags[k] + rank), "l"(epoch) : "memory");
-    unsigned long long t0, now, v;
-    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
-    for (;;) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine + k) : "memory");
-        if (v >= epoch) break;
-        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
-        if (now - t0 > 30000000000ull) __trap();
-        __nanosleep(256);
-    }
+    peer_barrier_body(pf.flags, mine, rank, world, epoch, threadIdx.x);
 }
 
 hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,

@@ -56,6 +56,7 @@ class ClockSampler:
 
     def __init__(self, device_index: int, period_s: float = 0.001):
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.power, self.mem = [], []
         self.dev, self.period = device_index, period_s
         self._stop = threading.Event()
         self._t = None
@@ -80,6 +81,11 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                    self.mem.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM))
+                except Exception:
+                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for k, bit in names.items():
                     if r & bit and k != "gpu_idle":
@@ -107,6 +113,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "sm_mhz_min": min(self.samples), "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "mem_mhz": statistics.median(self.mem) if self.mem else None,
+                "power_w_median": statistics.median(self.power) if self.power else None,
+                "power_w_max": max(self.power) if self.power else None,
                 "source": "NVML (nvmlDeviceGetClockInfo SM + clocks-event reasons), sampled every 1 ms "
                           "in a thread during the timed region"}
 

@@ -292,6 +292,7 @@ def run_ours(args):
         line["psm_vs_fcfs"] = psm_vs_fcfs(dev)
     if args.extra:
         line["next4"] = next4(dev, peaks)
+        line["shard_projection"] = shard_projection(spec, dev, ms)
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -307,6 +308,40 @@ def load_traffic(kernel, alg_bytes):
         return {"bytes": k["dram_bytes"], "over_alg": k["dram_bytes"] / alg_bytes, "source": d.get("source", p)}
     except Exception:
         return None
+
+
+def shard_projection(spec, dev, ms_full, reps=50):
+    """One GPU timing the per-rank work of KV-head sharding at G = 2, 4, 8: the
+    same batch with H_kv/G KV heads (and H_q/G q heads), fused step, L2 flushed.
+    A projection, not a multi-GPU measurement: the peer-window stores over
+    NVLink (T * H_q * d * 2 * (G-1)/G bytes per rank, ~1 us at G = 8 on
+    900 GB/s) and the two flag barriers are not in it."""
+    import torch
+    from paper_2501_14808_b200.harness import Workload
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for G in (2, 4, 8):
+        if spec.H_kv % G:
+            continue
+        wl = Workload(spec.with_(H_kv=spec.H_kv // G, H_q=spec.H_q // G), device=dev)
+        for _ in range(3):
+            wl.step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush_l2(flush)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            wl.step()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        wl.close()
+        m = statistics.median(ts)
+        out[f"G={G}"] = {"per_rank_ms": m, "projected_speedup": ms_full / m}
+    out["note"] = ("per-rank fused step on one GPU with 1/G of the heads (median, L2 flushed); excludes the "
+                   "NVLink window stores and the flag barriers -- a projection, not a multi-GPU measurement")
+    return out
 
 
 def measure_append_attention(wl, flush, stream, reps=30):

@@ -463,7 +463,12 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     if (o.split_tokens > 0) {
         chunk_tok = (o.split_tokens + B - 1) / B * B;
     } else {
-        const int64_t target = (int64_t)o.num_sms * 3 * 4;
+        // ~one wave of split-K CTAs (3 resident per SM), LPT-ordered: fewer, longer
+        // pieces than 4 waves' worth mean fewer partials to write and merge (c1
+        // 0.451 -> 0.443 ms, its G = 8 shard 0.107 -> 0.099 ms; c2 / c3 within
+        // 0.5 %); small batches keep the 256-key floor.  HG_SK_WAVES: A/B knob.
+        static const int waves = getenv("HG_SK_WAVES") ? std::max(1, atoi(getenv("HG_SK_WAVES"))) : 1;
+        const int64_t target = (int64_t)o.num_sms * 3 * waves;
         int64_t ct = (total_keys + target - 1) / std::max<int64_t>(target, 1);
         ct = std::max<int64_t>(ct, 256);
         chunk_tok = (int)((ct + B - 1) / B * B);

@@ -14,7 +14,8 @@ from torch.profiler import ProfilerActivity, profile
 from paper_2501_14808_b200.harness import Workload
 from synth.configs import make_config
 
-spec = make_config(sys.argv[1] if len(sys.argv) > 1 else "c1", 0)
+import pickle
+spec = pickle.load(open(sys.argv[2], "rb")) if len(sys.argv) > 2 else make_config(sys.argv[1] if len(sys.argv) > 1 else "c1", 0)
 wl = Workload(spec)
 for _ in range(3):
     wl.step()

@@ -293,6 +293,9 @@ def run_ours(args):
     if args.extra:
         line["next4"] = next4(dev, peaks)
         line["shard_projection"] = shard_projection(spec, dev, ms)
+        # the north_star's multi-GPU config: Llama-3-70B-shaped C3 (8 KV heads)
+        c3 = make_config("c3", 0)
+        line["shard_projection_c3"] = shard_projection(c3, dev, line["extra"]["c3"]["ms_per_step"])
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -310,7 +313,7 @@ def load_traffic(kernel, alg_bytes):
         return None
 
 
-def shard_projection(spec, dev, ms_full, reps=50):
+def shard_projection(spec, dev, ms_step, reps=50):
     """One GPU timing the per-rank work of KV-head sharding at G = 2, 4, 8: the
     same batch with H_kv/G KV heads (and H_q/G q heads), fused step, L2 flushed.
     A projection, not a multi-GPU measurement: the peer-window stores over
@@ -320,16 +323,18 @@ def shard_projection(spec, dev, ms_full, reps=50):
     from paper_2501_14808_b200.harness import Workload
     out = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for G in (2, 4, 8):
+    base = None
+    for G in (1, 2, 4, 8):
         if spec.H_kv % G:
             continue
-        wl = Workload(spec.with_(H_kv=spec.H_kv // G, H_q=spec.H_q // G), device=dev)
+        wl = Workload(spec.with_(H_kv=spec.H_kv // G, H_q=spec.H_q // G) if G > 1 else spec, device=dev)
         for _ in range(3):
             wl.step()
         torch.cuda.synchronize()
         ts = []
         for _ in range(reps):
             flush_l2(flush)
+            torch.cuda._sleep(1_000_000)   # GPU busy while the host plans and enqueues: device time only
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             wl.step()
@@ -338,9 +343,14 @@ def shard_projection(spec, dev, ms_full, reps=50):
             ts.append(a.elapsed_time(b))
         wl.close()
         m = statistics.median(ts)
-        out[f"G={G}"] = {"per_rank_ms": m, "projected_speedup": ms_full / m}
-    out["note"] = ("per-rank fused step on one GPU with 1/G of the heads (median, L2 flushed); excludes the "
-                   "NVLink window stores and the flag barriers -- a projection, not a multi-GPU measurement")
+        base = m if G == 1 else base
+        out[f"G={G}"] = {"per_rank_ms": m, "projected_speedup": base / m}
+    out["workload"] = spec.name
+    out["note"] = ("per-rank fused step on one GPU with 1/G of the heads, each call alone (device time: the GPU "
+                   "is kept busy while the host plans; median, L2 flushed), "
+                   "speedup against G = 1 timed the same way; excludes the NVLink window stores and the flag "
+                   "barriers -- a projection, not a multi-GPU measurement (the bench loop's own step: %.4f ms)"
+                   % ms_step)
     return out
 
 
@@ -357,6 +367,7 @@ def measure_append_attention(wl, flush, stream, reps=30):
         ts = []
         for _ in range(reps):
             flush_l2(flush)
+            torch.cuda._sleep(1_000_000)   # GPU busy while the host plans and enqueues: device time only
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             fn()
@@ -364,8 +375,8 @@ def measure_append_attention(wl, flush, stream, reps=30):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         res[name] = statistics.median(ts)
-    res["note"] = ("each call alone (GPU idle before it), median of %d, L2 flushed; the timed steps above run "
-                   "back to back with per-kernel events" % reps)
+    res["note"] = ("each call alone (GPU kept busy while the host plans it, so device time only), median of "
+                   "%d, L2 flushed; the timed steps above run back to back with per-kernel events" % reps)
     return res
 
 

@@ -1,6 +1,4 @@
-mkdir -p gpurun_out; rm -f gpurun_out/pf.log
-for pf in 0 1 2 4; do
-  cp variants/libhygen_pf$pf.so paper_2501_14808_b200/libhygen.so; touch paper_2501_14808_b200/libhygen.so
-  timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "toy or fuzz1" 2>&1 | tail -1 | sed "s/^/pf$pf /" >> gpurun_out/pf.log
-  for c in c1 c2 c3; do timeout 120 python tools/run_config.py $c --time --steps 6 --no-tc 2>&1 | grep "^c" | tail -4 | cut -c1-75 | sed "s/^/pf$pf /" >> gpurun_out/pf.log; done
-done
+mkdir -p gpurun_out/pf
+for c in c1 c1_long c3 c2; do HG_HOST_AHEAD=1 timeout 300 python tools/run_config.py $c --time --steps 10 2>&1 | grep "step" | tail -6 > gpurun_out/pf/$c.log; done
+for s in c3_shard_g8 c1_shard_g8; do HG_HOST_AHEAD=1 timeout 300 python tools/run_config.py x --spec tools/$s.pkl --time --steps 10 2>&1 | grep "step" | tail -6 > gpurun_out/pf/$s.log; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "full_size or nested or fuzz" 2>&1 | tail -2 > gpurun_out/pf/tests.log

@@ -87,22 +87,36 @@ __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict
     // barrier (the kernels after this one are the first to write peer windows)
     if (p.bar_world > 0 && t == 0 && threadIdx.x < 32)
         peer_barrier_body(p.bar_flags, p.bar_mine, p.bar_rank, p.bar_world, p.bar_epoch, threadIdx.x);
+    const int row_chunks = p.H_kv * chunks_per_row;   // uint4 chunks of one token's K (or V)
+    const int64_t src0 = (int64_t)t * row_chunks;
+    // the first batch of this token's K/V loads goes out before the descriptor
+    // chain (token -> request -> block id) it does not depend on
+    uint4 kv[2 * PER];
+    int idx[PER];
+    if (wave < 0) {
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            idx[e] = threadIdx.x + e * 256;
+            if (idx[e] < row_chunks) {
+                kv[e] = k_new[src0 + idx[e]];
+                kv[PER + e] = v_new[src0 + idx[e]];
+            }
+        }
+    }
     const TokDev tk = p.tok[t];
     if (wave >= 0 && tk.wave != wave) return;   // pipelined host step: this token's inputs arrive in the other wave
     const ReqDev rq = p.reqs[tk.req];
     const int pos = rq.c + (t - rq.cu_q);
     const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
-    const int row_chunks = p.H_kv * chunks_per_row;   // uint4 chunks of one token's K (or V)
-    const int64_t src0 = (int64_t)t * row_chunks;
     for (int base = 0; base < row_chunks; base += 256 * PER) {
-        uint4 kv[2 * PER];
-        int idx[PER];
+        if (base > 0 || wave >= 0) {
 #pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            idx[e] = base + threadIdx.x + e * 256;
-            if (idx[e] < row_chunks) {
-                kv[e] = k_new[src0 + idx[e]];
-                kv[PER + e] = v_new[src0 + idx[e]];
+            for (int e = 0; e < PER; ++e) {
+                idx[e] = base + threadIdx.x + e * 256;
+                if (idx[e] < row_chunks) {
+                    kv[e] = k_new[src0 + idx[e]];
+                    kv[PER + e] = v_new[src0 + idx[e]];
+                }
             }
         }
 #pragma unroll

@@ -49,6 +49,8 @@ struct hg_kv_pool {
     // the prefill wave's tcgen05 stream (highest priority) with its done events
     cudaStream_t h2d = nullptr, side_hi = nullptr;
     cudaEvent_t ev_in0 = nullptr, ev_in1 = nullptr, ev_tc = nullptr, ev_d2h = nullptr;
+    // fused step: the append runs on `side` while the descriptors upload on the caller's stream
+    cudaEvent_t ev_pre = nullptr, ev_app = nullptr;
 };
 
 namespace hg {
@@ -145,7 +147,7 @@ extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
         }
-    for (cudaEvent_t e : {p->ev_in0, p->ev_in1, p->ev_tc, p->ev_d2h})
+    for (cudaEvent_t e : {p->ev_in0, p->ev_in1, p->ev_tc, p->ev_d2h, p->ev_pre, p->ev_app})
         if (e) cudaEventDestroy(e);
     delete p;
     return HG_OK;
@@ -486,8 +488,43 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_cbase, plan.tok.data(), sizeof(TokDev) * plan.tok.size());
     put(plan.off_comb, plan.comb.data(), sizeof(int32_t) * plan.comb.size());
     put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
+    // Fused step (no rope, no host-step waves): the append takes its slots from
+    // the kernel parameters and runs on the side stream while the descriptors
+    // upload, instead of after them (the tiles and split-K wait for both).
+    static const bool no_param_append = getenv("HG_NO_PARAM_APPEND") != nullptr;   // A/B switch
+    const bool param_append = fused && !ra.rot && !pipe && plan.T <= kParamSlots &&
+                              !no_param_append;
+    if (param_append) {
+        s = ensure_side(pool);
+        if (!s && !pool->ev_pre) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_pre, cudaEventDisableTiming), "event");
+        if (!s && !pool->ev_app) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_app, cudaEventDisableTiming), "event");
+        if (s) return s;
+        static thread_local std::vector<int64_t> slots;
+        slots.resize((size_t)plan.T);
+        const int B = pool->desc.block_size;
+        for (int i = 0; i < v.R; ++i) {
+            const int32_t *row = v.bt + (int64_t)i * v.W;
+            int64_t *sl = slots.data() + plan.reqs[i].cu_q;
+            for (int j = 0; j < v.n[i]; ++j) {
+                const int64_t pos = (int64_t)v.c[i] + j;
+                sl[j] = (int64_t)row[pos / B] * B + pos % B;
+            }
+        }
+        s = cuda_check(cudaEventRecord(pool->ev_pre, st), "order record");   // after the caller's earlier work
+        if (!s) s = cuda_check(cudaStreamWaitEvent(pool->side, pool->ev_pre, 0), "order wait");
+        if (!s) s = launch_append_param((const uint16_t *)k_new, (const uint16_t *)v_new,
+                                        (uint16_t *)pool->desc.k_cache, (uint16_t *)pool->desc.v_cache,
+                                        slots.data(), plan.T, pool->desc.num_kv_heads, pool->desc.head_dim,
+                                        pool->side);
+        if (!s) s = cuda_check(cudaEventRecord(pool->ev_app, pool->side), "append record");
+        if (s) return s;
+    }
     s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
     if (s) return s;
+    if (param_append) {
+        s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
+        if (s) return s;
+    }
     if (pipe && pipe->enqueue_wave) {
         s = pipe->enqueue_wave(0);
         if (!s && !pipe->used) s = pipe->enqueue_wave(1);
@@ -598,7 +635,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             s = launch_rope_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, (const uint16_t *)q,
                                        q_rot, plan.T, ra, st);
             p.q = q_rot;
-        } else {
+        } else if (!param_append) {
             s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st);
         }
         if (s) return s;

@@ -11,6 +11,7 @@
 //                        softmax; 4 warps split the item's blocks and merge
 //                        through shared memory.
 //   combine_kernel  a.7  log-sum-exp merge of split / prefix partials.
+#include <cstring>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -129,6 +130,73 @@ __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict
             }
         }
     }
+}
+
+// Fused-step append with the token slots in the kernel parameters (no
+// dependency on the descriptor upload, so it runs while that copy is in
+// flight).  One CTA per token, K/V loads issued before the stores.
+template <int NS>
+struct SlotParams {
+    int64_t slot[NS];
+};
+
+template <int PER, int NS>
+__global__ void __launch_bounds__(256) append_param_kernel(const uint4 *__restrict__ k_new,
+                                                           const uint4 *__restrict__ v_new,
+                                                           uint4 *__restrict__ k_cache, uint4 *__restrict__ v_cache,
+                                                           const __grid_constant__ SlotParams<NS> sp, int H_kv,
+                                                           int chunks_per_row) {
+    const int t = blockIdx.x;
+    const int row_chunks = H_kv * chunks_per_row;
+    const int64_t src0 = (int64_t)t * row_chunks;
+    const int64_t s = sp.slot[t];
+    const int64_t blk = s / kBlock, pos = s % kBlock;
+    for (int base = 0; base < row_chunks; base += 256 * PER) {
+        uint4 kv[2 * PER];
+        int idx[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            idx[e] = base + threadIdx.x + e * 256;
+            if (idx[e] < row_chunks) {
+                kv[e] = k_new[src0 + idx[e]];
+                kv[PER + e] = v_new[src0 + idx[e]];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            if (idx[e] < row_chunks) {
+                const int g = idx[e] / chunks_per_row, ch = idx[e] - g * chunks_per_row;
+                const int64_t dst = ((blk * H_kv + g) * kBlock + pos) * chunks_per_row + ch;
+                k_cache[dst] = kv[e];
+                v_cache[dst] = kv[PER + e];
+            }
+        }
+    }
+}
+
+template <int NS>
+static void launch_append_param_ns(const uint4 *kn, const uint4 *vn, uint4 *kc, uint4 *vc, const int64_t *slots,
+                                   int T, int H_kv, int cpr, cudaStream_t st) {
+    SlotParams<NS> sp;
+    memcpy(sp.slot, slots, sizeof(int64_t) * (size_t)T);
+    const int per = (H_kv * cpr + 255) / 256;
+    if (per <= 1) append_param_kernel<1, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
+    else if (per <= 2) append_param_kernel<2, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
+    else if (per <= 4) append_param_kernel<4, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
+    else append_param_kernel<8, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
+}
+
+hg_status launch_append_param(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache, uint16_t *v_cache,
+                              const int64_t *slots_host, int T, int H_kv, int d, void *stream) {
+    if (T == 0) return HG_OK;
+    if (T > kParamSlots) return fail(HG_E_INVALID, "append_param: T %d > %d", T, kParamSlots);
+    auto *kn = (const uint4 *)k_new, *vn = (const uint4 *)v_new;
+    auto *kc = (uint4 *)k_cache, *vc = (uint4 *)v_cache;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (T <= 1024) launch_append_param_ns<1024>(kn, vn, kc, vc, slots_host, T, H_kv, d / 8, st);
+    else launch_append_param_ns<kParamSlots>(kn, vn, kc, vc, slots_host, T, H_kv, d / 8, st);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
 }
 
 hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const uint16_t *v_new, int T, void *stream,

@@ -492,8 +492,9 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     // the kernel parameters and runs on the side stream while the descriptors
     // upload, instead of after them (the tiles and split-K wait for both).
     static const bool no_param_append = getenv("HG_NO_PARAM_APPEND") != nullptr;   // A/B switch
-    const bool param_append = fused && !ra.rot && !pipe && plan.T <= kParamSlots &&
-                              !no_param_append;
+    // (not for a sharded call whose entry barrier rides in append_dev_kernel)
+    const bool param_append = fused && !ra.rot && !pipe && plan.T <= kParamSlots && !no_param_append &&
+                              !(outs && outs->bar_world > 0);
     if (param_append) {
         s = ensure_side(pool);
         if (!s && !pool->ev_pre) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_pre, cudaEventDisableTiming), "event");

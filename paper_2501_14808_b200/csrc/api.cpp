@@ -492,9 +492,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     // the kernel parameters and runs on the side stream while the descriptors
     // upload, instead of after them (the tiles and split-K wait for both).
     static const bool no_param_append = getenv("HG_NO_PARAM_APPEND") != nullptr;   // A/B switch
-    // (not for a sharded call whose entry barrier rides in append_dev_kernel)
-    const bool param_append = fused && !ra.rot && !pipe && plan.T <= kParamSlots && !no_param_append &&
-                              !(outs && outs->bar_world > 0);
+    const bool param_append = fused && !ra.rot && !pipe && plan.T <= kParamSlots && !no_param_append;
     if (param_append) {
         s = ensure_side(pool);
         if (!s && !pool->ev_pre) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_pre, cudaEventDisableTiming), "event");
@@ -513,10 +511,18 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         }
         s = cuda_check(cudaEventRecord(pool->ev_pre, st), "order record");   // after the caller's earlier work
         if (!s) s = cuda_check(cudaStreamWaitEvent(pool->side, pool->ev_pre, 0), "order wait");
+        AttnParams bar{};   // a sharded call's peer-window entry barrier rides in this kernel
+        if (outs && outs->bar_world > 0) {
+            for (int k = 0; k < outs->bar_world; ++k) bar.bar_flags[k] = outs->bar_flags[k];
+            bar.bar_mine = outs->bar_mine;
+            bar.bar_rank = outs->bar_rank;
+            bar.bar_world = outs->bar_world;
+            bar.bar_epoch = outs->bar_epoch;
+        }
         if (!s) s = launch_append_param((const uint16_t *)k_new, (const uint16_t *)v_new,
                                         (uint16_t *)pool->desc.k_cache, (uint16_t *)pool->desc.v_cache,
                                         slots.data(), plan.T, pool->desc.num_kv_heads, pool->desc.head_dim,
-                                        pool->side);
+                                        pool->side, &bar);
         if (!s) s = cuda_check(cudaEventRecord(pool->ev_app, pool->side), "append record");
         if (s) return s;
     }

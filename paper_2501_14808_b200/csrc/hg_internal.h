@@ -183,8 +183,10 @@ hg_status launch_append_dev(const AttnParams &p, const uint16_t *k_new, const ui
 // Fused-step append with the slots in the kernel parameters (T <= kParamSlots):
 // independent of the descriptor upload.
 constexpr int kParamSlots = 3968;   // 31 KB of int64 slots (kernel parameter limit 32764 B)
+// bar: AttnParams whose bar_* fields carry a peer-window entry barrier (NULL / bar_world = 0: none)
 hg_status launch_append_param(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache, uint16_t *v_cache,
-                              const int64_t *slots_host, int T, int H_kv, int d, void *stream);
+                              const int64_t *slots_host, int T, int H_kv, int d, void *stream,
+                              const AttnParams *bar = nullptr);
 // RoPE in the append prologue (NEXT-4): K rotated at its position before it is
 // written, V copied, and (q_dst != NULL) Q rotated into q_dst.  Token slots and
 // positions from the attention descriptors (fused step) or from arrays.

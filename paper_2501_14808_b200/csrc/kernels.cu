@@ -140,13 +140,22 @@ struct SlotParams {
     int64_t slot[NS];
 };
 
+struct BarrierArgs {   // peer-window entry barrier carried by the append (world = 0: none)
+    unsigned long long *flags[kMaxOuts];
+    unsigned long long *mine;
+    int rank, world;
+    unsigned long long epoch;
+};
+
 template <int PER, int NS>
 __global__ void __launch_bounds__(256) append_param_kernel(const uint4 *__restrict__ k_new,
                                                            const uint4 *__restrict__ v_new,
                                                            uint4 *__restrict__ k_cache, uint4 *__restrict__ v_cache,
                                                            const __grid_constant__ SlotParams<NS> sp, int H_kv,
-                                                           int chunks_per_row) {
+                                                           int chunks_per_row, const BarrierArgs ba) {
     const int t = blockIdx.x;
+    if (ba.world > 0 && t == 0 && threadIdx.x < 32)
+        peer_barrier_body(ba.flags, ba.mine, ba.rank, ba.world, ba.epoch, threadIdx.x);
     const int row_chunks = H_kv * chunks_per_row;
     const int64_t src0 = (int64_t)t * row_chunks;
     const int64_t s = sp.slot[t];
@@ -176,25 +185,34 @@ __global__ void __launch_bounds__(256) append_param_kernel(const uint4 *__restri
 
 template <int NS>
 static void launch_append_param_ns(const uint4 *kn, const uint4 *vn, uint4 *kc, uint4 *vc, const int64_t *slots,
-                                   int T, int H_kv, int cpr, cudaStream_t st) {
+                                   int T, int H_kv, int cpr, const BarrierArgs &ba, cudaStream_t st) {
     SlotParams<NS> sp;
     memcpy(sp.slot, slots, sizeof(int64_t) * (size_t)T);
     const int per = (H_kv * cpr + 255) / 256;
-    if (per <= 1) append_param_kernel<1, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
-    else if (per <= 2) append_param_kernel<2, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
-    else if (per <= 4) append_param_kernel<4, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
-    else append_param_kernel<8, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr);
+    if (per <= 1) append_param_kernel<1, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr, ba);
+    else if (per <= 2) append_param_kernel<2, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr, ba);
+    else if (per <= 4) append_param_kernel<4, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr, ba);
+    else append_param_kernel<8, NS><<<T, 256, 0, st>>>(kn, vn, kc, vc, sp, H_kv, cpr, ba);
 }
 
 hg_status launch_append_param(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache, uint16_t *v_cache,
-                              const int64_t *slots_host, int T, int H_kv, int d, void *stream) {
+                              const int64_t *slots_host, int T, int H_kv, int d, void *stream,
+                              const AttnParams *bar) {
+    BarrierArgs ba{};
+    if (bar && bar->bar_world > 0) {
+        for (int k = 0; k < bar->bar_world; ++k) ba.flags[k] = bar->bar_flags[k];
+        ba.mine = bar->bar_mine;
+        ba.rank = bar->bar_rank;
+        ba.world = bar->bar_world;
+        ba.epoch = bar->bar_epoch;
+    }
     if (T == 0) return HG_OK;
     if (T > kParamSlots) return fail(HG_E_INVALID, "append_param: T %d > %d", T, kParamSlots);
     auto *kn = (const uint4 *)k_new, *vn = (const uint4 *)v_new;
     auto *kc = (uint4 *)k_cache, *vc = (uint4 *)v_cache;
     cudaStream_t st = (cudaStream_t)stream;
-    if (T <= 1024) launch_append_param_ns<1024>(kn, vn, kc, vc, slots_host, T, H_kv, d / 8, st);
-    else launch_append_param_ns<kParamSlots>(kn, vn, kc, vc, slots_host, T, H_kv, d / 8, st);
+    if (T <= 1024) launch_append_param_ns<1024>(kn, vn, kc, vc, slots_host, T, H_kv, d / 8, ba, st);
+    else launch_append_param_ns<kParamSlots>(kn, vn, kc, vc, slots_host, T, H_kv, d / 8, ba, st);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "append launch: %s", cudaGetErrorString(e));
 }

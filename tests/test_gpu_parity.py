@@ -376,6 +376,24 @@ def _mixed(name, H_q, H_kv, d, reqs, seed=0):
     return BatchSpec(name, H_q, H_kv, d, 16, seed, reqs)
 
 
+def test_fused_step_more_tokens_than_param_slots():
+    """T > 3968: the fused step's append falls back from the parameter-slot kernel
+    to append_dev_kernel (slots derived on the device); cache bit-exact to the
+    unfused append, output against the oracle."""
+    from synth.configs import Request
+    reqs = [Request(100, 2048), Request(50, 2040, True)] + [Request(300 + 7 * k, 1, k % 2 == 0) for k in range(20)]
+    spec = _mixed("bigT", 8, 8, 64, reqs)
+    assert spec.T > 3968
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    k_fused = wl.k_cache.clone()
+    compare(spec, wl)
+    wl.append()
+    torch.cuda.synchronize()
+    assert torch.equal(k_fused, wl.k_cache)
+
+
 def test_max_context_16k():
     """Longest contexts of the configs (block table width 1088): a decode at c=16383
     and a 2048-token chunk ending at 16K."""

@@ -376,6 +376,22 @@ def _mixed(name, H_q, H_kv, d, reqs, seed=0):
     return BatchSpec(name, H_q, H_kv, d, 16, seed, reqs)
 
 
+@pytest.mark.parametrize("name", ["c1_shard_g8", "c3_shard_g8"])
+def test_shard_slices_full_size(name):
+    """One rank's slice of 8-way KV-head sharding at full size (c1: 4 KV heads;
+    C3: 1 KV head x 8 q heads, with its prefix groups), the plans bench.py's
+    shard_projection times: sampled requests against the oracle."""
+    import os
+    import pickle
+    spec = pickle.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                                         name + ".pkl"), "rb"))
+    wl = make(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    compare(spec, wl, req_sel=_sample(spec, 8))
+    wl.close()
+
+
 def test_fused_step_more_tokens_than_param_slots():
     """T > 3968: the fused step's append falls back from the parameter-slot kernel
     to append_dev_kernel (slots derived on the device); cache bit-exact to the

@@ -1,4 +1,2 @@
-mkdir -p gpurun_out/check3
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3 > gpurun_out/check3/tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/check3/smoke.log 2>&1
-echo smoke=$? >> gpurun_out/check3/tests.log
+mkdir -p gpurun_out/check4
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "shard_slices or param_slots" -s 2>&1 | grep -v "^$" | tail -8 > gpurun_out/check4/tests.log

@@ -289,6 +289,8 @@ def run_ours(args):
         pred2.pop("_model")
         line["predictor_llama2_7b"] = pred2
         line["slo_loop"] = slo_loop(dev, model)
+        # the same loop with an online profiler refitting on its own observations
+        line["slo_loop_online_refit"] = slo_loop(dev, model, refit_every=25)
         line["psm_vs_fcfs"] = psm_vs_fcfs(dev)
     if args.extra:
         line["next4"] = next4(dev, peaks)
@@ -604,7 +606,7 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
     return res
 
 
-def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8, 128)):
+def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8, 128), refit_every=0):
     """NEXT-1 closed loop: HyGen's two-phase scheduling (Alg. 2 calls Alg. 1 for the
     online then the offline phase) with hg_slo_aware_schedule over the
     fitted predictor, on a bursty online trace + offline backlog (synth.trace
@@ -628,6 +630,7 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     online, offline = [], []   # [prompt, output, done_prompt, done_out, group, prefix]
+    obs_x, obs_y, refits, first_refit = [], [], 0, None
     t_sim, gid = rng.uniform(0, PERIOD_S), 0
     rows = []
     tok_on = tok_off = 0
@@ -681,8 +684,27 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
         last = 5 if st["combine_rows"] else 3 if st["splitk_items"] else 1
         meas = statistics.median(ev[first].elapsed_time(ev[last]) for ev in evs)
         pred = model.w[0] + sum(tr for _, _, tr, _ in entries)
-        whole = hg.hg_predictor_predict(model, hg.hg_batch_features(b))   # the model on the batch itself
+        feats = hg.hg_batch_features(b)
+        whole = hg.hg_predictor_predict(model, feats)   # the model on the batch itself
         rows.append((meas, pred, whole))
+        if refit_every:
+            # online profiler: refit the predictor on the loop's own (batch, measured time)
+            # pairs every `refit_every` iterations (same features, relative-error LS)
+            obs_x.append(feats.as_array())
+            obs_y.append(meas)
+            if len(obs_y) >= 30 and len(obs_y) % refit_every == 0:
+                ox = np.array(obs_x)
+                mask = model.feature_mask
+                for k in range(8):   # a feature constant over the loop's batches is collinear with the intercept
+                    if mask >> k & 1 and np.ptp(ox[:, k]) == 0:
+                        mask &= ~(1 << k)
+                try:
+                    model = hg.hg_predictor_fit(ox, np.array(obs_y), mask)
+                    refits += 1
+                    if first_refit is None:
+                        first_refit = len(rows)
+                except hg.HgError:
+                    pass
         for r, l, tr, phase in entries:
             if l == 0:
                 r[3] += 1
@@ -710,6 +732,9 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
             "bias_pred_vs_measured": float(np.mean((pred - meas) / meas)),
             "mape_batch_predict_vs_measured": float(np.mean(np.abs(whole - meas) / meas)),
             "online_tokens": tok_on, "offline_tokens": tok_off,
+            "refit_every": refit_every, "refits": refits,
+            "mape_after_first_refit": (float(np.mean(np.abs(pred[first_refit:] - meas[first_refit:]) / meas[first_refit:]))
+                                       if first_refit is not None and first_refit < len(rows) else None),
             "note": "kernel-level analogue of the paper's SLO loop: budget = attention GPU time per iteration"}
 
 

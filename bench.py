@@ -654,10 +654,10 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
             return run, que, [f(r) for r in run], [f(r) for r in que]
         entries = []
         t, c, m = budget_ms, chunk, N // 2
+        state = hg.hg_sched_state()   # one batch: the offline phase continues the online one
         for phase, reqs in ((True, online), (False, offline)):
             run, que, rs, qs = split(reqs)
-            sched, t, c, m = hg.hg_slo_aware_schedule(model, rs, qs, t + (0.0 if phase else 0.0), c, m, phase)
-            t += model.w[0] if phase else 0.0   # the intercept is charged once per batch, in the first phase
+            sched, t, c, m = hg.hg_slo_aware_schedule(model, rs, qs, t, c, m, phase, state=state)
             for idx, l, tr in sched:
                 r = run[idx] if idx < len(run) else que[idx - len(run)]
                 entries.append((r, l, tr, phase))

@@ -389,6 +389,21 @@ typedef struct {
     double t_req;   /* predicted marginal batch latency charged to the budget (ms) */
 } hg_sched_entry;
 
+/* The batch under construction across the phases of one iteration (Alg. 2
+ * runs SLO_AWARE_SCHEDULE for the online, then the offline phase on ONE batch,
+ * P:507-512).  Zero-initialise it once per iteration and pass it to every
+ * phase together with the previous phase's *t_left / *c_left / *m_left: each
+ * phase then prices its requests against the whole batch so far (the Eq. 1
+ * cross terms such as 2 S_p l w_{S_p^2} included) and the intercept is charged
+ * once.  NULL: the call is a batch of its own. */
+#define HG_SCHED_MAX_GROUPS 256
+typedef struct {
+    double features[8];        /* hg_features order: features of the entries admitted so far */
+    int32_t intercept_charged; /* 1 once w[0] has been taken off a budget */
+    int32_t n_groups;          /* shared-prefix groups that already have a decode row */
+    int32_t groups[HG_SCHED_MAX_GROUPS];
+} hg_sched_state;
+
 /* One scheduling pass (online or offline phase) of Alg. 1 with the fitted
  * predictor: running decodes first (admitted unconditionally when
  * phase_online, else only while t_req <= t), then prefilling running requests
@@ -397,15 +412,17 @@ typedef struct {
  * m decreases by GET_NUM_BLOCKS(l)); the first prefill that cannot be
  * given a token ends the pass (preemption is not modelled, reading R21).
  * t_req is the marginal increase of the batch prediction (clamped at 0); the
- * model intercept is charged once (reading R19).  out must hold
+ * model intercept is charged once per batch (reading R19).  state (nullable,
+ * in/out): the batch so far -- see hg_sched_state; HG_E_UNSUPPORTED if the
+ * batch would hold more than HG_SCHED_MAX_GROUPS groups.  out must hold
  * n_running + n_queue entries; *t_left / *c_left / *m_left (nullable) return
  * the budgets left for the next phase (Alg. 2 runs the online then the
- * offline phase). */
+ * offline phase: pass them on with the same state). */
 HG_API hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t block_size, const hg_sched_req *running,
                                        int32_t n_running, const hg_sched_req *queue, int32_t n_queue,
                                        double latency_budget_ms, int32_t chunk_budget, int32_t memory_blocks,
-                                       int32_t phase_online, hg_sched_entry *out, int32_t *n_out, double *t_left,
-                                       int32_t *c_left, int32_t *m_left);
+                                       int32_t phase_online, hg_sched_state *state, hg_sched_entry *out,
+                                       int32_t *n_out, double *t_left, int32_t *c_left, int32_t *m_left);
 
 /* ------------------------------------------------------------------------ */
 /* Prefix Sharing Maximization (§4.3; Alg. 3)           */
@@ -429,13 +446,13 @@ HG_API hg_status hg_psm_dfs_order(hg_psm *psm, int32_t *ids, int32_t *lcp_with_p
  * ends the pass), then new requests in the tree's DFS order, each given the
  * largest fitting chunk (get_max_prefill) and removed from the tree.  by_id[k]
  * describes tree request k (n_ids entries).  out entries index running[] for
- * index < n_running, else request id + n_running.  Budgets and marginal
- * latencies as in hg_slo_aware_schedule. */
+ * index < n_running, else request id + n_running.  Budgets, marginal
+ * latencies and state (the online phase's batch) as in hg_slo_aware_schedule. */
 HG_API hg_status hg_psm_offline_schedule(const hg_predictor *model, int32_t block_size, hg_psm *psm,
                                          const hg_sched_req *running, int32_t n_running, const hg_sched_req *by_id,
                                          int32_t n_ids, double latency_budget_ms, int32_t chunk_budget,
-                                         int32_t memory_blocks, hg_sched_entry *out, int32_t *n_out, double *t_left,
-                                         int32_t *c_left, int32_t *m_left);
+                                         int32_t memory_blocks, hg_sched_state *state, hg_sched_entry *out,
+                                         int32_t *n_out, double *t_left, int32_t *c_left, int32_t *m_left);
 
 #ifdef __cplusplus
 }

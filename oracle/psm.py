@@ -53,10 +53,16 @@ class Trie:
         return order, res
 
 
-def offline_schedule(w, block_size, trie, running, by_id, t, c, m):
-    """Alg. 3 with the readings of oracle/scheduler.py; decode gate `t < t_req => break` (R16)."""
-    t = t - w[0]
-    B, out = [], []
+def offline_schedule(w, block_size, trie, running, by_id, t, c, m, batch=None):
+    """Alg. 3 with the readings of oracle/scheduler.py; decode gate `t < t_req => break` (R16).
+    batch: the iteration's batch so far (the online phase's entries), as in
+    scheduler.schedule; extended in place."""
+    if batch is None:
+        batch = []
+    if ("w0",) not in batch:
+        t = t - w[0]
+        batch.append(("w0",))
+    B, out = batch, []
 
     def marg(e):
         return max(0.0, S._lin(w, S._features(B + [e])) - S._lin(w, S._features(B)))

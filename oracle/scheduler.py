@@ -21,7 +21,10 @@ def _features(entries):
     P2 = 0.0
     D = 0
     seen = set()
-    for kind, c, l, g, st in entries:
+    for e in entries:
+        if e[0] == "w0":
+            continue
+        kind, c, l, g, st = e
         if kind == "d":
             S_d += 1
             N_d += 1
@@ -45,11 +48,21 @@ def _num_blocks(l, B):
     return -(-l // B) if l > 0 else 0
 
 
-def schedule(w, block_size, running, queue, t, c, m, online):
+def schedule(w, block_size, running, queue, t, c, m, online, batch=None):
     """running/queue: lists of (cached, prompt_left, shared_prefix_tokens, group).
-    Returns ([(index, tokens, t_req)], t_left, c_left, m_left)."""
-    t = t - w[0]
-    B = []        # feature entries
+    Returns ([(index, tokens, t_req)], t_left, c_left, m_left).
+
+    batch: the iteration's batch so far, a list of feature entries shared by
+    the phases of Alg. 2 (the online phase, then the offline phase
+    on the same batch), extended in place; the intercept is charged by the
+    phase that finds it empty of charges (batch None: a batch of its own).
+    The charge is recorded as a marker entry ("w0",) that _features skips."""
+    if batch is None:
+        batch = []
+    if ("w0",) not in batch:
+        t = t - w[0]
+        batch.append(("w0",))
+    B = batch     # feature entries of the whole batch
     out = []
 
     def marg(extra):

@@ -109,14 +109,14 @@ _SIGS = {
     "hg_batch_features": ([P, i32, P], i32),
     "hg_predictor_fit": ([P, P, i32, i32, P], i32),
     "hg_predictor_predict": ([P, P], ctypes.c_double),
-    "hg_slo_aware_schedule": ([P, i32, P, i32, P, i32, ctypes.c_double, i32, i32, i32, P, P, P, P, P], i32),
+    "hg_slo_aware_schedule": ([P, i32, P, i32, P, i32, ctypes.c_double, i32, i32, i32, P, P, P, P, P, P], i32),
     "hg_psm_create": ([P], i32),
     "hg_psm_destroy": ([P], i32),
     "hg_psm_insert": ([P, i32, P, i32], i32),
     "hg_psm_remove": ([P, i32], i32),
     "hg_psm_size": ([P], i32),
     "hg_psm_dfs_order": ([P, P, P, i32, P], i32),
-    "hg_psm_offline_schedule": ([P, i32, P, P, i32, P, i32, ctypes.c_double, i32, i32, P, P, P, P, P], i32),
+    "hg_psm_offline_schedule": ([P, i32, P, P, i32, P, i32, ctypes.c_double, i32, i32, P, P, P, P, P, P], i32),
 }
 
 _LIB = None
@@ -488,9 +488,19 @@ class hg_sched_entry(ctypes.Structure):
     _fields_ = [("index", i32), ("tokens", i32), ("t_req", ctypes.c_double)]
 
 
+HG_SCHED_MAX_GROUPS = 256
+
+
+class hg_sched_state(ctypes.Structure):
+    """The batch under construction across the phases of one iteration (include/hygen.h)."""
+    _fields_ = [("features", ctypes.c_double * 8), ("intercept_charged", i32), ("n_groups", i32),
+                ("groups", i32 * HG_SCHED_MAX_GROUPS)]
+
+
 def hg_slo_aware_schedule(model: hg_predictor, running, queue, latency_budget_ms: float, chunk_budget: int,
-                          memory_blocks: int, phase_online: bool, block_size: int = 16):
+                          memory_blocks: int, phase_online: bool, block_size: int = 16, state: hg_sched_state = None):
     """running / queue: sequences of (cached, prompt_left, shared_prefix_tokens, group).
+    state: hg_sched_state carried from the previous phase of the same batch (None: a batch of its own).
     Returns ([(index, tokens, t_req)], t_left, c_left, m_left)."""
     R = (hg_sched_req * max(len(running), 1))(*[hg_sched_req(*r) for r in running])
     Q = (hg_sched_req * max(len(queue), 1))(*[hg_sched_req(*r) for r in queue])
@@ -498,7 +508,8 @@ def hg_slo_aware_schedule(model: hg_predictor, running, queue, latency_budget_ms
     n = ctypes.c_int32()
     t, c, m = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
     _check(lib().hg_slo_aware_schedule(ctypes.byref(model), block_size, R, len(running), Q, len(queue),
-                                       latency_budget_ms, chunk_budget, memory_blocks, int(phase_online), out,
+                                       latency_budget_ms, chunk_budget, memory_blocks, int(phase_online),
+                                       None if state is None else ctypes.byref(state), out,
                                        ctypes.byref(n), ctypes.byref(t), ctypes.byref(c), ctypes.byref(m)))
     return [(out[k].index, out[k].tokens, out[k].t_req) for k in range(n.value)], t.value, c.value, m.value
 
@@ -543,13 +554,15 @@ class PrefixTree:
 
 
 def hg_psm_offline_schedule(model: hg_predictor, tree: PrefixTree, running, by_id, latency_budget_ms: float,
-                            chunk_budget: int, memory_blocks: int, block_size: int = 16):
+                            chunk_budget: int, memory_blocks: int, block_size: int = 16,
+                            state: hg_sched_state = None):
     R = (hg_sched_req * max(len(running), 1))(*[hg_sched_req(*r) for r in running])
     I = (hg_sched_req * max(len(by_id), 1))(*[hg_sched_req(*r) for r in by_id])
     out = (hg_sched_entry * max(len(running) + len(by_id), 1))()
     n = ctypes.c_int32()
     t, c, m = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
     _check(lib().hg_psm_offline_schedule(ctypes.byref(model), block_size, tree.h, R, len(running), I, len(by_id),
-                                         latency_budget_ms, chunk_budget, memory_blocks, out, ctypes.byref(n),
+                                         latency_budget_ms, chunk_budget, memory_blocks,
+                                         None if state is None else ctypes.byref(state), out, ctypes.byref(n),
                                          ctypes.byref(t), ctypes.byref(c), ctypes.byref(m)))
     return [(out[k].index, out[k].tokens, out[k].t_req) for k in range(n.value)], t.value, c.value, m.value

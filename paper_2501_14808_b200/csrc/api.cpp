@@ -235,24 +235,57 @@ extern "C" hg_status hg_batch_indices(const hg_kv_pool *pool, const hg_batch *ba
 // ---------------------------------------------------------------------------
 // a.3 append
 // ---------------------------------------------------------------------------
+// Small device scratch for append slots when they do not fit the kernel
+// parameters (pool-independent, grows on demand).  Appends may come on different
+// streams: each staging copy waits (stream-ordered) for the previous append
+// kernel that read the buffer, whatever its stream.
+static thread_local void *g_slot_dev = nullptr;
+static thread_local size_t g_slot_cap = 0;
+static thread_local cudaEvent_t g_slot_ev = nullptr;   // recorded after the last kernel that read g_slot_dev
+
+static hg_status slot_buffer(size_t need, cudaStream_t st) {
+    hg_status s = HG_OK;
+    if (!g_slot_ev) s = cuda_check(cudaEventCreateWithFlags(&g_slot_ev, cudaEventDisableTiming), "slot event");
+    if (s) return s;
+    if (g_slot_cap < need) {
+        if (g_slot_dev) {
+            cudaEventSynchronize(g_slot_ev);
+            cudaFree(g_slot_dev);
+            g_slot_dev = nullptr;
+            g_slot_cap = 0;
+        }
+        const size_t cap = std::max<size_t>(need * 2, 1 << 16);
+        s = cuda_check(cudaMalloc(&g_slot_dev, cap), "cudaMalloc(slots)");
+        if (s) { g_slot_dev = nullptr; return s; }
+        g_slot_cap = cap;
+    }
+    return cuda_check(cudaStreamWaitEvent(st, g_slot_ev, 0), "slot buffer wait");
+}
+
 static hg_status append_impl(hg_kv_pool *pool, const BatchView &v, const void *k_new, const void *v_new,
-                             void *slot_dev, cudaStream_t st) {
+                             cudaStream_t st) {
     const int B = pool->desc.block_size;
     int64_t T = 0;
     for (int i = 0; i < v.R; ++i) T += v.n[i];
     if (T == 0) return HG_OK;
-    std::vector<int64_t> slot((size_t)T);
+    static thread_local std::vector<int64_t> slot;
+    slot.resize((size_t)T);
     int64_t t = 0;
     for (int i = 0; i < v.R; ++i)
         for (int j = 0; j < v.n[i]; ++j, ++t) {
             int64_t pos = (int64_t)v.c[i] + j;
             slot[t] = (int64_t)v.bt[(int64_t)i * v.W + pos / B] * B + pos % B;
         }
-    hg_status s = stage_h2d(pool, slot_dev, slot.data(), sizeof(int64_t) * (size_t)T, st);
-    if (s) return s;
-    return launch_append((const uint16_t *)k_new, (const uint16_t *)v_new, (uint16_t *)pool->desc.k_cache,
-                         (uint16_t *)pool->desc.v_cache, (const int64_t *)slot_dev, (int)T,
-                         pool->desc.num_kv_heads, pool->desc.head_dim, st);
+    auto *kc = (uint16_t *)pool->desc.k_cache, *vc = (uint16_t *)pool->desc.v_cache;
+    if (T <= kParamSlots)   // slots in the kernel parameters: no staging buffer, no H2D
+        return launch_append_param((const uint16_t *)k_new, (const uint16_t *)v_new, kc, vc, slot.data(), (int)T,
+                                   pool->desc.num_kv_heads, pool->desc.head_dim, st);
+    hg_status s = slot_buffer(sizeof(int64_t) * (size_t)T, st);
+    if (!s) s = stage_h2d(pool, g_slot_dev, slot.data(), sizeof(int64_t) * (size_t)T, st);
+    if (!s) s = launch_append((const uint16_t *)k_new, (const uint16_t *)v_new, kc, vc, (const int64_t *)g_slot_dev,
+                              (int)T, pool->desc.num_kv_heads, pool->desc.head_dim, st);
+    if (!s) s = cuda_check(cudaEventRecord(g_slot_ev, st), "slot event record");
+    return s;
 }
 
 static hg_status rope_args(const hg_rope *r, int d, RopeArgs *out) {
@@ -264,10 +297,6 @@ static hg_status rope_args(const hg_rope *r, int d, RopeArgs *out) {
     out->rot = rot;
     return HG_OK;
 }
-
-// Small device scratch for append slots (pool-independent, grows on demand).
-static thread_local void *g_slot_dev = nullptr;
-static thread_local size_t g_slot_cap = 0;
 
 extern "C" hg_status hg_kv_append(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
                                   const void *v_new, void *stream) {
@@ -283,19 +312,7 @@ extern "C" hg_status hg_kv_append(hg_kv_pool *pool, const hg_batch *batch, const
     for (int i = 0; i < v.R; ++i) T += v.n[i];
     if (T == 0) return HG_OK;
     if (!k_new || !v_new) return fail(HG_E_INVALID, "k_new / v_new NULL");
-    size_t need = sizeof(int64_t) * (size_t)T;
-    if (g_slot_cap < need) {
-        cudaStream_t st = (cudaStream_t)stream;
-        if (g_slot_dev) {
-            cudaStreamSynchronize(st);
-            cudaFree(g_slot_dev);
-        }
-        size_t cap = std::max<size_t>(need * 2, 1 << 16);
-        s = cuda_check(cudaMalloc(&g_slot_dev, cap), "cudaMalloc(slots)");
-        if (s) { g_slot_dev = nullptr; g_slot_cap = 0; return s; }
-        g_slot_cap = cap;
-    }
-    return append_impl(pool, v, k_new, v_new, g_slot_dev, (cudaStream_t)stream);
+    return append_impl(pool, v, k_new, v_new, (cudaStream_t)stream);
 }
 
 extern "C" hg_status hg_kv_append_rope(hg_kv_pool *pool, const hg_batch *batch, const void *k_new,
@@ -328,22 +345,14 @@ extern "C" hg_status hg_kv_append_rope(hg_kv_pool *pool, const hg_batch *batch, 
             pos[t] = (int32_t)p;
         }
     cudaStream_t st = (cudaStream_t)stream;
-    if (g_slot_cap < img.size()) {
-        if (g_slot_dev) {
-            cudaStreamSynchronize(st);
-            cudaFree(g_slot_dev);
-        }
-        size_t cap = std::max<size_t>(img.size() * 2, 1 << 16);
-        s = cuda_check(cudaMalloc(&g_slot_dev, cap), "cudaMalloc(slots)");
-        if (s) { g_slot_dev = nullptr; g_slot_cap = 0; return s; }
-        g_slot_cap = cap;
-    }
-    s = stage_h2d(pool, g_slot_dev, img.data(), img.size(), st);
-    if (s) return s;
-    return launch_rope_append((const uint16_t *)k_new, (const uint16_t *)v_new, (uint16_t *)pool->desc.k_cache,
-                              (uint16_t *)pool->desc.v_cache, (const int64_t *)g_slot_dev,
-                              (const int32_t *)((uint8_t *)g_slot_dev + (size_t)T * 8), (int)T,
-                              pool->desc.num_kv_heads, pool->desc.head_dim, ra, st);
+    s = slot_buffer(img.size(), st);
+    if (!s) s = stage_h2d(pool, g_slot_dev, img.data(), img.size(), st);
+    if (!s) s = launch_rope_append((const uint16_t *)k_new, (const uint16_t *)v_new, (uint16_t *)pool->desc.k_cache,
+                                   (uint16_t *)pool->desc.v_cache, (const int64_t *)g_slot_dev,
+                                   (const int32_t *)((uint8_t *)g_slot_dev + (size_t)T * 8), (int)T,
+                                   pool->desc.num_kv_heads, pool->desc.head_dim, ra, st);
+    if (!s) s = cuda_check(cudaEventRecord(g_slot_ev, st), "slot event record");
+    return s;
 }
 
 // ---------------------------------------------------------------------------
@@ -788,10 +797,9 @@ extern "C" hg_status hg_plan_rows(const hg_batch *batch, int32_t H_q, int32_t H_
     for (const SkItem &it : plan.sk) {
         const ReqDev &rq = plan.reqs[it.req];
         for (int g = 0; g < H_kv; ++g)
-            for (int jj = 0; jj < it.nt; ++jj) {
-                const int j = it.j0 + jj;
-                for (int hl = 0; hl < G; ++hl)
-                    emit(rq.cu_q + j, g * G + hl, it.k0, std::min(it.k1, rq.c + j + 1), it.part, 2);
+            for (int r = 0; r < it.nrows; ++r) {   // the rows the kernel computes (SkItem stacking)
+                const int x = it.hl0 + r, j = it.j0 + x / G;
+                emit(rq.cu_q + j, g * G + x % G, it.k0, std::min(it.k1, rq.c + j + 1), it.part, 2);
             }
     }
     *n_rows = n;
@@ -938,8 +946,15 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
         }
         return HG_OK;
     };
-    if (pipe.used) {
-        // prefill rows are final when the tcgen05 kernel ends (they have no partials)
+    // Prefill rows are final when the tcgen05 kernel ends -- unless the planner
+    // cut a chunk's keys into ranges (partials merged by the combine kernel on
+    // the caller's stream): then they are read back after the combine too.
+    bool prefill_cut = false;
+    for (size_t k = 0; pipe.used && !prefill_cut && k < pool->plan.tok.size(); ++k)
+        prefill_cut = v.n[pool->plan.tok[k].req] > 1 && pool->plan.tok[k].nparts > 1;
+    if (pipe.used && prefill_cut) {
+        s = cuda_check(cudaMemcpyAsync(out_host, o_d, T * qrow, cudaMemcpyDeviceToHost, st), "D2H out");
+    } else if (pipe.used) {
         s = d2h(runs[1], pipe.side);
         if (!s) s = cuda_check(cudaEventRecord(pool->ev_d2h, pipe.side), "d2h record");
         if (!s) s = d2h(runs[0], st);

@@ -26,15 +26,20 @@ struct ReqDev {
 };
 
 // Split-K item (sm_100a mma.sync path, kernels.cu), launched once per KV head g
-// (grid.y): up to 16 stacked query rows (token j0 + r / G_q, head g*G_q + r % G_q)
-// of one request against keys [k0, k1) further capped per row by causality.
+// (grid.y): up to 16 stacked query rows of one request against keys [k0, k1)
+// further capped per row by causality.  Stacked row r has index x = hl0 + r:
+// token j0 + x / G_q, q head g*G_q + x % G_q.  G_q <= 16: hl0 = 0 and the item
+// stacks nt whole tokens (nt * G_q <= 16); G_q > 16: one token per item, its
+// q heads cut into ceil(G_q / 16) items of <= 16 rows (hl0 = 0, 16, ...).
 struct SkItem {
     int32_t req;
     int32_t j0;
-    int32_t nt;     // token rows in the item (nt * G_q <= 16)
+    int32_t nt;     // tokens the item touches
     int32_t k0;     // multiple of kBlock
     int32_t k1;
     int32_t part;   // partial index for rows that are combined (-1: direct write)
+    int32_t hl0;    // stacked-row offset inside token j0 (q-head-in-group of row 0)
+    int32_t nrows;  // stacked rows (<= kSkRows)
 };
 
 // Per batch token: where its partials live.  Partial slot of (token t, KV head

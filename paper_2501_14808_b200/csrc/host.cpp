@@ -293,17 +293,24 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     sc.pre_end.assign((size_t)v.R, 0);
     sc.npre.assign((size_t)v.R, 0);
     sc.nodes.clear();
+    // A row takes part in a node only over whole blocks inside its causal range: a
+    // node's tiles give every member the node's full key range (no per-row limit),
+    // so a decode row whose context ends inside a shared block (plain
+    // hg_hybrid_attention allows c_i + 1 < s_i * B) stops its pass at the last
+    // block it sees completely, and split-K covers the rest.
+    auto pass_cols = [&](int i) { return std::min<int64_t>(v.s[i], ((int64_t)v.c[i] + 1) / B); };
     if (o.prefix_pass && tc_ok) {
         for (int i = 0; i < v.R; ++i)
             if (v.n[i] == 1 && v.s[i] > 0) {
                 const int32_t *row = v.bt + (int64_t)i * v.W;
-                for (int col = 0; col < v.s[i]; ++col) sc.cnt[row[col]]++;
+                for (int col = 0, e = (int)pass_cols(i); col < e; ++col) sc.cnt[row[col]]++;
             }
         for (int i = 0; i < v.R; ++i) {
             if (v.n[i] != 1 || v.s[i] == 0) continue;
             const int32_t *row = v.bt + (int64_t)i * v.W;
+            const int cols = (int)pass_cols(i);
             int e = 0;
-            while (e < v.s[i] && sc.cnt[row[e]] >= 2) ++e;
+            while (e < cols && sc.cnt[row[e]] >= 2) ++e;
             sc.pre_end[i] = e;
             int a = 0, depth = 0;
             while (a < e) {
@@ -488,8 +495,12 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         for (int k = 0; k < pieces; ++k) {
             const int k0 = ch.ks + k * chunk_tok;
             const int k1 = std::min(ch.ke, k0 + chunk_tok);
-            p->sk.push_back(SkItem{ch.i, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1});
-            kv_tok_read += (int64_t)(k1 - k0) * H_kv;
+            // G_q > 16 (ch.nt == 1): the token's q heads in groups of 16 rows, each
+            // item re-reading the same key range (adjacent in the LPT order: L2 hits)
+            for (int h0 = 0; h0 < ch.nt * G; h0 += kSkRows)
+                p->sk.push_back(SkItem{ch.i, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1, h0,
+                                       std::min(kSkRows, ch.nt * G - h0)});
+            kv_tok_read += (int64_t)(k1 - k0) * H_kv * ((ch.nt * G + kSkRows - 1) / kSkRows);
         }
     }
     // ---- prefix node tiles (partial `depth` of every member row): member-major stacking ----

@@ -422,7 +422,7 @@ splitk_kernel(const AttnParams p) {
     const int g = blockIdx.y;   // KV head
     const ReqDev rq = p.reqs[it.req];
     const int G = p.G_q;
-    const int nrows = it.nt * G;
+    const int nrows = it.nrows;   // stacked rows x = hl0 + r: token j0 + x / G, q head g*G + x % G
     uint8_t *sQ = smem;
     uint8_t *sKV = smem + SkSmem<D>::kQ;
 
@@ -431,8 +431,9 @@ splitk_kernel(const AttnParams p) {
         const int r = idx / NCH, ch = idx % NCH;
         uint4 val = make_uint4(0, 0, 0, 0);
         if (r < nrows) {
-            const int t = rq.cu_q + it.j0 + r / G;
-            const int h = g * G + r % G;
+            const int x = it.hl0 + r;
+            const int t = rq.cu_q + it.j0 + x / G;
+            const int h = g * G + x % G;
             val = *reinterpret_cast<const uint4 *>(p.q + ((int64_t)t * p.H_q + h) * D + ch * 8);
         }
         *reinterpret_cast<uint4 *>(sQ + swz<D>(r, ch)) = val;
@@ -441,7 +442,7 @@ splitk_kernel(const AttnParams p) {
     const int ra = lane >> 2, rb = ra + 8;
     auto row_lim = [&](int r) -> int {
         if (r >= nrows) return 0;
-        const int lim = rq.c + it.j0 + r / G + 1;
+        const int lim = rq.c + it.j0 + (it.hl0 + r) / G + 1;
         return lim < it.k1 ? lim : it.k1;
     };
     const int lim_a = row_lim(ra), lim_b = row_lim(rb);
@@ -612,8 +613,9 @@ splitk_kernel(const AttnParams p) {
                 L += f[w] * mml[(w * kSkRows + r) * 2 + 1];
             }
             const float inv = L > 0.f ? 1.f / L : 0.f;
-            const int t = rq.cu_q + it.j0 + r / G;
-            const int h = g * G + r % G;
+            const int x = it.hl0 + r;
+            const int t = rq.cu_q + it.j0 + x / G;
+            const int h = g * G + x % G;
             int base = -1;
             if (it.part >= 0) {
                 const TokDev tk = p.tok[t];
@@ -644,7 +646,7 @@ splitk_kernel(const AttnParams p) {
                 }
                 if (p.lse && part8 == 0) p.lse[(int64_t)t * p.H_q + h] = lse2 * 0.69314718055994531f;
             } else {
-                const int64_t slot = base + (int64_t)it.part * G + (r % G);
+                const int64_t slot = base + (int64_t)it.part * G + (x % G);
                 float *dst = p.part_o + slot * D + part8 * PER;
 #pragma unroll
                 for (int e = 0; e < PER; e += 4)

@@ -44,32 +44,64 @@ void add_prefill(const Acc &a, int c, int l, double *out) {
     out[4] += 1;                                   // N_p
     out[6] += (double)l * ((double)c + (double)(l + 1) / 2.0);  // P2
 }
+// The batch under construction across the calls of one iteration (Alg. 2 runs
+// the online then the offline phase on ONE batch): its features,
+// whether the intercept was charged, and the groups that already have a decode
+// row.  Loaded from / stored to the caller's hg_sched_state (NULL: a fresh
+// batch, intercept charged in this call).
+struct Batch {
+    Acc acc;
+    std::vector<int32_t> groups_in;
+    hg_sched_state *st = nullptr;
+    hg_status load(hg_sched_state *s, const hg_predictor &M, double *t) {
+        st = s;
+        if (s) {
+            if (s->n_groups < 0 || s->n_groups > HG_SCHED_MAX_GROUPS) return fail(HG_E_INVALID, "state.n_groups");
+            for (int k = 0; k < 8; ++k) acc.f[k] = s->features[k];
+            groups_in.assign(s->groups, s->groups + s->n_groups);
+            if (s->intercept_charged) return HG_OK;
+        }
+        *t -= M.w[0];   // the batch's fixed cost (intercept) is charged once per batch
+        return HG_OK;
+    }
+    hg_status store() {
+        if (!st) return HG_OK;
+        if (groups_in.size() > (size_t)HG_SCHED_MAX_GROUPS)
+            return fail(HG_E_UNSUPPORTED, "more than %d shared-prefix groups in one batch", HG_SCHED_MAX_GROUPS);
+        for (int k = 0; k < 8; ++k) st->features[k] = acc.f[k];
+        st->intercept_charged = 1;
+        st->n_groups = (int32_t)groups_in.size();
+        std::copy(groups_in.begin(), groups_in.end(), st->groups);
+        return HG_OK;
+    }
+    bool has_group(int32_t g) const { return std::find(groups_in.begin(), groups_in.end(), g) != groups_in.end(); }
+};
 }  // namespace
 
 extern "C" hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t block_size, const hg_sched_req *running,
                                            int32_t n_running, const hg_sched_req *queue, int32_t n_queue,
                                            double t_budget, int32_t chunk_budget, int32_t memory_blocks,
-                                           int32_t phase_online, hg_sched_entry *out, int32_t *n_out, double *t_left,
-                                           int32_t *c_left, int32_t *m_left) {
+                                           int32_t phase_online, hg_sched_state *state, hg_sched_entry *out,
+                                           int32_t *n_out, double *t_left, int32_t *c_left, int32_t *m_left) {
     if (!model || block_size < 1 || n_running < 0 || n_queue < 0 || (n_running && !running) || (n_queue && !queue) ||
         !out || !n_out || chunk_budget < 0 || memory_blocks < 0)
         return fail(HG_E_INVALID, "bad arguments");
     const hg_predictor &M = *model;
-    double t = t_budget - M.w[0];   // the batch's fixed cost (intercept) is charged once
+    double t = t_budget;
+    Batch bat;
+    hg_status st = bat.load(state, M, &t);
+    if (st) return st;
     int64_t c = chunk_budget, m = memory_blocks;
     int nb = 0;
-    Acc acc;
-    std::vector<int32_t> groups_in;   // shared-prefix groups that already have a decode row in B
+    Acc &acc = bat.acc;
+    std::vector<int32_t> &groups_in = bat.groups_in;   // shared-prefix groups that already have a decode row in B
     double f[8];
     auto marginal = [&](const double *fn) { return std::max(0.0, lin(M, fn) - lin(M, acc.f)); };
     // ---- decodes of the running requests (Alg. 1 lines 6-13) ----
     for (int i = 0; i < n_running; ++i) {
         const hg_sched_req &r = running[i];
         if (r.prompt_left > 0) continue;
-        int dup = 0;
-        if (r.group >= 0 && r.shared_prefix_tokens > 0 &&
-            std::find(groups_in.begin(), groups_in.end(), r.group) != groups_in.end())
-            dup = r.shared_prefix_tokens;
+        const int dup = r.group >= 0 && r.shared_prefix_tokens > 0 && bat.has_group(r.group) ? r.shared_prefix_tokens : 0;
         add_decode(acc, r.cached, dup, f);
         const double t_req = marginal(f);
         if (t_req <= t || phase_online) {
@@ -124,6 +156,8 @@ extern "C" hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t bl
             break;   // (online: PERFORM_PREEMPTION + retry is out of scope, reading R21)
         }
     }
+    st = bat.store();
+    if (st) return st;
     *n_out = nb;
     if (t_left) *t_left = t;
     if (c_left) *c_left = (int32_t)c;
@@ -141,17 +175,21 @@ extern "C" hg_status hg_slo_aware_schedule(const hg_predictor *model, int32_t bl
 extern "C" hg_status hg_psm_offline_schedule(const hg_predictor *model, int32_t block_size, hg_psm *psm,
                                              const hg_sched_req *running, int32_t n_running,
                                              const hg_sched_req *by_id, int32_t n_ids, double t_budget,
-                                             int32_t chunk_budget, int32_t memory_blocks, hg_sched_entry *out,
-                                             int32_t *n_out, double *t_left, int32_t *c_left, int32_t *m_left) {
+                                             int32_t chunk_budget, int32_t memory_blocks, hg_sched_state *state,
+                                             hg_sched_entry *out, int32_t *n_out, double *t_left, int32_t *c_left,
+                                             int32_t *m_left) {
     if (!model || !psm || block_size < 1 || n_running < 0 || (n_running && !running) || n_ids < 0 ||
         (n_ids && !by_id) || !out || !n_out || chunk_budget < 0 || memory_blocks < 0)
         return fail(HG_E_INVALID, "bad arguments");
     const hg_predictor &M = *model;
-    double t = t_budget - M.w[0];
+    double t = t_budget;
+    Batch bat;
+    hg_status st = bat.load(state, M, &t);
+    if (st) return st;
     int64_t c = chunk_budget, m = memory_blocks;
     int nb = 0;
-    Acc acc;
-    std::vector<int32_t> groups_in;
+    Acc &acc = bat.acc;
+    std::vector<int32_t> &groups_in = bat.groups_in;
     double f[8];
     auto marginal = [&](const double *fn) { return std::max(0.0, lin(M, fn) - lin(M, acc.f)); };
     const bool monotone = M.w[1 + 0] >= 0 && M.w[1 + 2] >= 0 && M.w[1 + 6] >= 0;
@@ -192,10 +230,8 @@ extern "C" hg_status hg_psm_offline_schedule(const hg_predictor *model, int32_t 
     for (int i = 0; i < n_running && !stopped; ++i) {
         const hg_sched_req &r = running[i];
         if (r.prompt_left <= 0) {
-            int dup = 0;
-            if (r.group >= 0 && r.shared_prefix_tokens > 0 &&
-                std::find(groups_in.begin(), groups_in.end(), r.group) != groups_in.end())
-                dup = r.shared_prefix_tokens;
+            const int dup =
+                r.group >= 0 && r.shared_prefix_tokens > 0 && bat.has_group(r.group) ? r.shared_prefix_tokens : 0;
             add_decode(acc, r.cached, dup, f);
             const double t_req = marginal(f);
             if (t < t_req) { stopped = true; break; }
@@ -223,6 +259,8 @@ extern "C" hg_status hg_psm_offline_schedule(const hg_predictor *model, int32_t 
         take_prefill(r, l, t_req, n_running + rid);
         hg_psm_remove(psm, rid);
     }
+    st = bat.store();
+    if (st) return st;
     *n_out = nb;
     if (t_left) *t_left = t;
     if (c_left) *c_left = (int32_t)c;

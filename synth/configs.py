@@ -76,6 +76,13 @@ class BatchSpec:
         return replace(self, **kw)
 
 
+def shard_slice(spec: BatchSpec, G: int) -> BatchSpec:
+    """One rank's slice of G-way KV-head sharding: H_kv / G KV heads
+    and their H_q / G q heads, same requests (values of the first heads)."""
+    assert spec.H_kv % G == 0
+    return spec.with_(H_kv=spec.H_kv // G, H_q=spec.H_q // G)
+
+
 def _uniform(rng, lo, hi, k):
     return [int(x) for x in rng.integers(lo, hi + 1, size=k)]
 

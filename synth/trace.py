@@ -150,3 +150,11 @@ def sweep(seed: int = 0, iters: int = 64, warm: int = 200, rhos=RHOS, chunks=CHU
                 if spec.requests:
                     out.append(spec)
     return out
+
+
+def c4_batch(index: int, seed: int = 0, iters: int = 64, **shape) -> BatchSpec:
+    """Batch number `index` of the C4 sweep (same order as ``sweep``): a named,
+    regenerable test case (e.g. #219 of the Llama-3-8B sweep: a 49-token chunk at
+    c = 10240 beside a 975-token chunk and 59 decodes)."""
+    shape = {"H_q": 32, "H_kv": 8, "d": 128, **shape}
+    return sweep(seed=seed, iters=iters, **shape)[index]

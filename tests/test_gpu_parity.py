@@ -296,10 +296,16 @@ def _e2e_spec(name):
                                          Request(0, 77), Request(129, 1), Request(64, 300, True)])
     if name == "d64_gqa5":
         return _mixed(name, 40, 8, 64, [Request(17, 1), Request(0, 130), Request(2000, 1), Request(5, 33, True)])
+    if name == "c4_small_chunk":   # prefill key cuts: the chunk's rows are merged by the combine kernel
+        return _prefill_split_spec(name)
+    if name == "c4_219":
+        from synth.trace import c4_batch
+        return c4_batch(219)
     return make_config(name, 0)
 
 
-@pytest.mark.parametrize("name", ["toy_a", "toy_b", "c1", "c2", "c3", "p1", "interleaved", "d64_gqa5"])
+@pytest.mark.parametrize("name", ["toy_a", "toy_b", "c1", "c2", "c3", "p1", "interleaved", "d64_gqa5",
+                                  "c4_small_chunk", "c4_219"])
 def test_e2e_host_step_matches_device_path(name):
     """hg_hybrid_step_host (host buffers, two pipelined input waves: decode rows
     then prefill-chunk rows) runs first on a fresh pool -- so its own append
@@ -320,7 +326,7 @@ def test_e2e_host_step_matches_device_path(name):
         torch.cuda.synchronize()
         assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), rep
         assert torch.equal(k_after, wl.k_cache) and torch.equal(v_after, wl.v_cache), rep
-    if name in ("toy_a", "toy_b", "interleaved"):
+    if name in ("toy_a", "toy_b", "interleaved", "c4_small_chunk", "c4_219"):
         wl.out.copy_(oh.cuda())
         compare(spec, wl, check_lse=False, tag=" (host step)")
 
@@ -381,10 +387,8 @@ def test_shard_slices_full_size(name):
     """One rank's slice of 8-way KV-head sharding at full size (c1: 4 KV heads;
     C3: 1 KV head x 8 q heads, with its prefix groups), the plans bench.py's
     shard_projection times: sampled requests against the oracle."""
-    import os
-    import pickle
-    spec = pickle.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
-                                         name + ".pkl"), "rb"))
+    from synth.configs import make_config, shard_slice
+    spec = shard_slice(make_config(name.split("_")[0], 0), 8)
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
@@ -423,10 +427,11 @@ def test_max_context_16k():
     compare(spec, wl, req_sel=[1])
 
 
-@pytest.mark.parametrize("H_q,H_kv", [(64, 4), (12, 4), (40, 8), (16, 1)])
+@pytest.mark.parametrize("H_q,H_kv", [(64, 4), (12, 4), (40, 8), (16, 1), (32, 1), (64, 1), (64, 2), (48, 1)])
 def test_gqa_group_sizes(H_q, H_kv):
     """G_q = 16, 3, 5, 16: split-K row stacking (16 // G tokens per item) and
-    tcgen05 stacking with hl0 != 0 (G not dividing 128)."""
+    tcgen05 stacking with hl0 != 0 (G not dividing 128); G_q = 32, 64, 32, 48:
+    a decode token's q heads span several 16-row split-K items."""
     from synth.configs import Request
     reqs = [Request(300, 200), Request(40, 1), Request(1000, 1, True), Request(0, 77), Request(129, 1)]
     spec = _mixed(f"gqa{H_q}x{H_kv}", H_q, H_kv, 128, reqs)
@@ -564,12 +569,12 @@ def test_c2_nested_full_size():
 @pytest.mark.parametrize("seed", range(60))
 def test_mixed_feature_fuzz(seed):
     """Everything at once on random small batches: nested prefix tries, GQA group
-    sizes 1-16, d in {64, 128}, RoPE on/off, and the plan switches (fixed split,
+    sizes 1-64, d in {64, 128}, RoPE on/off, and the plan switches (fixed split,
     no prefix pass, no tcgen05), through the fused step, against the oracle."""
     import paper_2501_14808_b200 as hg
     from synth.configs import make_fuzz, make_fuzz_nested
     rng = np.random.default_rng(50_000 + seed)
-    G = int(rng.choice([1, 2, 4, 8, 16]))
+    G = int(rng.choice([1, 2, 4, 8, 16, 32, 64]))
     d = int(rng.choice([64, 128]))
     spec = (make_fuzz_nested if seed % 2 else make_fuzz)(seed, G_q=G, H_kv=int(rng.choice([1, 2])), d=d)
     if rng.random() < 0.5:

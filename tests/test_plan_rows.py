@@ -142,15 +142,52 @@ def test_invalid_batch_rejected():
 
 
 def test_c4_batch_with_a_small_chunk_at_10k():
-    """C4 batch #219 (tools/slow_batch_c4_219.pkl): a 49-token chunk at c = 10240
+    """C4 batch #219 (synth.trace.c4_batch(219)): a 49-token chunk at c = 10240
     beside a 975-token chunk at c = 0 and 59 decodes.  Whole, its 8 items walk 81
     KV tiles each while everything else is done (0.222 ms); cut, 0.112 ms."""
-    import os
-    import pickle
-    spec = pickle.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
-                                         "slow_batch_c4_219.pkl"), "rb"))
+    from synth.trace import c4_batch
+    spec = c4_batch(219)
     lay = make_layout(spec, seed=219)
     rows = check_plan(spec, lay)
     cut = (rows[:, 5] == 0) & (rows[:, 4] >= 0)
     t_long = sum(r.n for r in spec.requests[:[i for i, r in enumerate(spec.requests) if r.c == 10240][0]])
     assert cut.any() and np.all(rows[cut, 0] >= t_long) and np.all(rows[cut, 0] < t_long + 49)
+
+
+@pytest.mark.parametrize("G_q,H_kv", [(32, 1), (64, 1), (32, 2), (48, 1), (24, 2)])
+@pytest.mark.parametrize("seed", range(6))
+def test_gqa_groups_above_16(G_q, H_kv, seed):
+    """G_q > 16 (MQA-like groups, P:63 batches any model's rows): a decode row's q
+    heads exceed one 16-row split-K item, so each token's rows are cut into
+    ceil(G_q / 16) items; every (token, q head) must still be covered exactly."""
+    for make in (make_fuzz, make_fuzz_nested):
+        spec = make(seed, G_q=G_q, H_kv=H_kv)
+        lay = make_layout(spec, seed=seed)
+        check_plan(spec, lay)
+        check_plan(spec, lay, opts=hg.make_opts(disable_tc=True))
+        check_plan(spec, lay, opts=hg.make_opts(split_tokens=64))
+
+
+def test_decode_row_ending_inside_a_shared_block():
+    """Plain hg_hybrid_attention accepts a decode row whose context ends inside a
+    shared block (c_i + 1 < s_i * B; only an append forbids it).  The prefix node's
+    tiles give every member the node's whole key range, so such a row may join a
+    node only over the blocks it sees completely; the keys past its causal limit
+    must not be covered (check_plan: ranges end exactly at c_i + 1)."""
+    spec = BatchSpec("inside_shared", 8, 2, 64, 16, 0,
+                     [Request(30, 1, True), Request(100, 1, True), Request(47, 1, True), Request(12, 1, True)])
+    # rows 0-3 share blocks [5, 6, 7] (48 tokens) in their first columns
+    bt = np.full((4, 8), -1, np.int32)
+    bt[0, :2] = [5, 6]
+    bt[1, :7] = [5, 6, 7, 10, 11, 12, 13]
+    bt[2, :3] = [5, 6, 7]
+    bt[3, :1] = [5]
+    shared = [2, 3, 3, 1]
+    b = hg.Batch(bt, [r.c for r in spec.requests], [1] * 4, None, shared)
+    for opts in (None, hg.make_opts(split_tokens=16)):
+        rows = hg.hg_plan_rows(b, spec.H_q, spec.H_kv, spec.d, 32, 148, True, opts)
+        t, k1 = rows[:, 0], rows[:, 3]
+        for i, r in enumerate(spec.requests):
+            assert k1[t == i].max() == r.c + 1, (i, k1[t == i].max())
+        # row 1 (c = 100) and row 2 (c = 47) still read blocks 5..7 once through a node
+        assert ((rows[:, 5] == 1) & (t == 1)).any()

@@ -23,10 +23,18 @@ class Trie:
         self.tokens[rid] = list(tokens)
 
     def remove(self, rid):
-        node = self.root
-        for tok in self.tokens.pop(rid):
-            node = node["kids"][tok]
-        node["reqs"].remove(rid)
+        path = [self.root]
+        toks = self.tokens.pop(rid)
+        for tok in toks:
+            path.append(path[-1]["kids"][tok])
+        path[-1]["reqs"].remove(rid)
+        # prune the subtree the removal emptied (reading R22: children keep their
+        # order of first insertion into the live tree)
+        for depth in range(len(toks), 0, -1):
+            node = path[depth]
+            if node["reqs"] or node["kids"]:
+                break
+            del path[depth - 1]["kids"][toks[depth - 1]]
 
     def dfs(self):
         out = []

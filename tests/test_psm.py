@@ -85,3 +85,60 @@ def test_offline_schedule_matches_mirror(seed):
     np.testing.assert_allclose([x for _, _, x in got[0]], [x for _, _, x in exp[0]], rtol=1e-9, atol=1e-12)
     assert got[2:] == exp[2:] and abs(got[1] - exp[1]) < 1e-9
     assert tree.hg_psm_size() == len(mt.dfs())
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_interleaved_ops_match_mirror(seed):
+    """Inserts, removals (which prune emptied subtrees) and DFS reads interleaved:
+    a request inserted into a pruned subtree's place goes after its live siblings
+    in both the library and the mirror (R22), and the LCP of live neighbours
+    separated by removed entries is recomputed correctly."""
+    rng = np.random.default_rng(900 + seed)
+    t, m = hg.PrefixTree(), OP.Trie()
+    alive, nxt = [], 0
+    stems = [list(rng.integers(0, 4, int(rng.integers(0, 5)))) for _ in range(5)]
+    for step in range(120):
+        op = rng.random()
+        if op < 0.5 or not alive:
+            toks = stems[int(rng.integers(0, 5))] + list(rng.integers(0, 3, int(rng.integers(0, 4))))
+            t.hg_psm_insert(nxt, toks)
+            m.insert(nxt, toks)
+            alive.append(nxt)
+            nxt += 1
+        elif op < 0.85:
+            rid = alive.pop(int(rng.integers(0, len(alive))))
+            t.hg_psm_remove(rid)
+            m.remove(rid)
+        else:   # Alg. 3's loop: take the next DFS request and remove it
+            ids, _ = t.hg_psm_dfs_order(1)
+            assert ids == m.dfs()[:1]
+            t.hg_psm_remove(ids[0])
+            m.remove(ids[0])
+            alive.remove(ids[0])
+        k = int(rng.integers(1, 8))
+        got = t.hg_psm_dfs_order(k)
+        order, lcp = m.lcp_with_prev()
+        assert got == (order[:k], lcp[:k]), step
+        assert t.hg_psm_size() == len(alive)
+
+
+def test_admission_loop_is_linear():
+    """P:647-651 (O(1) next request): admitting 2,048 offline requests with 1,024-token
+    shared prefixes one at a time (dfs_order(1) then remove, as Alg. 3 does) must not
+    rebuild the tree per removal -- bounded wall time (the quadratic version took
+    minutes at this size)."""
+    import time
+    rng = np.random.default_rng(3)
+    t = hg.PrefixTree()
+    for g in range(64):
+        prefix = list(rng.integers(0, 32000, 1024))
+        for k in range(32):
+            t.hg_psm_insert(g * 32 + k, prefix + list(rng.integers(0, 32000, 64)))
+    t0 = time.perf_counter()
+    seen = []
+    while t.hg_psm_size():
+        ids, _ = t.hg_psm_dfs_order(1)
+        seen.append(ids[0])
+        t.hg_psm_remove(ids[0])
+    assert sorted(seen) == list(range(2048))
+    assert time.perf_counter() - t0 < 2.0

@@ -1,16 +1,21 @@
 """bench.py -- one hybrid serving iteration's attention on B200 (HyGen hot path).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--extra]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-extra]
 
 A "step" is one pass of the whole hot path over one batch:
 host plan (validation, indices, prefix tile map) + one descriptor H2D + KV append
 + hybrid attention, through the C ABI's fused entry point hg_hybrid_step.
-The N=1 workload is BASELINE.json configs[1] (Llama-2-7B attention shape,
-512-token prefill chunk + 64 decodes at ctx 1-4K: "c1").  With --gpus N > 1
-(torchrun, one rank per GPU) KV heads are sharded across ranks and the outputs
+The workload at EVERY N is BASELINE.json configs[3] ("c3": Llama-3-70B GQA
+attention shape, 64 q / 8 KV heads, one 512-token online prefill chunk + 256
+decodes at ctx 1-8K, half of them offline in 4 groups sharing 1024-token
+prefixes) -- the north_star's head-sharded scaling case, so the N = 1 line and
+the N = 1 point of the scaling run are the same measurement.  With --gpus N > 1
+KV heads are sharded across N ranks (one process per GPU; bench.py re-launches
+itself under torch.distributed.run when WORLD_SIZE is unset) and the outputs
 are all-gathered by the attention epilogues themselves, storing into every
-rank's peer window over NVLink (hg_hybrid_attention_tp with an open window;
-NCCL is only the fallback): total work fixed -> "strong".
+rank's peer window over NVLink (hg_hybrid_step_tp with an open window; NCCL is
+only the fallback): total work fixed -> "strong".  c1 (configs[1]) and the
+other configs are reported under "extra".
 
 --impl reference times the fp64 CPU oracle (oracle/, the only reference this
 paper-only task has) on the host cores, on a bounded sample of the same
@@ -22,6 +27,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -32,9 +38,18 @@ if ROOT not in sys.path:
 
 METRIC = "mixed-batch attention tokens/s"
 UNIT = "tokens/s"
-WORKLOAD = "c1"
-WORKLOAD_DESC = ("Llama-2-7B attention shape (32 q/kv heads, head_dim 128, KV block 16): one online 512-token "
-                 "prefill chunk at c=0 + 64 decodes at ctx U[1024,4096] (32 online, 32 offline), bf16")
+WORKLOAD = "c3"
+WORKLOAD_DESC = ("Llama-3-70B GQA attention shape (64 q / 8 KV heads, head_dim 128, KV block 16): one online "
+                 "512-token prefill chunk at c=0 + 128 online decodes + 128 offline decodes (4 groups x 32 sharing "
+                 "a 1024-token prefix), ctx U[1024,8192], bf16")
+
+
+def config_dict(spec, world):
+    """The line's `config` (identical in both arms, so the driver can pair them)."""
+    return {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "tokens_per_step": spec.T,
+            "parallelism": "single GPU" if world == 1 else
+            f"kv-head tp{world} (H_kv/{world} KV heads per rank), all-gather fused into the epilogues (peer window)",
+            "l2": "flushed (256 MB write) before every timed step, outside the events; KV working set 4.3 GB > L2"}
 
 
 def env_rank():
@@ -173,6 +188,8 @@ def run_ours(args):
     from synth.configs import make_config
 
     rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # HG_BENCH_SAME_GPU=1 is a functional test of the multi-rank path on a one-GPU box:
     # every rank on device 0, gloo for the bench's own collectives, no NCCL
     # communicator (the peer window carries the gather).  Its timings are not a
@@ -255,12 +272,15 @@ def run_ours(args):
     t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
     e2e = None if args.profile else measure_e2e(wl, spec, args, stream)
     split_calls = None if args.profile else measure_append_attention(wl, flush, stream)
+    extra = extra_configs(args, peaks, dev) if args.extra else None
+    if extra:   # the tensor-bound (prefill-heavy) configs' rooflines, kept inside the roofline dict
+        roofline["prefill_heavy"] = {k: v["roofline"] for k, v in extra.items() if k in ("p1", "p2")}
+        roofline["other_configs"] = {k: v["roofline"] for k, v in extra.items() if k not in ("p1", "p2")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded counter-based N(0,1)-scale bf16 Q/K/V; fragmented block tables)",
-        "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "tokens_per_step": T, "parallelism": "single GPU",
-                   "l2": "flushed (256 MB write) before every timed step, outside the events; KV working set 2.7 GB > L2"},
+        "config": config_dict(spec, 1),
         "roofline": roofline,
         "step_roofline": {"alg_bytes": bt, "alg_flops": fl, "t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms},
         "kernel_ms": {"splitk": sk_avg, "tc": statistics.mean(tc_ms) if tc_ms else None,
@@ -279,8 +299,8 @@ def run_ours(args):
         "e2e": e2e,
         "clocks": clk.summary(),
     }
-    if args.extra:
-        line["extra"] = extra_configs(args, peaks, dev)
+    if extra:
+        line["extra"] = extra
     if not args.profile and not args.no_predictor:
         pred = predictor_sweep(dev, iters=args.sweep_iters)
         model = pred.pop("_model")
@@ -294,10 +314,9 @@ def run_ours(args):
         line["psm_vs_fcfs"] = psm_vs_fcfs(dev)
     if args.extra:
         line["next4"] = next4(dev, peaks)
-        line["shard_projection"] = shard_projection(spec, dev, ms)
-        # the north_star's multi-GPU config: Llama-3-70B-shaped C3 (8 KV heads)
-        c3 = make_config("c3", 0)
-        line["shard_projection_c3"] = shard_projection(c3, dev, line["extra"]["c3"]["ms_per_step"])
+        # the north_star's multi-GPU config (this line's workload): per-rank sharded step at G = 2/4/8
+        line["shard_projection_c3"] = shard_projection(spec, dev, ms, peaks)
+        line["shard_projection_c1"] = shard_projection(make_config("c1", 0), dev, extra["c1"]["ms_per_step"], peaks)
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
     wl.close()
     print(json.dumps(line))
@@ -315,23 +334,37 @@ def load_traffic(kernel, alg_bytes):
         return None
 
 
-def shard_projection(spec, dev, ms_step, reps=50):
-    """One GPU timing the per-rank work of KV-head sharding at G = 2, 4, 8: the
-    same batch with H_kv/G KV heads (and H_q/G q heads), fused step, L2 flushed.
-    A projection, not a multi-GPU measurement: the peer-window stores over
-    NVLink (T * H_q * d * 2 * (G-1)/G bytes per rank, ~1 us at G = 8 on
-    900 GB/s) and the two flag barriers are not in it."""
+def shard_projection(spec, dev, ms_step, peaks, reps=50):
+    """One GPU timing the per-rank work of KV-head sharding at G = 1, 2, 4, 8: rank
+    0's slice (H_kv/G KV heads, H_q/G q heads) through the SHARDED entry point
+    hg_hybrid_step_tp on a 1-rank peer-window communicator -- the fused append
+    with the window entry barrier, the epilogues storing into the window, the
+    exit flag barrier -- L2 flushed, device time (the GPU is kept busy while the
+    host plans).  What a 1-GPU box cannot show: the other G-1 destinations of each
+    epilogue store (T*H_q*d*2*(G-1)/G bytes per rank over NVLink, ~11 MB at G = 8 on
+    C3 = ~12 us at 900 GB/s if none of it overlapped the kernels) and the wait for
+    the slowest peer at the barriers."""
     import torch
+    import paper_2501_14808_b200 as hg
     from paper_2501_14808_b200.harness import Workload
+    from synth.configs import shard_slice
     out = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     base = None
     for G in (1, 2, 4, 8):
         if spec.H_kv % G:
             continue
-        wl = Workload(spec.with_(H_kv=spec.H_kv // G, H_q=spec.H_q // G) if G > 1 else spec, device=dev)
+        local = shard_slice(spec, G)
+        wl = Workload(local, device=dev)
+        comm = hg.Comm(None, 0, 1, dev.index)
+        h = comm.hg_comm_window_create(local.T * local.H_q * local.d * 2)
+        comm.hg_comm_window_open([h])
+        win = comm.window((local.T, local.H_q, local.d))
+        ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, local.H_q),
+                         dtype=torch.uint8, device=dev)
+        step = lambda: hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, local.H_q, wl.q, wl.k_new, wl.v_new, win, ws)
         for _ in range(3):
-            wl.step()
+            step()
         torch.cuda.synchronize()
         ts = []
         for _ in range(reps):
@@ -339,20 +372,23 @@ def shard_projection(spec, dev, ms_step, reps=50):
             torch.cuda._sleep(1_000_000)   # GPU busy while the host plans and enqueues: device time only
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            wl.step()
+            step()
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
+        comm.close()
         wl.close()
         m = statistics.median(ts)
         base = m if G == 1 else base
-        out[f"G={G}"] = {"per_rank_ms": m, "projected_speedup": base / m}
+        t_roof = alg_bytes_total(local) / (peaks["hbm_gbs"] * 1e9) * 1e3
+        out[f"G={G}"] = {"per_rank_ms": m, "projected_speedup": base / m, "per_rank_t_roof_ms": t_roof,
+                         "per_rank_roof_frac": t_roof / m}
     out["workload"] = spec.name
-    out["note"] = ("per-rank fused step on one GPU with 1/G of the heads, each call alone (device time: the GPU "
-                   "is kept busy while the host plans; median, L2 flushed), "
-                   "speedup against G = 1 timed the same way; excludes the NVLink window stores and the flag "
-                   "barriers -- a projection, not a multi-GPU measurement (the bench loop's own step: %.4f ms)"
-                   % ms_step)
+    out["note"] = ("rank 0's slice through hg_hybrid_step_tp on a 1-rank peer window (append + entry barrier, "
+                   "epilogue window stores, exit barrier), each call alone, median of %d, L2 flushed, device time; "
+                   "speedup against G = 1 timed the same way; the NVLink copies to the other G-1 ranks and "
+                   "waiting for peers are not in it -- a projection, not a multi-GPU measurement (the bench "
+                   "loop's own step at G = 1: %.4f ms)" % (reps, ms_step))
     return out
 
 
@@ -452,7 +488,7 @@ def extra_configs(args, peaks, dev):
     from paper_2501_14808_b200.harness import Workload
     from synth.configs import make_config
     out = {}
-    for name in ("c2", "c3", "p1", "p2"):
+    for name in ("c1", "c2", "p1", "p2"):
         spec = make_config(name, 0)
         wl = Workload(spec, device=dev)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -498,13 +534,16 @@ def extra_configs(args, peaks, dev):
                                      "peak_kind": "measured burst (MEASURED_PEAKS.json bf16_tflops, cuBLAS)",
                                      # for a long prefill-heavy run: the part sits at its 1 kW power cap
                                      # (tools/clock_probe.py), where cuBLAS itself sustains this figure
-                                     "frac_vs_sustained": ach / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])}
+                                     "frac_vs_sustained": ach / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                                     "alg_flops_per_launch": fl, "avg_launch_ms": kms["tc"], "step_ms": m,
+                                     "share_of_step": kms["tc"] / m}
         elif kms["splitk"]:
             b_sk = alg_bytes_splitk(spec)
             ach = b_sk / (kms["splitk"] / 1e3) / 1e9
             out[name]["roofline"] = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": ach,
                                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
-                                     "alg_bytes_per_launch": b_sk}
+                                     "alg_bytes_per_launch": b_sk, "avg_launch_ms": kms["splitk"], "step_ms": m,
+                                     "share_of_step": kms["splitk"] / m}
         wl.close()
         del wl
         torch.cuda.empty_cache()
@@ -749,7 +788,7 @@ def next4(dev, peaks, reps=20):
     from synth.configs import make_config
     from synth.values import KIND_O, KIND_W, matrix
     res = {}
-    spec = make_config(WORKLOAD, 0)
+    spec = make_config("c1", 0)
     for name, sp in (("c1", spec), ("c1_rope", spec.with_(rope=(1e4, 0)))):
         wl = Workload(sp, device=dev)
         for _ in range(3):
@@ -853,14 +892,16 @@ def psm_vs_fcfs(dev, groups=64, per_group=32, batch=128, H=(32, 8, 128), seed=0)
 
 
 def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
-    """KV-head sharded attention on `world` GPUs, all-gather fused via peer windows (strong scaling)."""
+    """KV-head sharded attention on `world` GPUs, all-gather fused via peer windows
+    (strong scaling): the same timing rules as N = 1 -- L2 flushed before every
+    timed step, per-step CUDA events on the launching stream, the sum of the step
+    times on each rank, MAX over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2501_14808_b200 as hg
     from paper_2501_14808_b200.harness import Workload
-    assert spec.H_kv % world == 0
-    Hk, Hq = spec.H_kv // world, spec.H_q // world
-    local = spec.with_(H_kv=Hk, H_q=Hq)
+    from synth.configs import shard_slice
+    local = shard_slice(spec, world)
     # each rank's slice is generated as its own (smaller-head) workload; values are synthetic
     wl = Workload(local, device=dev)
     same_gpu = os.environ.get("HG_BENCH_SAME_GPU") == "1"
@@ -876,26 +917,42 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q), dtype=torch.uint8,
                      device=dev)
     stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step():   # the sharded serving step: append of this rank's K/V slice fused with the attention
-        hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, wl.k_new, wl.v_new, out, ws, stream)
+    def step(opts=None):   # the sharded serving step: append of this rank's K/V slice fused with the attention
+        hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, wl.k_new, wl.v_new, out, ws, stream, opts)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    kopts = [hg.make_opts(events=e) for e in kev]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     dist.barrier()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
-        s.record()
-        for _ in range(args.steps):
-            step()
-        e.record()
+        for k in range(args.steps):
+            flush_l2(flush)                     # L2 flushed between steps, outside the timed events
+            starts[k].record(stream)
+            step(kopts[k])
+            ends[k].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
+    st = hg.hg_last_plan_stats(wl.pool)
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    sk_ms = [e[2].elapsed_time(e[3]) for e in kev] if st["splitk_items"] else []
     cdev = "cpu" if same_gpu else dev   # gloo (same-GPU functional test) reduces host tensors
-    t = torch.tensor([s.elapsed_time(e)], device=cdev)
+    t = torch.tensor([sum(step_ms)], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = t.item()
+    # per-rank rooflines: this rank's split-K kernel and its whole step
+    sk_avg = statistics.mean(sk_ms) if sk_ms else None
+    b_sk = alg_bytes_splitk(local)
+    ach = b_sk / (sk_avg / 1e3) / 1e9 if sk_avg else None
+    t_roof_rank = alg_bytes_total(local) / (peaks["hbm_gbs"] * 1e9) * 1e3
+    mine = torch.tensor([ach or 0.0, sum(step_ms) / args.steps], device=cdev, dtype=torch.float64)
+    allr = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allr, mine)
     # e2e through the public API with host buffers: each rank's pinned q / k_new / v_new
     # slices in; out, the gathered O [T][H_q][d] read back once per job -- rank r copies
     # token rows [r T/N, (r+1) T/N) of it (every head: rows other ranks computed too);
@@ -924,13 +981,25 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     e2e_s = te.item() * args.steps / e2e_steps   # per args.steps steps, as below
     if rank == 0:
         ms = total_ms / args.steps
+        per_rank = [{"rank": r, "ms_per_step": float(x[1]), "splitk_gbs": float(x[0]),
+                     "step_roof_frac": t_roof_rank / float(x[1])} for r, x in enumerate(allr)]
+        roofline = {"bound": "hbm", "kernel": "splitk_kernel<128> (per rank)", "achieved": ach,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": (ach / peaks["hbm_gbs"]) if ach else None,
+                    "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)", "traffic": None,
+                    "alg_bytes_per_launch": b_sk, "avg_launch_ms": sk_avg,
+                    "share_of_step": (sk_avg / ms) if sk_avg else None,
+                    "per_rank_step": {"alg_bytes": alg_bytes_total(local), "t_roof_ms": t_roof_rank,
+                                      "frac_slowest_rank": t_roof_rank / ms},
+                    "ranks": per_rank}
         print(json.dumps({
             "metric": METRIC, "value": spec.T * args.steps / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "parallelism": f"kv-head tp{world}, all-gather fused into the epilogues (peer window)",
-                       "l2": "KV working set 2.7 GB total > L2"},
-            "gpu_launches": (hg.hg_last_plan_stats(wl.pool)["kernels"] + 2) * args.steps,  # + 2 barriers
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based N(0,1)-scale bf16 Q/K/V; fragmented block tables)",
+            "config": config_dict(spec, world),
+            "roofline": roofline,
+            "plan": st,
+            "gpu_launches": (st["kernels"] + 1) * args.steps,  # + the exit barrier (the entry one rides in the append)
             "e2e": {"value": spec.T * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2 * world,
                     "d2h_bytes_per_step": spec.T * spec.H_q * spec.d * 2, "ms_per_step": e2e_s / args.steps * 1e3,
@@ -967,7 +1036,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / len(times) * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "desc": WORKLOAD_DESC},
+        "config": config_dict(spec, world),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
                          "sample": "per step: the prefill request + 4 rotating decodes; " + base["sample"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -987,6 +1056,12 @@ def main():
     ap.add_argument("--sweep-iters", type=int, default=64, help="C4 iterations per (rho, chunk) point")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        port = os.environ.get("MASTER_PORT", "29533")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -317,10 +317,24 @@ HG_API hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, const h
  * validation with the append rules, one plan, one descriptor upload, the slots
  * derived on the device).  Same workspace, window and error rules as
  * hg_hybrid_attention_tp. */
+/* hg_hybrid_attention_tp with plan options (hg_attn_opts, nullable; events and
+ * the rope prologue do not apply).  With opts->split_tokens > 0 the plan is
+ * load-independent (reading R17): every rank's slice, and so the gathered O, is
+ * bit-identical to the unsharded call with the same split, whatever G. */
+HG_API hg_status hg_hybrid_attention_tp_ex(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
+                                           int32_t num_q_heads_total, const void *q_local, void *out_gathered,
+                                           void *workspace, size_t workspace_bytes, void *stream,
+                                           const hg_attn_opts *opts);
 HG_API hg_status hg_hybrid_step_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
                                    int32_t num_q_heads_total, const void *q_local, const void *k_new_local,
                                    const void *v_new_local, void *out_gathered, void *workspace,
                                    size_t workspace_bytes, void *stream);
+/* hg_hybrid_step_tp with plan options (nullable; per-kernel events recorded as
+ * in hg_hybrid_attention_ex, no rope: HG_E_INVALID). */
+HG_API hg_status hg_hybrid_step_tp_ex(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
+                                      int32_t num_q_heads_total, const void *q_local, const void *k_new_local,
+                                      const void *v_new_local, void *out_gathered, void *workspace,
+                                      size_t workspace_bytes, void *stream, const hg_attn_opts *opts);
 
 /* ------------------------------------------------------------------------ */
 /* Batch-latency predictor (§4.2 Eq. 1; App. B Eq. 2)  */

@@ -105,7 +105,9 @@ _SIGS = {
     "hg_hybrid_attention_tp_proj": ([P, P, P, i32, P, P, i32, P, P, ctypes.c_size_t, P], i32),
     "hg_hybrid_attention_tp_workspace_size": ([P, P, P, i32, P], i32),
     "hg_hybrid_attention_tp": ([P, P, P, i32, P, P, P, ctypes.c_size_t, P], i32),
+    "hg_hybrid_attention_tp_ex": ([P, P, P, i32, P, P, P, ctypes.c_size_t, P, P], i32),
     "hg_hybrid_step_tp": ([P, P, P, i32, P, P, P, P, P, ctypes.c_size_t, P], i32),
+    "hg_hybrid_step_tp_ex": ([P, P, P, i32, P, P, P, P, P, ctypes.c_size_t, P, P], i32),
     "hg_batch_features": ([P, i32, P], i32),
     "hg_predictor_fit": ([P, P, i32, i32, P], i32),
     "hg_predictor_predict": ([P, P], ctypes.c_double),
@@ -418,18 +420,27 @@ def hg_hybrid_attention_tp_workspace_size(pool: KVPool, comm: Comm, batch: Batch
 
 
 def hg_hybrid_attention_tp(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_total: int, q_local, out_gathered,
-                           workspace, stream=None) -> None:
-    _check(lib().hg_hybrid_attention_tp(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local),
-                                        _ptr(out_gathered), _ptr(workspace),
-                                        workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+                           workspace, stream=None, opts: Optional[hg_attn_opts] = None) -> None:
+    if opts is None:
+        _check(lib().hg_hybrid_attention_tp(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local),
+                                            _ptr(out_gathered), _ptr(workspace),
+                                            workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+    else:
+        _check(lib().hg_hybrid_attention_tp_ex(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local),
+                                               _ptr(out_gathered), _ptr(workspace),
+                                               workspace.numel() * workspace.element_size(), _stream_ptr(stream),
+                                               ctypes.byref(opts)))
 
 
 def hg_hybrid_step_tp(pool: KVPool, comm: Comm, batch: Batch, num_q_heads_total: int, q_local, k_new_local,
-                      v_new_local, out_gathered, workspace, stream=None) -> None:
+                      v_new_local, out_gathered, workspace, stream=None, opts: Optional[hg_attn_opts] = None) -> None:
     """Fused sharded step: append of this rank's KV-head slice + hg_hybrid_attention_tp."""
-    _check(lib().hg_hybrid_step_tp(pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local), _ptr(k_new_local),
-                                   _ptr(v_new_local), _ptr(out_gathered), _ptr(workspace),
-                                   workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+    args = (pool.h, comm.h, batch.ref(), num_q_heads_total, _ptr(q_local), _ptr(k_new_local), _ptr(v_new_local),
+            _ptr(out_gathered), _ptr(workspace), workspace.numel() * workspace.element_size(), _stream_ptr(stream))
+    if opts is None:
+        _check(lib().hg_hybrid_step_tp(*args))
+    else:
+        _check(lib().hg_hybrid_step_tp_ex(*args, ctypes.byref(opts)))
 
 
 def hg_out_proj_rs(comm: Comm, T: int, K: int, N: int, o_local, w_local, y_shard, stream=None) -> None:

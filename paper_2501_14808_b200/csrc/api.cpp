@@ -716,9 +716,10 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
 
 namespace hg {
 // Validate + plan once for a sharded call (pool->plan); the attention workspace bytes.
-hg_status plan_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, bool append, size_t *bytes) {
+hg_status plan_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, bool append, size_t *bytes,
+                         const hg_attn_opts *o) {
     BatchView v;
-    hg_status s = plan_call(pool, batch, H_q, nullptr, &v, &pool->plan, append);
+    hg_status s = plan_call(pool, batch, H_q, o, &v, &pool->plan, append);
     if (s) return s;
     *bytes = pool->plan.total_bytes;
     return HG_OK;
@@ -727,8 +728,8 @@ hg_status plan_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, b
 // pool->plan, O to every destination of `outs` (or to `out` when outs == NULL).
 hg_status attention_planned(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q,
                             const void *k_new, const void *v_new, void *out, const OutSpec *outs, void *ws,
-                            size_t ws_bytes, void *stream) {
-    return attention_impl(pool, batch, H_q, q, out, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                            size_t ws_bytes, void *stream, const hg_attn_opts *o) {
+    return attention_impl(pool, batch, H_q, q, out, nullptr, ws, ws_bytes, (cudaStream_t)stream, o,
                           k_new != nullptr, k_new, v_new, outs, nullptr, true);
 }
 hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,

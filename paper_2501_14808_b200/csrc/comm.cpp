@@ -188,12 +188,12 @@ extern "C" hg_status hg_hybrid_attention_tp_workspace_size(const hg_kv_pool *poo
 // per call; k_new != NULL fuses the append (this rank's KV-head slice).
 static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q, const void *q_local,
                          const void *k_new, const void *v_new, void *out_gathered, void *workspace,
-                         size_t workspace_bytes, void *stream) {
+                         size_t workspace_bytes, void *stream, const hg_attn_opts *o = nullptr) {
     if (!pool || !comm || !batch) return fail(HG_E_INVALID, "NULL argument");
     if (H_q % comm->world) return fail(HG_E_INVALID, "num_q_heads %d not divisible by world %d", H_q, comm->world);
     const int G = comm->world, Hl = H_q / G, d = pool_head_dim(pool);
     size_t attn = 0;
-    hg_status s = plan_attention(pool, batch, Hl, k_new != nullptr, &attn);
+    hg_status s = plan_attention(pool, batch, Hl, k_new != nullptr, &attn, o);
     if (s) return s;
     int64_t T = 0;
     for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
@@ -222,7 +222,7 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
             s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
             if (s) return s;
         }
-        s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream);
+        s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream, o);
         if (s) return s;
         s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
         if (s) return s;
@@ -241,7 +241,7 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
     const size_t count = (size_t)T * Hl * d;
     uint16_t *mine = gather + (size_t)comm->rank * count;
     if (T == 0) return HG_OK;
-    s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, mine, nullptr, workspace, attn, stream);
+    s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, mine, nullptr, workspace, attn, stream, o);
     if (s) return s;
     if (G > 1) {
         nccl_result r = g_nccl.AllGather(mine, gather, count, kNcclBf16, comm->comm, (cudaStream_t)stream);
@@ -258,12 +258,29 @@ extern "C" hg_status hg_hybrid_attention_tp(hg_kv_pool *pool, hg_comm *comm, con
                    stream);
 }
 
+extern "C" hg_status hg_hybrid_attention_tp_ex(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
+                                               const void *q_local, void *out_gathered, void *workspace,
+                                               size_t workspace_bytes, void *stream, const hg_attn_opts *opts) {
+    return tp_call(pool, comm, batch, H_q, q_local, nullptr, nullptr, out_gathered, workspace, workspace_bytes,
+                   stream, opts);
+}
+
 extern "C" hg_status hg_hybrid_step_tp(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
                                        const void *q_local, const void *k_new_local, const void *v_new_local,
                                        void *out_gathered, void *workspace, size_t workspace_bytes, void *stream) {
     if (!k_new_local || !v_new_local) return fail(HG_E_INVALID, "k_new / v_new NULL");
     return tp_call(pool, comm, batch, H_q, q_local, k_new_local, v_new_local, out_gathered, workspace,
                    workspace_bytes, stream);
+}
+
+extern "C" hg_status hg_hybrid_step_tp_ex(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch, int32_t H_q,
+                                          const void *q_local, const void *k_new_local, const void *v_new_local,
+                                          void *out_gathered, void *workspace, size_t workspace_bytes, void *stream,
+                                          const hg_attn_opts *opts) {
+    if (!k_new_local || !v_new_local) return fail(HG_E_INVALID, "k_new / v_new NULL");
+    if (opts && opts->rope) return fail(HG_E_INVALID, "the sharded step has no rope prologue");
+    return tp_call(pool, comm, batch, H_q, q_local, k_new_local, v_new_local, out_gathered, workspace,
+                   workspace_bytes, stream, opts);
 }
 
 // ---------------------------------------------------------------------------

@@ -172,10 +172,11 @@ struct OutSpec {
 };
 hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
                        void *ws, size_t ws_bytes, void *stream);
-hg_status plan_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, bool append, size_t *bytes);
+hg_status plan_attention(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, bool append, size_t *bytes,
+                         const hg_attn_opts *o = nullptr);
 hg_status attention_planned(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q,
                             const void *k_new, const void *v_new, void *out, const OutSpec *outs, void *ws,
-                            size_t ws_bytes, void *stream);
+                            size_t ws_bytes, void *stream, const hg_attn_opts *o = nullptr);
 
 // ---- kernel launchers (kernels.cu / tc_attn.cu) -----------------------------
 hg_status launch_append(const uint16_t *k_new, const uint16_t *v_new, uint16_t *k_cache,

@@ -42,7 +42,18 @@ def compare(spec, wl, req_sel=None, check_lse=True, tag=""):
     mx = np.abs(a - b).max()
     worst = max(np.linalg.norm(out[rows_of(spec, i)] - o_ref[rows_of(spec, i)]) /
                 np.linalg.norm(o_ref[rows_of(spec, i)]) for i in sel)
-    print(f"{spec.name}{tag}: rel-L2 {rel:.3e} max-abs {mx:.3e} worst-request rel-L2 {worst:.3e}")
+    # the share of max-abs that bf16 output rounding alone explains: the GPU's bf16 O
+    # against the oracle rounded to bf16 (RNE), i.e. the kernel's own error
+    b16 = torch.from_numpy(b).to(torch.bfloat16).double().numpy()
+    mx16 = np.abs(a - b16).max()
+    msg = (f"{spec.name}{tag}: rel-L2 {rel:.3e} max-abs {mx:.3e} (vs bf16(oracle) {mx16:.3e}) "
+           f"worst-request rel-L2 {worst:.3e} "
+           f"({'whole tensor' if req_sel is None else f'{len(sel)} requests'}, {len(idx)} rows)")
+    print(msg)
+    import os
+    if os.environ.get("HG_PARITY_LOG"):   # evidence log (profiles/), one line per comparison
+        with open(os.environ["HG_PARITY_LOG"], "a") as f:
+            f.write(msg + "\n")
     assert rel <= REL_L2 and mx <= MAX_ABS, (rel, mx)
     if check_lse:
         dl = np.abs(lse[idx] - lse_ref[idx]).max()
@@ -153,23 +164,17 @@ def test_shared_vs_private_copies():
     compare(priv, b)
 
 
-def _sample(spec, k=6):
-    """Requests checked at full size: every prefill request, plus decodes spread over the batch."""
-    pre = [i for i, r in enumerate(spec.requests) if r.n > 1]
-    dec = [i for i, r in enumerate(spec.requests) if r.n == 1]
-    step = max(1, len(dec) // k)
-    return sorted(set(pre + dec[::step][:k] + dec[-1:]))
-
-
-@pytest.mark.parametrize("name", ["c1", "c1_long", "c2", "c2_g8", "c2_none", "c3", "p1", "p2"])
-def test_full_size_sampled(name):
+@pytest.mark.parametrize("name", ["c1", "c1_long", "c2", "c2_g8", "c2_none", "c2_nested", "c3", "p1", "p2"])
+def test_full_size_whole_tensor(name):
+    """§8(c.1) acceptance at BASELINE.json's full sizes, in the launch
+    configuration bench.py times (the fused step): rel-L2 over the WHOLE output
+    tensor against the fp64 oracle, max-abs, LSE, and the worst single request."""
     from synth.configs import make_config
     spec = make_config(name, 0)
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    sel = _sample(spec) if name not in ("p1", "p2") else [0] if name == "p2" else [0, 3]
-    compare(spec, wl, req_sel=sel)
+    compare(spec, wl)
     wl.close()
 
 
@@ -223,7 +228,7 @@ def test_peaked(name, q_scale):
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    compare(spec, wl, req_sel=[1] if name == "p1" else [0] if name == "p2" else _sample(spec, 4))
+    compare(spec, wl)
     wl.close()
 
 
@@ -235,7 +240,7 @@ def test_full_size_second_seed(name):
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    compare(spec, wl, req_sel=_sample(spec, 4))
+    compare(spec, wl)
     wl.close()
 
 
@@ -251,9 +256,8 @@ def test_c2_shared_vs_private_full_size():
     d = (a.out.double() - b.out.double())
     assert d.abs().max().item() <= MAX_ABS
     assert (d.norm() / b.out.double().norm()).item() <= REL_L2
-    sel = _sample(a.spec, 4)
-    compare(a.spec, a, req_sel=sel)
-    compare(b.spec, b, req_sel=sel)
+    compare(a.spec, a)
+    compare(b.spec, b)
     a.close()
     b.close()
 
@@ -392,7 +396,7 @@ def test_shard_slices_full_size(name):
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    compare(spec, wl, req_sel=_sample(spec, 8))
+    compare(spec, wl)
     wl.close()
 
 
@@ -422,9 +426,7 @@ def test_max_context_16k():
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    compare(spec, wl, req_sel=[0, 2])
-    # the chunk: check its first and last rows through a reduced oracle request set
-    compare(spec, wl, req_sel=[1])
+    compare(spec, wl)
 
 
 @pytest.mark.parametrize("H_q,H_kv", [(64, 4), (12, 4), (40, 8), (16, 1), (32, 1), (64, 1), (64, 2), (48, 1)])
@@ -449,7 +451,7 @@ def test_head_dim_64_large_prefill():
     wl = make(spec)
     wl.step()
     torch.cuda.synchronize()
-    compare(spec, wl, req_sel=[0, 3, 8])
+    compare(spec, wl)
 
 
 def test_prefix_group_with_prefill_member():
@@ -562,7 +564,7 @@ def test_c2_nested_full_size():
     # Beside the (much longer) split-K pass the planner takes 256-row items: H_kv*(4 + 8)
     assert st["prefix_tiles"] == spec.H_kv * (1024 // 256 + 8), st
     assert st["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
-    compare(spec, wl, req_sel=_sample(spec, 10))
+    compare(spec, wl)
     wl.close()
 
 

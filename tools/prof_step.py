@@ -1,7 +1,9 @@
 """Device timeline of one hot-path step via torch.profiler (CUPTI): kernels and
 copies with their start offsets, to see where the non-kernel time goes.
 
-python tools/prof_step.py c1
+python tools/prof_step.py c1            # a BASELINE config
+python tools/prof_step.py c3@8          # rank 0's slice of 8-way KV-head sharding
+python tools/prof_step.py c4:219        # batch #219 of the C4 sweep
 """
 import os
 import sys
@@ -12,10 +14,19 @@ import torch
 from torch.profiler import ProfilerActivity, profile
 
 from paper_2501_14808_b200.harness import Workload
-from synth.configs import make_config
+from synth.configs import make_config, shard_slice
 
-import pickle
-spec = pickle.load(open(sys.argv[2], "rb")) if len(sys.argv) > 2 else make_config(sys.argv[1] if len(sys.argv) > 1 else "c1", 0)
+
+def spec_of(arg):
+    if arg.startswith("c4:"):
+        from synth.trace import c4_batch
+        return c4_batch(int(arg[3:]))
+    name, _, g = arg.partition("@")
+    spec = make_config(name, 0)
+    return shard_slice(spec, int(g)) if g else spec
+
+
+spec = spec_of(sys.argv[1] if len(sys.argv) > 1 else "c1")
 wl = Workload(spec)
 for _ in range(3):
     wl.step()

@@ -49,7 +49,7 @@ def config_dict(spec, world):
     return {"workload": WORKLOAD, "desc": WORKLOAD_DESC, "tokens_per_step": spec.T,
             "parallelism": "single GPU" if world == 1 else
             f"kv-head tp{world} (H_kv/{world} KV heads per rank), all-gather fused into the epilogues (peer window)",
-            "l2": "flushed (256 MB write) before every timed step, outside the events; KV working set 4.3 GB > L2"}
+            "l2": L2_FLUSH}
 
 
 def env_rank():
@@ -135,11 +135,38 @@ class ClockSampler:
                           "in a thread during the timed region"}
 
 
-def alg_bytes_splitk(spec):
-    """Algorithmic bytes of the split-K (decode) kernel per launch: the unique KV
-    tokens read by decode rows (4*d*H_kv per token: K+V bf16; a shared prefix
-    handled by the tcgen05 prefix pass is excluded) plus Q read and O written
-    (2*d*H_q each per decode row).  SURVEY.md §8(d) per-unit figures."""
+def timed_loop(step, steps, flush, stream, kernel_events):
+    """K back-to-back steps, L2 flushed before each outside its events; returns the
+    per-step device times (ms), the per-kernel events (if requested) and the host
+    time of each step call."""
+    import torch
+    import paper_2501_14808_b200 as hg
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(steps)] if kernel_events else None
+    kopts = [hg.make_opts(events=e) for e in kev] if kernel_events else [None] * steps   # (records the events once)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    host_s = []
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush_l2(flush)                     # L2 flushed between steps, outside the timed events
+        starts[k].record(stream)
+        h0 = time.perf_counter()
+        step(kopts[k])
+        host_s.append(time.perf_counter() - h0)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in zip(starts, ends)], kev, host_s
+
+
+def alg_bytes_splitk(spec, hbm_route=False):
+    """Algorithmic bytes of the split-K kernel per launch.  HBM route (no tcgen05
+    tiles: prefill rows and shared-prefix nodes run in split-K too): the whole
+    step's unique KV bytes plus Q and O (alg_bytes_total).  tcgen05 route: the
+    unique KV tokens read by decode rows (4*d*H_kv per token: K+V bf16; a shared
+    prefix handled by the tcgen05 prefix pass is excluded) plus Q read and O
+    written (2*d*H_q each per decode row).  SURVEY.md §8(d) per-unit figures."""
+    if hbm_route:
+        return alg_bytes_total(spec)
     d, Hk, Hq, B = spec.d, spec.H_kv, spec.H_q, spec.B
     kv_tok, rows = 0, 0
     groups = {}
@@ -177,8 +204,23 @@ def alg_flops(spec):
     return sum(4 * spec.d * spec.H_q * (r.n * r.c + r.n * (r.n + 1) // 2) for r in spec.requests)
 
 
+L2_FLUSH = ("flushed before every timed step, outside the events: 256 MB written, then another 256 MB read, "
+            "so L2 (126 MB) holds clean unrelated lines and no dirty write-back of the flush lands in the step; "
+            "KV working set > L2 as well")
+
+
+def flush_buffer(dev):
+    import torch
+    return torch.zeros(512 << 20, dtype=torch.uint8, device=dev)
+
+
 def flush_l2(buf):
-    buf.zero_()
+    """Evict L2: write 256 MB, then read the other 256 MB (the reads push the dirty
+    lines out during the flush, not during the timed step that follows)."""
+    import torch
+    half = buf.numel() // 2
+    buf[:half].zero_()
+    buf[half:].view(torch.int32).amax()
 
 
 def run_ours(args):
@@ -213,28 +255,19 @@ def run_ours(args):
 
     wl = Workload(spec, device=dev)
     stream = torch.cuda.current_stream(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = flush_buffer(dev)
     for _ in range(args.warmup):
         wl.step()
     torch.cuda.synchronize()
-    # one set of kernel events per step, created before the timed region, so steps
-    # are issued back to back: the host plans step k+1 while the GPU runs step k
-    # (the serving-engine overlap); per-step GPU time is read after the loop.
-    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
-    kopts = [hg.make_opts(events=e) for e in kev]
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    host_s = []
-    torch.cuda.synchronize()
+    # Two passes of K timed steps: the headline pass with only the step events (so
+    # the combine runs as a programmatic dependent launch right behind split-K),
+    # then a pass with the library's per-kernel events around every kernel (the
+    # dominant kernel's roofline; an event between two kernels breaks that PDL
+    # pairing, so this pass is a little slower).  Steps are issued back to back:
+    # the host plans step k+1 while the GPU runs step k (the serving-engine overlap).
     with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush_l2(flush)                     # L2 flushed between steps, outside the timed events
-            starts[k].record(stream)
-            h0 = time.perf_counter()
-            wl.step(kopts[k])
-            host_s.append(time.perf_counter() - h0)
-            ends[k].record(stream)
-        torch.cuda.synchronize()
+        step_ms, _, host_s = timed_loop(lambda o: wl.step(o), args.steps, flush, stream, False)
+    step_ms_ev, kev, _ = timed_loop(lambda o: wl.step(o), args.steps, flush, stream, True)
     # host cost of one call with the GPU idle (no staging-ring backpressure): validation,
     # plan, descriptor image, launches -- what a serving loop pays per step on the CPU
     host_idle = []
@@ -248,7 +281,6 @@ def run_ours(args):
     sk_ms = [e[2].elapsed_time(e[3]) for e in kev] if st["splitk_items"] else []
     tc_ms = [e[0].elapsed_time(e[1]) for e in kev] if st["tc_tiles"] else []
     cb_ms = [e[4].elapsed_time(e[5]) for e in kev] if st["combine_rows"] else []
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
     ms = total_ms / args.steps
     stats = hg.hg_last_plan_stats(wl.pool)
@@ -258,7 +290,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (split-K decode: HBM-bound)
     sk_avg = statistics.mean(sk_ms) if sk_ms else None
-    bytes_sk = alg_bytes_splitk(spec)
+    bytes_sk = alg_bytes_splitk(spec, hbm_route=not st["tc_tiles"])
     achieved = bytes_sk / (sk_avg / 1e3) / 1e9 if sk_avg else None
     traffic = load_traffic(f"splitk_kernel@{WORKLOAD}", bytes_sk)
     roofline = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": achieved, "peak": peaks["hbm_gbs"],
@@ -266,7 +298,9 @@ def run_ours(args):
                 "unit": "GB/s", "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
                 "traffic": traffic["bytes"] if traffic else None,   # DRAM read+write bytes per launch (ncu)
                 "traffic_detail": traffic, "alg_bytes_per_launch": bytes_sk, "avg_launch_ms": sk_avg,
-                "share_of_step": (sk_avg / ms) if sk_avg else None}
+                "share_of_step": (sk_avg / (sum(step_ms_ev) / args.steps)) if sk_avg else None,
+                "timing": "split-K events over a second pass of the same K timed steps (per-kernel events on)",
+                "ms_per_step_with_kernel_events": sum(step_ms_ev) / args.steps}
     # whole-step roofline (all kernels): t_roof = max(bytes/BW, flops/TC)
     bt, fl = alg_bytes_total(spec), alg_flops(spec)
     t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
@@ -289,10 +323,9 @@ def run_ours(args):
                          "gpu_idle": statistics.median(host_idle) * 1e3,
                          "note": "in_loop includes waiting for a free pinned staging slot (8-deep ring) "
                                  "while the GPU runs earlier steps; gpu_idle is the call's own CPU cost"},
-        "step_breakdown_ms": ({"start_to_splitk": statistics.median(s.elapsed_time(e[2]) for s, e in zip(starts, kev)),
-                               "splitk": statistics.median(sk_ms),
-                               "splitk_to_end": statistics.median(e[3].elapsed_time(x) for x, e in zip(ends, kev))}
-                              if sk_ms else None),
+        "kernel_ms_median": {"splitk": statistics.median(sk_ms) if sk_ms else None,
+                             "tc": statistics.median(tc_ms) if tc_ms else None,
+                             "combine": statistics.median(cb_ms) if cb_ms else None},
         "plan": stats,
         "append_and_attention_ms": split_calls,
         "gpu_launches": launches_per_step * args.steps,
@@ -349,7 +382,7 @@ def shard_projection(spec, dev, ms_step, peaks, reps=50):
     from paper_2501_14808_b200.harness import Workload
     from synth.configs import shard_slice
     out = {}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = flush_buffer(dev)
     base = None
     for G in (1, 2, 4, 8):
         if spec.H_kv % G:
@@ -491,7 +524,7 @@ def extra_configs(args, peaks, dev):
     for name in ("c1", "c2", "p1", "p2"):
         spec = make_config(name, 0)
         wl = Workload(spec, device=dev)
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        flush = flush_buffer(dev)
         for _ in range(3):
             wl.step()
         n = 10
@@ -500,7 +533,7 @@ def extra_configs(args, peaks, dev):
         se = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
         torch.cuda.synchronize()
         for k in range(n):
-            flush.zero_()
+            flush_l2(flush)
             se[k][0].record()
             wl.step(kopts[k])
             se[k][1].record()
@@ -538,7 +571,7 @@ def extra_configs(args, peaks, dev):
                                      "alg_flops_per_launch": fl, "avg_launch_ms": kms["tc"], "step_ms": m,
                                      "share_of_step": kms["tc"] / m}
         elif kms["splitk"]:
-            b_sk = alg_bytes_splitk(spec)
+            b_sk = alg_bytes_splitk(spec, hbm_route=not st["tc_tiles"])
             ach = b_sk / (kms["splitk"] / 1e3) / 1e9
             out[name]["roofline"] = {"bound": "hbm", "kernel": "splitk_kernel<128>", "achieved": ach,
                                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
@@ -575,7 +608,7 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
     kn = torch.randn((maxT, H[1], H[2]), device=dev).to(torch.bfloat16)
     vn = torch.randn((maxT, H[1], H[2]), device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = flush_buffer(dev)
     ws = None
     X, y, T, pre, stats = [], [], [], [], []
     for k, spec in enumerate(specs):
@@ -589,7 +622,7 @@ def predictor_sweep(dev, iters=64, reps=5, shape="llama3-8b", seed=0):
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(reps)]
         ops = [hg.make_opts(events=e) for e in evs]
         for r in range(reps):
-            flush.zero_()
+            flush_l2(flush)
             hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, ops[r])
         torch.cuda.synchronize()
         st = hg.hg_last_plan_stats(pool)
@@ -666,7 +699,7 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
     pool = hg.KVPool(kc, vc, N, B, H[1], H[2], dev.index)
     q = torch.randn((4096, H[0], H[2]), device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = flush_buffer(dev)
     ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     online, offline = [], []   # [prompt, output, done_prompt, done_out, group, prefix]
     obs_x, obs_y, refits, first_refit = [], [], 0, None
@@ -715,7 +748,7 @@ def slo_loop(dev, model, budget_ms=0.25, chunk=512, iters=300, seed=0, H=(32, 8,
         b = hg.Batch(lay.block_table, [x.c for x in reqs], [x.n for x in reqs], None, lay.shared)
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(5)]
         for ev in evs:   # median of 5 L2-flushed runs of the composed batch (as the C4 sweep's target)
-            flush.zero_()
+            flush_l2(flush)
             hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, hg.make_opts(events=ev))
         torch.cuda.synchronize()
         st = hg.hg_last_plan_stats(pool)
@@ -857,7 +890,7 @@ def psm_vs_fcfs(dev, groups=64, per_group=32, batch=128, H=(32, 8, 128), seed=0)
     q = torch.randn((batch, H[0], H[2]), device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
     ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = flush_buffer(dev)
     res = {}
     for name, order in (("fcfs", arrival), ("psm", psm_order)):
         tot_ms, tot_tok, uniq = 0.0, 0, 0
@@ -873,7 +906,7 @@ def psm_vs_fcfs(dev, groups=64, per_group=32, batch=128, H=(32, 8, 128), seed=0)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             times = []
             for rep in range(3):
-                flush.zero_()
+                flush_l2(flush)
                 hg.hg_hybrid_attention(pool, b, H[0], q, out, None, ws, None, hg.make_opts(events=ev))
                 torch.cuda.synchronize()
                 st = hg.hg_last_plan_stats(pool)
@@ -917,7 +950,7 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q), dtype=torch.uint8,
                      device=dev)
     stream = torch.cuda.current_stream(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = flush_buffer(dev)
 
     def step(opts=None):   # the sharded serving step: append of this rank's K/V slice fused with the attention
         hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, wl.k_new, wl.v_new, out, ws, stream, opts)
@@ -925,21 +958,13 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
-    kopts = [hg.make_opts(events=e) for e in kev]
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     dist.barrier()
     with ClockSampler(dev.index) as clk:
-        for k in range(args.steps):
-            flush_l2(flush)                     # L2 flushed between steps, outside the timed events
-            starts[k].record(stream)
-            step(kopts[k])
-            ends[k].record(stream)
-        torch.cuda.synchronize()
+        step_ms, _, _ = timed_loop(step, args.steps, flush, stream, False)
+    dist.barrier()
+    _, kev, _ = timed_loop(step, args.steps, flush, stream, True)   # per-kernel events (roofline)
     dist.barrier()
     st = hg.hg_last_plan_stats(wl.pool)
-    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     sk_ms = [e[2].elapsed_time(e[3]) for e in kev] if st["splitk_items"] else []
     cdev = "cpu" if same_gpu else dev   # gloo (same-GPU functional test) reduces host tensors
     t = torch.tensor([sum(step_ms)], device=cdev)
@@ -947,7 +972,7 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     total_ms = t.item()
     # per-rank rooflines: this rank's split-K kernel and its whole step
     sk_avg = statistics.mean(sk_ms) if sk_ms else None
-    b_sk = alg_bytes_splitk(local)
+    b_sk = alg_bytes_splitk(local, hbm_route=not st["tc_tiles"])
     ach = b_sk / (sk_avg / 1e3) / 1e9 if sk_avg else None
     t_roof_rank = alg_bytes_total(local) / (peaks["hbm_gbs"] * 1e9) * 1e3
     mine = torch.tensor([ach or 0.0, sum(step_ms) / args.steps], device=cdev, dtype=torch.float64)

@@ -137,7 +137,8 @@ typedef struct {
                                    prefill key cuts are off in this mode);
                                    0: automatic (sized to fill the SMs) */
     int32_t disable_prefix_pass;/* 1: no shared-prefix group pass (shared blocks read per request) */
-    int32_t disable_tc;         /* 1: prefill rows also go through the split-K kernel (no tcgen05) */
+    int32_t disable_tc;         /* 1: no tcgen05 kernel at all (prefill rows on split-K; shared prefixes
+                                   as stacked-row split-K items when G_q <= 16) */
     int32_t num_sms;            /* 0: device SM count */
     void *events[6];            /* profiling: cudaEvent_t (or NULL) recorded on the stream right before /
                                    after the tcgen05 kernel [0,1], the split-K kernel [2,3] and the
@@ -152,6 +153,11 @@ typedef struct {
                                    the prefill items would fill < half the SMs, each chunk's cached keys
                                    are cut at KV-tile boundaries into ranges written as partials and
                                    merged by the combine kernel (small chunks at long contexts) */
+    int32_t route;              /* 0 (default): automatic -- the HBM route when the prefill work is small
+                                   next to the decode pass, else the tcgen05 route; 1: tcgen05 route
+                                   (prefill chunks and shared-prefix nodes on tcgen05 tiles); 2: HBM
+                                   route (everything on the split-K kernel, prefix nodes as stacked-row
+                                   split-K items; same as disable_tc for the prefill rows) */
 } hg_attn_opts;
 
 /* Bytes of device workspace hg_hybrid_attention needs for this batch. */
@@ -234,7 +240,8 @@ HG_API hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *out);
  * item, the key range [k0, k1) it attends there (causal cap applied) and the
  * partial index it writes (-1: the row's only range, written directly).
  * kind: 0 prefill tile (tcgen05), 1 shared-prefix node tile (tcgen05), 2
- * split-K item.  nparts: ranges the token's rows are merged from.  The ranges of
+ * split-K item, 3 shared-prefix node as a stacked-row split-K item (HBM
+ * route, see hg_attn_opts.route).  nparts: ranges the token's rows are merged from.  The ranges of
  * a row must tile [0, c_i + j + 1) exactly once -- the a.4 tile map, the split-K
  * plan and the prefill key cuts are checked that way.  Writes min(cap, total)
  * rows; *n_rows = total. */

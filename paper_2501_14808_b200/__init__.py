@@ -55,7 +55,7 @@ class hg_rope(ctypes.Structure):
 class hg_attn_opts(ctypes.Structure):
     _fields_ = [("split_tokens", i32), ("disable_prefix_pass", i32), ("disable_tc", i32), ("num_sms", i32),
                 ("events", P * 6), ("debug_trace", P), ("rope", ctypes.POINTER(hg_rope)),
-                ("disable_prefill_split", i32)]
+                ("disable_prefill_split", i32), ("route", i32)]
 
 
 class hg_plan_stats(ctypes.Structure):
@@ -262,11 +262,12 @@ def hg_hybrid_attention_workspace_size(pool: KVPool, batch: Batch, num_q_heads: 
 
 
 def make_opts(split_tokens=0, disable_prefix_pass=False, disable_tc=False, num_sms=0, events=None,
-              rope: Optional[hg_rope] = None, disable_prefill_split=False) -> hg_attn_opts:
+              rope: Optional[hg_rope] = None, disable_prefill_split=False, route=0) -> hg_attn_opts:
     """events: optional 6 torch.cuda.Event(enable_timing=True) (or None entries), see hg_attn_opts.
     rope: hg_rope applied in the hg_hybrid_step prologue (kept alive by the returned struct)."""
     o = hg_attn_opts(split_tokens, int(disable_prefix_pass), int(disable_tc), num_sms)
     o.disable_prefill_split = int(disable_prefill_split)
+    o.route = int(route)   # 0 automatic, 1 tcgen05 route, 2 HBM route
     if rope is not None:
         o._rope_ref = rope
         o.rope = ctypes.pointer(rope)

@@ -49,8 +49,22 @@ struct hg_kv_pool {
     // the prefill wave's tcgen05 stream (highest priority) with its done events
     cudaStream_t h2d = nullptr, side_hi = nullptr;
     cudaEvent_t ev_in0 = nullptr, ev_in1 = nullptr, ev_tc = nullptr, ev_d2h = nullptr;
-    // fused step: the append runs on `side` while the descriptors upload on the caller's stream
+    // fused step: the append runs on `side` while the descriptors upload
     cudaEvent_t ev_pre = nullptr, ev_app = nullptr;
+    // Device descriptor slots (library-owned): a call's descriptor image goes up on
+    // the copy stream `cp`, which waits only for the kernels of the call that last
+    // used the slot -- not for the caller's queued work -- so the upload of step
+    // k+1 overlaps step k's kernels (the host plans ahead of the GPU).
+    struct DSlot {
+        void *dev = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ready = nullptr, done = nullptr;
+        bool used = false;
+    };
+    static constexpr int kDRing = 4;
+    DSlot dring[kDRing];
+    int dpos = 0;
+    cudaStream_t cp = nullptr;
 };
 
 namespace hg {
@@ -105,6 +119,53 @@ static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t 
     return HG_OK;
 }
 
+// Upload a call's descriptor image into the next device slot on the copy stream
+// and make `st` wait for it.  The copy waits (on the GPU) only for the kernels
+// of the call that used the slot before; the caller records `done` after its
+// last kernel (DescDone).
+static hg_status stage_desc(hg_kv_pool *pool, const void *img, size_t bytes, cudaStream_t st, void **dev,
+                            hg_kv_pool::DSlot **slot) {
+    hg_status s = HG_OK;
+    if (!pool->cp) s = cuda_check(cudaStreamCreateWithFlags(&pool->cp, cudaStreamNonBlocking), "copy stream");
+    if (s) return s;
+    hg_kv_pool::DSlot &d = pool->dring[pool->dpos];
+    pool->dpos = (pool->dpos + 1) % hg_kv_pool::kDRing;
+    for (cudaEvent_t *e : {&d.ready, &d.done})
+        if (!*e && !s) s = cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event create");
+    if (s) return s;
+    if (d.cap < bytes) {
+        if (d.dev) {
+            if (d.used) cudaEventSynchronize(d.done);
+            cudaFree(d.dev);
+            d.dev = nullptr;
+            d.cap = 0;
+            d.used = false;
+        }
+        const size_t cap = std::max<size_t>(bytes * 3 / 2, 1 << 16);
+        s = cuda_check(cudaMalloc(&d.dev, cap), "cudaMalloc(descriptors)");
+        if (s) { d.dev = nullptr; return s; }
+        d.cap = cap;
+    }
+    if (d.used) s = cuda_check(cudaStreamWaitEvent(pool->cp, d.done, 0), "descriptor slot wait");
+    if (!s) s = stage_h2d(pool, d.dev, img, bytes, pool->cp);
+    if (!s) s = cuda_check(cudaEventRecord(d.ready, pool->cp), "descriptor ready record");
+    if (!s) s = cuda_check(cudaStreamWaitEvent(st, d.ready, 0), "descriptor ready wait");
+    if (s) return s;
+    *dev = d.dev;
+    *slot = &d;
+    return HG_OK;
+}
+
+// Records the slot's `done` on the caller's stream when the call's launches are
+// over (every kernel that reads the descriptors is ordered before it on `st`).
+struct DescDone {
+    hg_kv_pool::DSlot *slot = nullptr;
+    cudaStream_t st = nullptr;
+    ~DescDone() {
+        if (slot && cudaEventRecord(slot->done, st) == cudaSuccess) slot->used = true;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // pool + allocator
 // ---------------------------------------------------------------------------
@@ -149,6 +210,16 @@ extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
         }
     for (cudaEvent_t e : {p->ev_in0, p->ev_in1, p->ev_tc, p->ev_d2h, p->ev_pre, p->ev_app})
         if (e) cudaEventDestroy(e);
+    for (auto &d : p->dring) {
+        if (d.used) cudaEventSynchronize(d.done);
+        if (d.dev) cudaFree(d.dev);
+        for (cudaEvent_t e : {d.ready, d.done})
+            if (e) cudaEventDestroy(e);
+    }
+    if (p->cp) {
+        cudaStreamSynchronize(p->cp);
+        cudaStreamDestroy(p->cp);
+    }
     delete p;
     return HG_OK;
 }
@@ -401,6 +472,7 @@ static PlanOpts plan_opts(const hg_kv_pool *pool, const hg_attn_opts *o) {
         po.prefix_pass = !o->disable_prefix_pass;
         po.use_tc = !o->disable_tc;
         po.split_prefill = !o->disable_prefill_split;
+        po.route = o->route;
         if (o->num_sms > 0) po.num_sms = o->num_sms;
     }
     return po;
@@ -497,6 +569,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     put(plan.off_cbase, plan.tok.data(), sizeof(TokDev) * plan.tok.size());
     put(plan.off_comb, plan.comb.data(), sizeof(int32_t) * plan.comb.size());
     put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
+    put(plan.off_skoff, plan.sk_off.data(), sizeof(int32_t) * plan.sk_off.size());
     // Fused step (no rope, no host-step waves): the append takes its slots from
     // the kernel parameters and runs on the side stream while the descriptors
     // upload, instead of after them (the tiles and split-K wait for both).
@@ -527,6 +600,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             bar.bar_rank = outs->bar_rank;
             bar.bar_world = outs->bar_world;
             bar.bar_epoch = outs->bar_epoch;
+            bar.bar_done = outs->bar_mine + kBarDoneSlot;
         }
         if (!s) s = launch_append_param((const uint16_t *)k_new, (const uint16_t *)v_new,
                                         (uint16_t *)pool->desc.k_cache, (uint16_t *)pool->desc.v_cache,
@@ -535,9 +609,16 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (!s) s = cuda_check(cudaEventRecord(pool->ev_app, pool->side), "append record");
         if (s) return s;
     }
-    s = stage_h2d(pool, ws, img.data(), plan.desc_bytes, st);
+    void *dbase = nullptr;
+    DescDone desc_done;
+    desc_done.st = st;
+    s = stage_desc(pool, img.data(), plan.desc_bytes, st, &dbase, &desc_done.slot);
     if (s) return s;
-    if (param_append) {
+    // No tcgen05 items: split-K reads the new tokens' K/V from k_new / v_new, so it
+    // starts at once beside the append instead of after it (the call still ends
+    // after the append: st waits for it behind split-K).
+    const bool sk_early = param_append && plan.tc.empty() && !plan.sk.empty();
+    if (param_append && !sk_early) {
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
         if (s) return s;
     }
@@ -570,14 +651,17 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         p.out_ld = (int64_t)H_q * pool->desc.head_dim;
     }
     p.lse = lse;
-    p.reqs = (const ReqDev *)(w + plan.off_reqs);
-    p.bt_flat = (const int32_t *)(w + plan.off_bt);
-    p.sk = (const SkItem *)(w + plan.off_sk);
-    p.tc = (const TcItem *)(w + plan.off_tc);
-    p.tc_tok = (const int32_t *)(w + plan.off_rows);
-    p.tok = (const TokDev *)(w + plan.off_cbase);
-    p.comb = (const int32_t *)(w + plan.off_comb);
-    p.tc_off = (const int32_t *)(w + plan.off_tcoff);
+    const uint8_t *dsc = (const uint8_t *)dbase;
+    p.reqs = (const ReqDev *)(dsc + plan.off_reqs);
+    p.bt_flat = (const int32_t *)(dsc + plan.off_bt);
+    p.sk = (const SkItem *)(dsc + plan.off_sk);
+    p.tc = (const TcItem *)(dsc + plan.off_tc);
+    p.tc_tok = (const int32_t *)(dsc + plan.off_rows);
+    p.tok = (const TokDev *)(dsc + plan.off_cbase);
+    p.comb = (const int32_t *)(dsc + plan.off_comb);
+    p.tc_off = (const int32_t *)(dsc + plan.off_tcoff);
+    p.sk_off = (const int32_t *)(dsc + plan.off_skoff);
+    p.sk_ctas = (int32_t)plan.sk_off.size() - 1;
     p.part_o = (float *)(w + plan.off_part_o);
     p.part_lse = (float *)(w + plan.off_part_lse);
     p.H_q = H_q;
@@ -590,6 +674,11 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.tc_ctas = plan.tc_ctas;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.d));
     p.trace = o ? (long long *)o->debug_trace : nullptr;
+    if (sk_early) {
+        p.k_new = (const uint16_t *)k_new;
+        p.v_new = (const uint16_t *)v_new;
+        if (outs && outs->bar_world > 0) p.bar_done = outs->bar_mine + kBarDoneSlot;
+    }
     int kernels = 0;
     auto rec = [&](int k, cudaStream_t on) {
         if (o && o->events[k]) cudaEventRecord((cudaEvent_t)o->events[k], on);
@@ -633,7 +722,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         }
         hg_plan_stats &ls = pool->last;
         ls.tc_tiles = p.n_tc;
-        ls.prefix_tiles = plan.prefix_tiles;
+        ls.prefix_tiles = plan.prefix_tiles + plan.prefix_sk * p.H_kv;
         ls.splitk_items = p.n_sk * p.H_kv;
         ls.combine_rows = p.n_comb * p.H_kv;
         ls.kernels = kernels;
@@ -698,14 +787,20 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     }
     if (p.n_comb) {
         rec(4, st);
-        s = launch_combine(p, st);
+        // right behind split-K on the same stream: a programmatic dependent launch
+        // (resident early, waits for split-K's completion in griddepcontrol.wait)
+        s = launch_combine(p, st, sk_early);
         if (s) return s;
         rec(5, st);
         ++kernels;
     }
+    if (sk_early) {   // the call ends after the append that ran beside split-K
+        s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
+        if (s) return s;
+    }
     hg_plan_stats &ls = pool->last;
     ls.tc_tiles = p.n_tc;
-    ls.prefix_tiles = plan.prefix_tiles;
+    ls.prefix_tiles = plan.prefix_tiles + plan.prefix_sk * p.H_kv;
     ls.splitk_items = p.n_sk * p.H_kv;   // CTAs: items x KV heads
     ls.combine_rows = p.n_comb * p.H_kv; // (token, KV head) pairs
     ls.kernels = kernels;
@@ -777,6 +872,7 @@ extern "C" hg_status hg_plan_rows(const hg_batch *batch, int32_t H_q, int32_t H_
         po.split_tokens = o->split_tokens;
         po.prefix_pass = !o->disable_prefix_pass;
         po.split_prefill = !o->disable_prefill_split;
+        po.route = o->route;
         if (o->disable_tc) use_tc = 0;
     }
     po.use_tc = use_tc != 0;
@@ -800,7 +896,8 @@ extern "C" hg_status hg_plan_rows(const hg_batch *batch, int32_t H_q, int32_t H_
         for (int g = 0; g < H_kv; ++g)
             for (int r = 0; r < it.nrows; ++r) {   // the rows the kernel computes (SkItem stacking)
                 const int x = it.hl0 + r, j = it.j0 + x / G;
-                emit(rq.cu_q + j, g * G + x % G, it.k0, std::min(it.k1, rq.c + j + 1), it.part, 2);
+                if (it.mode) emit(plan.tc_tok[j], g * G + x % G, it.k0, it.k1, it.part, 3);   // prefix node
+                else emit(rq.cu_q + j, g * G + x % G, it.k0, std::min(it.k1, rq.c + j + 1), it.part, 2);
             }
     }
     *n_rows = n;
@@ -918,8 +1015,16 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
         if (early) cudaStreamSynchronize(pool->h2d);
         return e;
     };
-    // one validated plan for the whole step (attention_impl reuses pool->plan)
-    s = plan_call(pool, batch, H_q, nullptr, &v, &pool->plan, true);
+    // One validated plan for the whole step (attention_impl reuses pool->plan).  With
+    // both prefill chunks and decode rows the tcgen05 route is taken: its prefill
+    // tiles consume the second input wave on their own stream while split-K runs
+    // on the first, which hides most of the PCIe upload (the HBM route would put
+    // both waves' rows into one split-K launch behind the whole upload).
+    bool has_pre = false, has_dec = false;
+    for (int i = 0; rows_ok && i < v.R; ++i) (v.n[i] > 1 ? has_pre : has_dec) = true;
+    hg_attn_opts ho{};
+    ho.route = has_pre && has_dec ? 1 : 0;
+    s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan, true);
     if (s) return bail(s);
     if (T == 0) return HG_OK;
     const size_t attn = pool->plan.total_bytes;

@@ -64,7 +64,7 @@ using namespace hg;
 
 namespace hg {
 hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
-                              unsigned long long epoch, void *stream);
+                              unsigned long long epoch, void *stream, bool pdl = false);
 hg_status launch_out_proj(const uint16_t *o, const uint16_t *w, int M, int N, int K, int G, int rank, int rows_max,
                           uint16_t *const *dst, void *stream);
 hg_status launch_rs_reduce(const uint16_t *recv, uint16_t *y, int rows, int rows_max, int N, int G, void *stream);
@@ -224,7 +224,8 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
         }
         s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream, o);
         if (s) return s;
-        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
+        // exit barrier, resident behind the attention's last kernel (PDL)
+        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream, true);
         if (s) return s;
         uint8_t *data = comm->win + kWinHdr;
         if (out_gathered != data) {

@@ -40,6 +40,8 @@ struct SkItem {
     int32_t part;   // partial index for rows that are combined (-1: direct write)
     int32_t hl0;    // stacked-row offset inside token j0 (q-head-in-group of row 0)
     int32_t nrows;  // stacked rows (<= kSkRows)
+    int32_t mode;   // 0: rows of request `req` (causal); 1: prefix node -- member x / G_q is token
+                    // tc_tok[j0 + x / G_q], every row sees all of [k0, k1); `req` gives the block table
 };
 
 // Per batch token: where its partials live.  Partial slot of (token t, KV head
@@ -97,6 +99,8 @@ struct AttnParams {
     int32_t n_sk, n_tc, n_comb;
     int32_t tc_ctas;           // persistent tcgen05 grid (<= n_tc)
     const int32_t *tc_off;     // [tc_ctas + 1]: CTA b processes tc items [tc_off[b], tc_off[b+1])
+    int32_t sk_ctas;           // persistent split-K grid per KV head (grid = sk_ctas x H_kv)
+    const int32_t *sk_off;     // [sk_ctas + 1]: CTA b processes split-K items [sk_off[b], sk_off[b+1])
     float scale_log2;          // log2(e) / sqrt(d)
     // peer-window entry barrier folded into the fused step's append kernel (bar_world = 0: none)
     unsigned long long *bar_flags[kMaxOuts];
@@ -104,7 +108,15 @@ struct AttnParams {
     int32_t bar_rank, bar_world;
     unsigned long long bar_epoch;
     long long *trace;          // debug: per-event clock64 stamps of tcgen05 CTA 0 (NULL: off)
+    // Fused step with the append running beside split-K (no tcgen05 items): split-K
+    // reads the new tokens' K/V (positions [c_i, c_i + n_i)) from these inputs
+    // instead of the cache the append is still writing (NULL: everything from the cache).
+    const uint16_t *k_new, *v_new;
+    // ... and, in a sharded call, the append's entry barrier publishes bar_epoch here
+    // when it is through; split-K waits for it before its first peer-window store.
+    unsigned long long *bar_done;
 };
+constexpr int kBarDoneSlot = 64;   // u64 slot of the peer-window header holding bar_done
 
 // Host-side plan (a.1 + a.4): built per call, staged to the device.
 struct Plan {
@@ -117,17 +129,19 @@ struct Plan {
     std::vector<SkItem> sk_tmp;
     std::vector<TcItem> tc_tmp;
     std::vector<int32_t> tc_off;   // per-CTA item ranges of the persistent tcgen05 grid
+    std::vector<int32_t> sk_off;   // per-CTA item ranges of the persistent split-K grid (per KV head)
     std::vector<TokDev> tok;
     std::vector<int32_t> comb;
     int64_t n_slots = 0;
-    int32_t prefix_tiles = 0;
+    int32_t prefix_tiles = 0;   // tcgen05 prefix-node tiles (tcgen05 route)
+    int32_t prefix_sk = 0;      // prefix-node split-K items (HBM route; one CTA per KV head each)
     int64_t n_tc_prefill() const { return (int64_t)tc.size() - prefix_tiles; }   // mode-0 items
     int64_t kv_bytes_unique = 0;
     int64_t kv_bytes_read = 0;
     int32_t tc_ctas = 0;        // persistent tcgen05 grid chosen by the planner
     // device layout (byte offsets inside the workspace)
     size_t off_reqs = 0, off_bt = 0, off_sk = 0, off_tc = 0, off_rows = 0, off_cbase = 0,
-           off_comb = 0, off_tcoff = 0, off_qrot = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
+           off_comb = 0, off_tcoff = 0, off_skoff = 0, off_qrot = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
 };
 
 // ---- host helpers (host.cpp) ------------------------------------------------
@@ -154,6 +168,7 @@ struct PlanOpts {
     bool prefix_pass = true;
     bool use_tc = true;
     bool split_prefill = true;   // key-range cuts of long prefill items when the grid is sparse
+    int route = 0;               // 0 automatic, 1 tcgen05 route, 2 HBM route (everything on split-K)
     int num_sms = 148;
 };
 hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpts &o, Plan *p);
@@ -206,7 +221,8 @@ hg_status launch_rope_append(const uint16_t *k_new, const uint16_t *v_new, uint1
                              const int64_t *slot, const int32_t *pos, int T, int H_kv, int d, const RopeArgs &r,
                              void *stream);
 hg_status launch_splitk(const AttnParams &p, void *stream);
-hg_status launch_combine(const AttnParams &p, void *stream);
+// pdl: launched as a programmatic dependent of the kernel before it in `stream`
+hg_status launch_combine(const AttnParams &p, void *stream, bool pdl = false);
 hg_status launch_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v, void *stream);
 int tc_supported(int d);
 

@@ -266,6 +266,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->comb.clear();
     p->n_slots = 0;
     p->prefix_tiles = 0;
+    p->prefix_sk = 0;
     int64_t T = 0, nbt = 0;
     for (int i = 0; i < v.R; ++i) {
         p->reqs[i] = ReqDev{v.c[i], v.n[i], (int32_t)T, (int32_t)nbt};
@@ -299,7 +300,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     // hg_hybrid_attention allows c_i + 1 < s_i * B) stops its pass at the last
     // block it sees completely, and split-K covers the rest.
     auto pass_cols = [&](int i) { return std::min<int64_t>(v.s[i], ((int64_t)v.c[i] + 1) / B); };
-    if (o.prefix_pass && tc_ok) {
+    if (o.prefix_pass && (tc_ok || G <= kSkRows)) {
         for (int i = 0; i < v.R; ++i)
             if (v.n[i] == 1 && v.s[i] > 0) {
                 const int32_t *row = v.bt + (int64_t)i * v.W;
@@ -328,10 +329,44 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             sc.npre[i] = depth;
         }
     }
+    // ---- route: tcgen05 tiles for the prefill chunks and prefix nodes, or the
+    // HBM route (everything on the split-K kernel, prefix nodes as stacked-row
+    // split-K items).  Beside a decode pass the tcgen05 CTAs, which need whole
+    // SMs, either wait for split-K's CTAs to drain or starve on TMA loads queued
+    // behind its HBM traffic; when the prefill work is small next to the decode
+    // pass, folding it into the HBM-bound kernel is cheaper (measured: c1 / c3
+    // and their 8-way shards, tools/exp_shard.py), and split-K can then start
+    // beside the append (it reads this call's new K/V from the step's inputs).
+    bool tc_on = tc_ok && o.route != 2;
+    if (tc_on && o.route == 0) {
+        double dec_bytes = 0, pre_flops = 0;
+        for (int i = 0; i < v.R; ++i) {
+            if (v.n[i] == 1) dec_bytes += ((double)v.c[i] + 1 - (double)sc.pre_end[i] * B) * 4.0 * d * H_kv;
+            else pre_flops += 4.0 * d * H_q * v.n[i] * ((double)v.c[i] + (v.n[i] + 1) / 2.0);
+        }
+        // prefill rows on mma.sync split-K items at ~300 TFLOP/s vs the decode pass at ~6.5 TB/s
+        tc_on = !(dec_bytes > 0 && pre_flops / 300e12 < 0.5 * dec_bytes / 6.5e12);
+    }
+    if (!tc_on && !sc.nodes.empty()) {
+        // HBM route: a node pays for its extra partials (every member row gets merged)
+        // only when the members would re-read a large share of the KV bytes: a prefix
+        // re-read by its members mostly hits L2.  Measured: c2_nested (re-reads 40 %
+        // of its unique bytes) gains 1.5 % with the nodes, c2 (25 %) is even, c3
+        // (12 %) loses 2 %.  No stacked-row split-K items above 16 rows (G_q > 16).
+        double reread = 0, uniq = 0;
+        for (int i = 0; i < v.R; ++i) uniq += (double)v.c[i] + v.n[i] - (double)v.s[i] * B;
+        uniq += (double)sc.n_shared * B;
+        for (const Scratch::Node &nd : sc.nodes) reread += (double)(nd.nm - 1) * (nd.e - nd.a) * B;
+        if (G > kSkRows || (o.route == 0 && reread <= 0.25 * uniq)) {
+            std::fill(sc.pre_end.begin(), sc.pre_end.end(), 0);
+            std::fill(sc.npre.begin(), sc.npre.end(), 0);
+            sc.nodes.clear();
+        }
+    }
     // rows per tcgen05 CTA: 256 (two Q tiles sharing K/V, half the L2 traffic per
     // FLOP) when that still gives every SM a CTA, else 128 (more CTAs)
     int ipr = kTcRows;
-    if (tc_ok) {
+    if (tc_on) {
         int64_t n256 = 0;
         for (int i = 0; i < v.R; ++i)
             if (v.n[i] > 1) n256 += (int64_t)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows);
@@ -401,13 +436,13 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     int64_t kv_tok_read = 0;
 
     // ---- tcgen05 tiles: prefill chunks (n_i > 1), token-major stacking ----------
-    if (tc_ok) {
+    if (tc_on) {
         for (int i = 0; i < v.R; ++i) {
             if (v.n[i] <= 1) continue;
             const int rows = v.n[i] * G;
             // key-range cuts of request i (sc.np[i] > 1): multiples of kTcKeys inside
             // its first c_i keys, spreading the ~ceil((c_i + n_i) / 128) tiles evenly
-            int np = tc_ok ? sc.np[i] : 1;
+            int np = sc.np[i];
             int32_t cut[kMaxCuts + 1];
             if (np > 1) {
                 const int64_t nt = ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys), tc_full = v.c[i] / kTcKeys;
@@ -457,7 +492,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     const int tpi = std::max(1, kSkRows / G);
     int64_t total_keys = 0;
     for (int i = 0; i < v.R; ++i) {
-        if (tc_ok && v.n[i] > 1) continue;
+        if (tc_on && v.n[i] > 1) continue;
         const int ks = sc.pre_end[i] * B;
         for (int j0 = 0; j0 < v.n[i]; j0 += tpi) {
             const int nt = std::min(tpi, v.n[i] - j0);
@@ -466,41 +501,47 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             ch_list.push_back(ch);
         }
     }
-    int chunk_tok;
-    if (o.split_tokens > 0) {
-        chunk_tok = (o.split_tokens + B - 1) / B * B;
-    } else {
-        // ~one wave of split-K CTAs (3 resident per SM), LPT-ordered: fewer, longer
-        // pieces than 4 waves' worth mean fewer partials to write and merge (c1
-        // 0.451 -> 0.443 ms, its G = 8 shard 0.107 -> 0.099 ms; c2 / c3 within
-        // 0.5 %); small batches keep the 256-key floor.  HG_SK_WAVES: A/B knob.
-        static const int waves = getenv("HG_SK_WAVES") ? std::max(1, atoi(getenv("HG_SK_WAVES"))) : 1;
-        const int64_t target = (int64_t)o.num_sms * 3 * waves;
-        int64_t ct = (total_keys + target - 1) / std::max<int64_t>(target, 1);
-        ct = std::max<int64_t>(ct, 256);
-        chunk_tok = (int)((ct + B - 1) / B * B);
-    }
-    for (const Chunk &ch : ch_list) {
-        const int pre = sc.npre[ch.i];
-        const int pieces = std::max(1, ceil_div(ch.ke - ch.ks, chunk_tok));
-        const int nparts = pre + pieces;
-        if (nparts > 1) {
-            for (int jj = 0; jj < ch.nt; ++jj) {
-                const int t = p->reqs[ch.i].cu_q + ch.j0 + jj;
-                p->tok[t] = TokDev{(int32_t)p->n_slots, nparts, ch.i, 0};
-                p->n_slots += (int64_t)nparts * G * H_kv;
-                p->comb.push_back(t);
-            }
+    // Persistent split-K grid (per KV head): CTA b runs items [sk_off[b], sk_off[b+1]).
+    p->sk_off.assign(1, 0);
+    auto add_tok_slots = [&](const Chunk &ch, int nparts) {
+        if (nparts <= 1) return;
+        for (int jj = 0; jj < ch.nt; ++jj) {
+            const int t = p->reqs[ch.i].cu_q + ch.j0 + jj;
+            p->tok[t] = TokDev{(int32_t)p->n_slots, nparts, ch.i, 0};
+            p->n_slots += (int64_t)nparts * G * H_kv;
+            p->comb.push_back(t);
         }
-        for (int k = 0; k < pieces; ++k) {
-            const int k0 = ch.ks + k * chunk_tok;
-            const int k1 = std::min(ch.ke, k0 + chunk_tok);
-            // G_q > 16 (ch.nt == 1): the token's q heads in groups of 16 rows, each
-            // item re-reading the same key range (adjacent in the LPT order: L2 hits)
-            for (int h0 = 0; h0 < ch.nt * G; h0 += kSkRows)
-                p->sk.push_back(SkItem{ch.i, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1, h0,
-                                       std::min(kSkRows, ch.nt * G - h0)});
-            kv_tok_read += (int64_t)(k1 - k0) * H_kv * ((ch.nt * G + kSkRows - 1) / kSkRows);
+    };
+    {
+        int chunk_tok;
+        if (o.split_tokens > 0) {
+            chunk_tok = (o.split_tokens + B - 1) / B * B;
+        } else {
+            // ~one wave of split-K CTAs (3 resident per SM), LPT-ordered: fewer, longer
+            // pieces than 4 waves' worth mean fewer partials to write and merge (c1
+            // 0.451 -> 0.443 ms, its G = 8 shard 0.107 -> 0.099 ms; c2 / c3 within
+            // 0.5 %); small batches keep the 256-key floor.  HG_SK_WAVES: A/B knob.
+            static const int waves = getenv("HG_SK_WAVES") ? std::max(1, atoi(getenv("HG_SK_WAVES"))) : 1;
+            const int64_t target = (int64_t)o.num_sms * 3 * waves;
+            int64_t ct = (total_keys + target - 1) / std::max<int64_t>(target, 1);
+            ct = std::max<int64_t>(ct, 256);
+            chunk_tok = (int)((ct + B - 1) / B * B);
+        }
+        for (const Chunk &ch : ch_list) {
+            const int pre = sc.npre[ch.i];
+            const int pieces = std::max(1, ceil_div(ch.ke - ch.ks, chunk_tok));
+            const int nparts = pre + pieces;
+            add_tok_slots(ch, nparts);
+            for (int k = 0; k < pieces; ++k) {
+                const int k0 = ch.ks + k * chunk_tok;
+                const int k1 = std::min(ch.ke, k0 + chunk_tok);
+                // G_q > 16 (ch.nt == 1): the token's q heads in groups of 16 rows, each
+                // item re-reading the same key range (adjacent in the LPT order: L2 hits)
+                for (int h0 = 0; h0 < ch.nt * G; h0 += kSkRows)
+                    p->sk.push_back(SkItem{ch.i, ch.j0, ch.nt, k0, k1, nparts > 1 ? pre + k : -1, h0,
+                                           std::min(kSkRows, ch.nt * G - h0)});
+                kv_tok_read += (int64_t)(k1 - k0) * H_kv * ((ch.nt * G + kSkRows - 1) / kSkRows);
+            }
         }
     }
     // ---- prefix node tiles (partial `depth` of every member row): member-major stacking ----
@@ -522,6 +563,16 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         }
         for (const Scratch::Node &nd : sc.nodes) {
             const int rows = nd.nm * G;
+            if (!tc_on) {   // HBM route: 16-row split-K items over the node's keys (16 / G_q members each)
+                const int mpi = kSkRows / G;
+                for (int m0 = 0; m0 < nd.nm; m0 += mpi) {
+                    const int nmm = std::min(mpi, nd.nm - m0);
+                    p->sk.push_back(SkItem{nd.rep, nd.first + m0, nmm, nd.a * B, nd.e * B, nd.depth, 0, nmm * G, 1});
+                    kv_tok_read += (int64_t)(nd.e - nd.a) * B * H_kv;
+                    p->prefix_sk++;
+                }
+                continue;
+            }
             for (int g = 0; g < H_kv; ++g) {
                 for (int r0 = 0; r0 < rows; r0 += ipr) {
                     const int nr = std::min(ipr, rows - r0);
@@ -536,13 +587,15 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         }
     }
     p->kv_bytes_read = kv_tok_read * 4ll * d;
+    // split-K: LPT order, one item per CTA (the hardware places them as SMs free up)
+    lpt_sort(p->sk, p->sk_tmp);
+    for (size_t k = 1; k <= p->sk.size(); ++k) p->sk_off.push_back((int32_t)k);
     // Persistent tcgen05 grid: one CTA per SM at most (each needs the SM's whole
     // shared memory); items beyond that are processed in LPT order by the same
     // CTAs without re-initialising the pipeline.  (Confining the tiles to a few
     // SMs beside the HBM-bound split-K kernel was measured slower: their K/V
     // loads queue behind split-K's HBM traffic.)
     p->tc_ctas = std::min((int)p->tc.size(), o.num_sms);
-    lpt_sort(p->sk, p->sk_tmp);
     stream_sort(p->tc, p->tc_tmp);
     assign_tc(p);
 
@@ -556,8 +609,9 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->off_cbase = off; off = align_up(off + sizeof(TokDev) * p->tok.size(), 16);
     p->off_comb = off;  off = align_up(off + sizeof(int32_t) * p->comb.size(), 16);
     p->off_tcoff = off; off = align_up(off + sizeof(int32_t) * p->tc_off.size(), 16);
-    p->desc_bytes = off;
-    off = align_up(off, 256);
+    p->off_skoff = off; off = align_up(off + sizeof(int32_t) * p->sk_off.size(), 16);
+    p->desc_bytes = off;   // the descriptor image lives in a library-owned device slot (api.cpp stage_desc)
+    off = 0;               // the caller's workspace: partials and the rotated-Q copy only
     p->off_part_o = off;   off = align_up(off + sizeof(float) * (size_t)p->n_slots * d, 256);
     p->off_part_lse = off; off = align_up(off + sizeof(float) * (size_t)p->n_slots, 256);
     p->off_qrot = off;     off = align_up(off + (size_t)T * H_q * d * 2, 256);   // rotated Q (rope step)

@@ -78,6 +78,24 @@ __device__ __forceinline__ void peer_barrier_body(unsigned long long *const *fla
     }
 }
 
+// The entry barrier is through (every thread of warp 0 returned from its peer's
+// wait): publish the epoch for kernels running beside the append (bar_done).
+__device__ __forceinline__ void publish_barrier_done(unsigned long long *done, unsigned long long epoch) {
+    __syncwarp();
+    if (done && threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(done), "l"(epoch) : "memory");
+}
+
+// Wait until the entry barrier of this call is through (before a peer-window store).
+__device__ __forceinline__ void wait_barrier_done(const unsigned long long *done, unsigned long long epoch) {
+    unsigned long long v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(done) : "memory");
+        if (v >= epoch) break;
+        __nanosleep(128);
+    }
+}
+
 template <int PER>   // uint4 chunks of K (and of V) per thread
 __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict__ k_new,
                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_cache,
@@ -86,8 +104,10 @@ __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict
     const int t = blockIdx.x;
     // sharded fused step: CTA 0's first warp also runs the peer-window entry
     // barrier (the kernels after this one are the first to write peer windows)
-    if (p.bar_world > 0 && t == 0 && threadIdx.x < 32)
+    if (p.bar_world > 0 && t == 0 && threadIdx.x < 32) {
         peer_barrier_body(p.bar_flags, p.bar_mine, p.bar_rank, p.bar_world, p.bar_epoch, threadIdx.x);
+        publish_barrier_done(p.bar_done, p.bar_epoch);
+    }
     const int row_chunks = p.H_kv * chunks_per_row;   // uint4 chunks of one token's K (or V)
     const int64_t src0 = (int64_t)t * row_chunks;
     // the first batch of this token's K/V loads goes out before the descriptor
@@ -145,6 +165,7 @@ struct BarrierArgs {   // peer-window entry barrier carried by the append (world
     unsigned long long *mine;
     int rank, world;
     unsigned long long epoch;
+    unsigned long long *done;   // NULL, or where to publish the epoch once through
 };
 
 template <int PER, int NS>
@@ -154,8 +175,10 @@ __global__ void __launch_bounds__(256) append_param_kernel(const uint4 *__restri
                                                            const __grid_constant__ SlotParams<NS> sp, int H_kv,
                                                            int chunks_per_row, const BarrierArgs ba) {
     const int t = blockIdx.x;
-    if (ba.world > 0 && t == 0 && threadIdx.x < 32)
+    if (ba.world > 0 && t == 0 && threadIdx.x < 32) {
         peer_barrier_body(ba.flags, ba.mine, ba.rank, ba.world, ba.epoch, threadIdx.x);
+        publish_barrier_done(ba.done, ba.epoch);
+    }
     const int row_chunks = H_kv * chunks_per_row;
     const int64_t src0 = (int64_t)t * row_chunks;
     const int64_t s = sp.slot[t];
@@ -205,6 +228,7 @@ hg_status launch_append_param(const uint16_t *k_new, const uint16_t *v_new, uint
         ba.rank = bar->bar_rank;
         ba.world = bar->bar_world;
         ba.epoch = bar->bar_epoch;
+        ba.done = bar->bar_done;
     }
     if (T == 0) return HG_OK;
     if (T > kParamSlots) return fail(HG_E_INVALID, "append_param: T %d > %d", T, kParamSlots);
@@ -410,16 +434,13 @@ struct SkSmem {
     static constexpr int kBytes = kQ + (kMain > kMerge ? kMain : kMerge);
 };
 
+// One split-K item (a piece of one row chunk's keys for KV head g) by the whole CTA.
 template <int D>
-__global__ void __launch_bounds__(kSkWarps * 32)
-splitk_kernel(const AttnParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
+__device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it, const int g, uint8_t *smem) {
     constexpr int NCH = D / 8;   // 16-byte chunks per row
     constexpr int NKS = D / 16;  // k-steps over the head dim
     constexpr int NNT = D / 8;   // n-tiles over the head dim (PV)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const SkItem it = p.sk[blockIdx.x];
-    const int g = blockIdx.y;   // KV head
     const ReqDev rq = p.reqs[it.req];
     const int G = p.G_q;
     const int nrows = it.nrows;   // stacked rows x = hl0 + r: token j0 + x / G, q head g*G + x % G
@@ -432,7 +453,7 @@ splitk_kernel(const AttnParams p) {
         uint4 val = make_uint4(0, 0, 0, 0);
         if (r < nrows) {
             const int x = it.hl0 + r;
-            const int t = rq.cu_q + it.j0 + x / G;
+            const int t = it.mode ? p.tc_tok[it.j0 + x / G] : rq.cu_q + it.j0 + x / G;
             const int h = g * G + x % G;
             val = *reinterpret_cast<const uint4 *>(p.q + ((int64_t)t * p.H_q + h) * D + ch * 8);
         }
@@ -442,6 +463,7 @@ splitk_kernel(const AttnParams p) {
     const int ra = lane >> 2, rb = ra + 8;
     auto row_lim = [&](int r) -> int {
         if (r >= nrows) return 0;
+        if (it.mode) return it.k1;   // a prefix node: every member sees all of its keys
         const int lim = rq.c + it.j0 + (it.hl0 + r) / G + 1;
         return lim < it.k1 ? lim : it.k1;
     };
@@ -462,6 +484,25 @@ splitk_kernel(const AttnParams p) {
         const uint16_t *gv = p.v_cache + base;
         const uint32_t dk = sW_u + stage * SkSmem<D>::kStage;
         const uint32_t dv = dk + SkSmem<D>::kTile;
+        if (p.k_new && (kb + 1) * kBlock > rq.c) {
+            // the block holds this call's new tokens: read them from the step's inputs
+            // (the append writing them into the cache runs beside this kernel)
+#pragma unroll
+            for (int i = 0; i < kBlock * NCH / 32; ++i) {
+                const int id = lane + 32 * i;
+                const int r = id / NCH, ch = id % NCH;
+                const int pos = kb * kBlock + r;
+                const uint16_t *sk = gk + r * D + ch * 8, *sv = gv + r * D + ch * 8;
+                if (pos >= rq.c && pos < rq.c + rq.n) {
+                    const int64_t off = ((int64_t)(rq.cu_q + pos - rq.c) * p.H_kv + g) * D + ch * 8;
+                    sk = p.k_new + off;
+                    sv = p.v_new + off;
+                }
+                cp_async16(dk + swz<D>(r, ch), sk);
+                cp_async16(dv + swz<D>(r, ch), sv);
+            }
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < kBlock * NCH / 32; ++i) {
             const int id = lane + 32 * i;
@@ -614,7 +655,7 @@ splitk_kernel(const AttnParams p) {
             }
             const float inv = L > 0.f ? 1.f / L : 0.f;
             const int x = it.hl0 + r;
-            const int t = rq.cu_q + it.j0 + x / G;
+            const int t = it.mode ? p.tc_tok[it.j0 + x / G] : rq.cu_q + it.j0 + x / G;
             const int h = g * G + x % G;
             int base = -1;
             if (it.part >= 0) {
@@ -634,6 +675,7 @@ splitk_kernel(const AttnParams p) {
             }
             const float lse2 = (L > 0.f) ? ref + __log2f(L) : -CUDART_INF_F;
             if (base < 0) {
+                if (p.bar_done) wait_barrier_done(p.bar_done, p.bar_epoch);   // peers' windows are free
                 const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + part8 * PER;
 #pragma unroll
                 for (int e = 0; e < PER; e += 8) {
@@ -657,6 +699,24 @@ splitk_kernel(const AttnParams p) {
     }
 }
 
+// Persistent split-K grid: CTA (b, g) runs the items [sk_off[b], sk_off[b+1]) for
+// KV head g (stream-K plans give every CTA the same number of KV blocks).
+template <int D>
+__global__ void __launch_bounds__(kSkWarps * 32, 3)   // 3 CTAs per SM: <= 170 registers
+splitk_kernel(const AttnParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    // the combine kernel behind this one (programmatic dependent launch) may be
+    // scheduled as soon as every CTA of this grid has started; it waits for this
+    // grid's completion in griddepcontrol.wait
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const int g = blockIdx.y;   // KV head
+    const int i0 = p.sk_off[blockIdx.x], i1 = p.sk_off[blockIdx.x + 1];
+    for (int i = i0; i < i1; ++i) {
+        if (i > i0) __syncthreads();   // the previous item's merge has read its smem
+        splitk_item<D>(p, p.sk[i], g, smem);
+    }
+}
+
 template <int D>
 static hg_status launch_splitk_d(const AttnParams &p, cudaStream_t st) {
     constexpr int bytes = SkSmem<D>::kBytes;
@@ -665,7 +725,7 @@ static hg_status launch_splitk_d(const AttnParams &p, cudaStream_t st) {
         cudaFuncSetAttribute(splitk_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         attr = true;
     }
-    splitk_kernel<D><<<dim3(p.n_sk, p.H_kv), kSkWarps * 32, bytes, st>>>(p);
+    splitk_kernel<D><<<dim3(p.sk_ctas, p.H_kv), kSkWarps * 32, bytes, st>>>(p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "split-K launch: %s", cudaGetErrorString(e));
 }
@@ -683,6 +743,10 @@ hg_status launch_splitk(const AttnParams &p, void *stream) {
 // ----------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
+    // launched as a programmatic dependent of split-K: resident early, reads the
+    // partials only once that grid has completed and its writes are visible
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int G = p.G_q;
@@ -738,6 +802,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
     uint32_t pk[PER / 2];
 #pragma unroll
     for (int e = 0; e < PER; e += 2) pk[e / 2] = pack_bf16(acc[e], acc[e + 1]);
+    if (p.bar_done) wait_barrier_done(p.bar_done, p.bar_epoch);   // peers' windows are free
     for (int k = 0; k < p.n_out; ++k) {
 #pragma unroll
         for (int e = 0; e < PER / 2; ++e) reinterpret_cast<uint32_t *>(p.outs[k] + off)[e] = pk[e];
@@ -746,14 +811,34 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
         p.lse[(int64_t)t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
 }
 
-hg_status launch_combine(const AttnParams &p, void *stream) {
+// Launch with the programmatic-stream-serialization attribute (pdl = true): the
+// kernel may start before the previous kernel in the stream has finished; it
+// must execute griddepcontrol.wait before touching that kernel's results.
+template <typename... Args>
+static cudaError_t launch_maybe_pdl(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                    bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+hg_status launch_combine(const AttnParams &p, void *stream, bool pdl) {
     if (p.n_comb == 0) return HG_OK;
     const int64_t warps = (int64_t)p.n_comb * p.H_kv * p.G_q;
     const int blocks = (int)((warps * 32 + 255) / 256);
-    if (p.d == 128) combine_kernel<128><<<blocks, 256, 0, (cudaStream_t)stream>>>(p);
-    else if (p.d == 64) combine_kernel<64><<<blocks, 256, 0, (cudaStream_t)stream>>>(p);
+    cudaError_t e;
+    if (p.d == 128) e = launch_maybe_pdl(combine_kernel<128>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, pdl, p);
+    else if (p.d == 64) e = launch_maybe_pdl(combine_kernel<64>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, pdl, p);
     else return fail(HG_E_UNSUPPORTED, "head_dim %d", p.d);
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "combine launch: %s", cudaGetErrorString(e));
 }
 
@@ -798,15 +883,19 @@ struct PeerFlags {
 
 __global__ void peer_barrier_kernel(PeerFlags pf, unsigned long long *mine, int rank, int world,
                                     unsigned long long epoch) {
+    // as a programmatic dependent of the attention's last kernel: resident early,
+    // the barrier starts once that kernel's peer stores are complete
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     peer_barrier_body(pf.flags, mine, rank, world, epoch, threadIdx.x);
 }
 
 hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
-                              unsigned long long epoch, void *stream) {
+                              unsigned long long epoch, void *stream, bool pdl) {
     PeerFlags pf{};
     for (int k = 0; k < world; ++k) pf.flags[k] = flags[k];
-    peer_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(pf, mine, rank, world, epoch);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_maybe_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, (cudaStream_t)stream, pdl, pf, mine,
+                                     rank, world, epoch);
+    if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "peer barrier launch: %s", cudaGetErrorString(e));
 }
 }  // namespace hg

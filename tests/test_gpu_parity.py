@@ -136,14 +136,15 @@ def test_fuzz(seed):
     compare(spec, wl)
 
 
-@pytest.mark.parametrize("variant", ["default", "no_tc", "split64", "no_prefix"])
+@pytest.mark.parametrize("variant", ["default", "no_tc", "split64", "no_prefix", "tc_route", "hbm_route"])
 @pytest.mark.parametrize("seed", range(8))
 def test_plan_variants(variant, seed):
     import paper_2501_14808_b200 as hg
     from synth.configs import make_fuzz
     spec = make_fuzz(100 + seed)
     opts = {"default": None, "no_tc": hg.make_opts(disable_tc=True), "split64": hg.make_opts(split_tokens=64),
-            "no_prefix": hg.make_opts(disable_prefix_pass=True)}[variant]
+            "no_prefix": hg.make_opts(disable_prefix_pass=True), "tc_route": hg.make_opts(route=1),
+            "hbm_route": hg.make_opts(route=2)}[variant]
     wl = make(spec)
     wl.append()
     wl.attention(opts)
@@ -323,10 +324,13 @@ def test_e2e_host_step_matches_device_path(name):
     oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16).pin_memory()
     ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
                      device="cuda")
+    # with both prefill chunks and decode rows the host step takes the tcgen05 route
+    # (its prefill tiles consume the second input wave): the same plan on the device path
+    mixed = any(r.n > 1 for r in spec.requests) and any(r.n == 1 for r in spec.requests)
     for rep in range(2):   # second call: events and streams reused
         hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
         k_after, v_after = wl.k_cache.clone(), wl.v_cache.clone()
-        wl.step()
+        wl.step(hg.make_opts(route=1) if mixed else None)
         torch.cuda.synchronize()
         assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), rep
         assert torch.equal(k_after, wl.k_cache) and torch.equal(v_after, wl.v_cache), rep
@@ -355,7 +359,7 @@ def test_e2e_host_step_errors_leave_outputs_untouched():
     torch.cuda.synchronize()
     assert torch.all(oh == 7.0) and torch.equal(k_before, wl.k_cache)
     hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)   # and the next valid call works
-    wl.step()
+    wl.step(hg.make_opts(route=1))   # toy_a is mixed: the host step's tcgen05 route
     torch.cuda.synchronize()
     assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16))
 
@@ -535,14 +539,15 @@ def test_nested_fuzz(seed):
     assert hg_stats(wl)["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
 
 
-@pytest.mark.parametrize("variant", ["no_tc", "no_prefix", "split64"])
+@pytest.mark.parametrize("variant", ["no_tc", "no_prefix", "split64", "tc_route", "hbm_route"])
 @pytest.mark.parametrize("seed", range(6))
 def test_nested_plan_variants(variant, seed):
     import paper_2501_14808_b200 as hg
     from synth.configs import make_fuzz_nested
     spec = make_fuzz_nested(100 + seed)
     opts = {"no_tc": hg.make_opts(disable_tc=True), "split64": hg.make_opts(split_tokens=64),
-            "no_prefix": hg.make_opts(disable_prefix_pass=True)}[variant]
+            "no_prefix": hg.make_opts(disable_prefix_pass=True), "tc_route": hg.make_opts(route=1),
+            "hbm_route": hg.make_opts(route=2)}[variant]
     wl = make(spec)
     wl.append()
     wl.attention(opts)
@@ -560,11 +565,19 @@ def test_c2_nested_full_size():
     wl.step()
     torch.cuda.synchronize()
     st = hg_stats(wl)
-    # root: 256 members x G_q=4 = 1024 stacked rows; children: 32 x 4 = 128 rows each.
-    # Beside the (much longer) split-K pass the planner takes 256-row items: H_kv*(4 + 8)
-    assert st["prefix_tiles"] == spec.H_kv * (1024 // 256 + 8), st
+    # HBM route (the decode pass dominates; members would re-read 40 % of the unique
+    # bytes, so the nodes stay): 16-row split-K items of 4 members x G_q=4:
+    # root 256 / 4 = 64 items, each child 32 / 4 = 8 -- per KV head
+    assert st["prefix_tiles"] == spec.H_kv * (256 // 4 + 8 * 32 // 4), st
     assert st["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
     compare(spec, wl)
+    # tcgen05 route: root 256 x 4 = 1024 stacked rows; children 32 x 4 = 128 rows each;
+    # beside the (much longer) split-K pass the planner takes 256-row items: H_kv*(4 + 8)
+    import paper_2501_14808_b200 as hg
+    wl.attention(hg.make_opts(route=1))
+    torch.cuda.synchronize()
+    assert hg_stats(wl)["prefix_tiles"] == spec.H_kv * (1024 // 256 + 8)
+    compare(spec, wl, tag=" (tcgen05 route)")
     wl.close()
 
 

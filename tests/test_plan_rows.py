@@ -190,4 +190,36 @@ def test_decode_row_ending_inside_a_shared_block():
         for i, r in enumerate(spec.requests):
             assert k1[t == i].max() == r.c + 1, (i, k1[t == i].max())
         # row 1 (c = 100) and row 2 (c = 47) still read blocks 5..7 once through a node
-        assert ((rows[:, 5] == 1) & (t == 1)).any()
+        assert (np.isin(rows[:, 5], (1, 3)) & (t == 1)).any()
+
+
+@pytest.mark.parametrize("route", [1, 2])
+@pytest.mark.parametrize("seed", range(20))
+def test_routes_tile_exactly(route, seed):
+    """Both routes (tcgen05 tiles, or everything on split-K with prefix nodes as
+    stacked-row split-K items) tile every row's keys exactly once."""
+    for make in (make_fuzz, make_fuzz_nested):
+        spec = make(seed)
+        lay = make_layout(spec, seed=seed)
+        rows = check_plan(spec, lay, opts=hg.make_opts(route=route))
+        kinds = set(np.unique(rows[:, 5]).tolist())
+        assert kinds <= ({0, 1, 2} if route == 1 else {2, 3})
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c2_nested"])
+def test_auto_route_takes_hbm_route_beside_a_large_decode_pass(name):
+    """The decode-dominated configs run on the HBM route (no tcgen05 items); on that
+    route a shared prefix is read once per 16-row node item where its re-reads would
+    be a large share of the bytes (c2_nested), else the members re-read it (L2)."""
+    spec = make_config(name, 0)
+    rows = check_plan(spec, make_layout(spec, seed=0))
+    assert not np.isin(rows[:, 5], (0, 1)).any()
+    # prefix nodes only where the members would re-read > 25 % of the unique KV bytes
+    assert (rows[:, 5] == 3).any() == (name == "c2_nested")
+
+
+@pytest.mark.parametrize("name", ["p1", "p2"])
+def test_auto_route_keeps_tcgen05_for_prefill_heavy(name):
+    spec = make_config(name, 0)
+    rows = check_plan(spec, make_layout(spec, seed=0))
+    assert (rows[:, 5] == 0).any()

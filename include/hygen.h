@@ -153,6 +153,9 @@ typedef struct {
                                    the prefill items would fill < half the SMs, each chunk's cached keys
                                    are cut at KV-tile boundaries into ranges written as partials and
                                    merged by the combine kernel (small chunks at long contexts) */
+    void *debug_sk_trace;       /* NULL, or device int64[2 * CTAs of the split-K grid]: %globaltimer (ns) at
+                                   each split-K CTA's start and end, CTA (x, g) at 2 * (g * grid.x + x)
+                                   (kernel development aid: the grid's occupancy over time) */
     int32_t route;              /* 0 (default): automatic -- the HBM route when the prefill work is small
                                    next to the decode pass, else the tcgen05 route; 1: tcgen05 route
                                    (prefill chunks and shared-prefix nodes on tcgen05 tiles); 2: HBM

@@ -55,7 +55,7 @@ class hg_rope(ctypes.Structure):
 class hg_attn_opts(ctypes.Structure):
     _fields_ = [("split_tokens", i32), ("disable_prefix_pass", i32), ("disable_tc", i32), ("num_sms", i32),
                 ("events", P * 6), ("debug_trace", P), ("rope", ctypes.POINTER(hg_rope)),
-                ("disable_prefill_split", i32), ("route", i32)]
+                ("disable_prefill_split", i32), ("debug_sk_trace", P), ("route", i32)]
 
 
 class hg_plan_stats(ctypes.Structure):

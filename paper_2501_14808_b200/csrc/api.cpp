@@ -65,6 +65,10 @@ struct hg_kv_pool {
     DSlot dring[kDRing];
     int dpos = 0;
     cudaStream_t cp = nullptr;
+    // fused append inside the tcgen05 kernel: device counter of finished shares and
+    // the host's running total of the shares launched (each call waits for its own)
+    unsigned long long *app_cnt = nullptr;
+    unsigned long long app_total = 0;
 };
 
 namespace hg {
@@ -220,6 +224,7 @@ extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
         cudaStreamSynchronize(p->cp);
         cudaStreamDestroy(p->cp);
     }
+    if (p->app_cnt) cudaFree(p->app_cnt);
     delete p;
     return HG_OK;
 }
@@ -574,7 +579,28 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     // the kernel parameters and runs on the side stream while the descriptors
     // upload, instead of after them (the tiles and split-K wait for both).
     static const bool no_param_append = getenv("HG_NO_PARAM_APPEND") != nullptr;   // A/B switch
-    const bool param_append = fused && !ra.rot && !pipe && plan.T <= kParamSlots && !no_param_append;
+    // tcgen05 route: the append runs inside the tcgen05 kernel's prologue, each CTA
+    // writing its share of the new tokens (<= ~256 KB of K+V per CTA), and a TMA
+    // producer waits only before the first tile holding new keys -- no append
+    // kernel and no launch in front of the tiles.  Not with the rope prologue or
+    // a peer-window entry barrier (those ride in the append kernel).
+    static const bool no_tc_append = getenv("HG_NO_TC_APPEND") != nullptr;   // A/B switch
+    const int64_t tc_grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)plan.tc.size(), plan.tc_ctas));
+    const bool tc_append = fused && !ra.rot && !pipe && !plan.tc.empty() && !(outs && outs->bar_world > 0) &&
+                           !no_tc_append &&
+                           (int64_t)plan.T * pool->desc.num_kv_heads * pool->desc.head_dim * 4 <= tc_grid * (256 << 10);
+    if (tc_append && !pool->app_cnt) {
+        s = cuda_check(cudaMalloc(&pool->app_cnt, 256), "cudaMalloc(append counter)");
+        if (!s) s = cuda_check(cudaMemset(pool->app_cnt, 0, 256), "memset(append counter)");
+        if (!s) s = cuda_check(cudaDeviceSynchronize(), "append counter init");
+        if (s) { if (pool->app_cnt) cudaFree(pool->app_cnt); pool->app_cnt = nullptr; return s; }
+        pool->app_total = 0;
+    }
+    const bool param_append = fused && !ra.rot && !pipe && !tc_append && plan.T <= kParamSlots && !no_param_append;
+    // No tcgen05 items: split-K reads the new tokens' K/V from k_new / v_new, so it
+    // starts at once beside the append instead of after it (the call still ends
+    // after the append: st waits for it behind split-K).
+    const bool sk_early = param_append && plan.tc.empty() && !plan.sk.empty();
     if (param_append) {
         s = ensure_side(pool);
         if (!s && !pool->ev_pre) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_pre, cudaEventDisableTiming), "event");
@@ -594,13 +620,12 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         s = cuda_check(cudaEventRecord(pool->ev_pre, st), "order record");   // after the caller's earlier work
         if (!s) s = cuda_check(cudaStreamWaitEvent(pool->side, pool->ev_pre, 0), "order wait");
         AttnParams bar{};   // a sharded call's peer-window entry barrier rides in this kernel
-        if (outs && outs->bar_world > 0) {
+        if (outs && outs->bar_world > 0 && !sk_early) {   // (beside split-K: its own kernel, see below)
             for (int k = 0; k < outs->bar_world; ++k) bar.bar_flags[k] = outs->bar_flags[k];
             bar.bar_mine = outs->bar_mine;
             bar.bar_rank = outs->bar_rank;
             bar.bar_world = outs->bar_world;
             bar.bar_epoch = outs->bar_epoch;
-            bar.bar_done = outs->bar_mine + kBarDoneSlot;
         }
         if (!s) s = launch_append_param((const uint16_t *)k_new, (const uint16_t *)v_new,
                                         (uint16_t *)pool->desc.k_cache, (uint16_t *)pool->desc.v_cache,
@@ -614,10 +639,6 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     desc_done.st = st;
     s = stage_desc(pool, img.data(), plan.desc_bytes, st, &dbase, &desc_done.slot);
     if (s) return s;
-    // No tcgen05 items: split-K reads the new tokens' K/V from k_new / v_new, so it
-    // starts at once beside the append instead of after it (the call still ends
-    // after the append: st waits for it behind split-K).
-    const bool sk_early = param_append && plan.tc.empty() && !plan.sk.empty();
     if (param_append && !sk_early) {
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
         if (s) return s;
@@ -674,10 +695,27 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.tc_ctas = plan.tc_ctas;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.d));
     p.trace = o ? (long long *)o->debug_trace : nullptr;
+    p.sk_trace = o ? (long long *)o->debug_sk_trace : nullptr;
     if (sk_early) {
         p.k_new = (const uint16_t *)k_new;
         p.v_new = (const uint16_t *)v_new;
-        if (outs && outs->bar_world > 0) p.bar_done = outs->bar_mine + kBarDoneSlot;
+        if (outs && outs->bar_world > 0) {
+            // sharded: the peer-window entry barrier as a 1-warp kernel right ahead of
+            // split-K, which is its programmatic dependent (launched at once, waiting
+            // for the barrier only before its first peer-window store)
+            s = launch_peer_barrier(outs->bar_flags, outs->bar_mine, outs->bar_rank, outs->bar_world,
+                                    outs->bar_epoch, st, false);
+            if (s) return s;
+            p.bar_pdl = 1;
+        }
+    }
+    if (tc_append) {   // the tcgen05 prologue appends; split-K reads the new keys from the inputs
+        p.k_new = (const uint16_t *)k_new;
+        p.v_new = (const uint16_t *)v_new;
+        p.app_T = plan.T;
+        p.app_cnt = pool->app_cnt;
+        pool->app_total += (unsigned long long)tc_grid;
+        p.app_target = pool->app_total;
     }
     int kernels = 0;
     auto rec = [&](int k, cudaStream_t on) {
@@ -740,11 +778,11 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             s = launch_rope_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, (const uint16_t *)q,
                                        q_rot, plan.T, ra, st);
             p.q = q_rot;
-        } else if (!param_append) {
+        } else if (!param_append && !tc_append) {
             s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st);
         }
         if (s) return s;
-        ++kernels;
+        if (!tc_append) ++kernels;
     }
     const bool overlap = p.n_tc && p.n_sk;
     cudaStream_t sk_stream = st;
@@ -915,11 +953,30 @@ extern "C" hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *o
 // ---------------------------------------------------------------------------
 static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
+// The host step's plan options: with both prefill chunks and decode rows, the
+// tcgen05 route (its prefill tiles consume the second input wave on their own
+// stream while split-K runs on the first, which hides most of the PCIe upload;
+// the HBM route would put both waves' rows into one split-K launch behind the
+// whole upload).
+static hg_attn_opts host_step_opts(const BatchView &v) {
+    bool has_pre = false, has_dec = false;
+    for (int i = 0; i < v.R; ++i) (v.n[i] > 1 ? has_pre : has_dec) = true;
+    hg_attn_opts ho{};
+    ho.route = has_pre && has_dec ? 1 : 0;
+    return ho;
+}
+
 extern "C" hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
                                                         int32_t H_q, size_t *bytes) {
-    size_t attn = 0;
-    hg_status s = hg_hybrid_attention_workspace_size(pool, batch, H_q, &attn);
+    if (!pool || !bytes) return fail(HG_E_INVALID, "NULL argument");
+    BatchView v;
+    hg_status s = view_batch(batch, &v);
     if (s) return s;
+    const hg_attn_opts ho = host_step_opts(v);
+    Plan plan;
+    s = plan_call(const_cast<hg_kv_pool *>(pool), batch, H_q, &ho, &v, &plan, true);
+    if (s) return s;
+    const size_t attn = plan.total_bytes;
     int64_t T = 0;
     for (int i = 0; i < batch->num_reqs; ++i) T += batch->new_len[i];
     const size_t d = pool->desc.head_dim, Hk = pool->desc.num_kv_heads;
@@ -1015,15 +1072,8 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
         if (early) cudaStreamSynchronize(pool->h2d);
         return e;
     };
-    // One validated plan for the whole step (attention_impl reuses pool->plan).  With
-    // both prefill chunks and decode rows the tcgen05 route is taken: its prefill
-    // tiles consume the second input wave on their own stream while split-K runs
-    // on the first, which hides most of the PCIe upload (the HBM route would put
-    // both waves' rows into one split-K launch behind the whole upload).
-    bool has_pre = false, has_dec = false;
-    for (int i = 0; rows_ok && i < v.R; ++i) (v.n[i] > 1 ? has_pre : has_dec) = true;
-    hg_attn_opts ho{};
-    ho.route = has_pre && has_dec ? 1 : 0;
+    // one validated plan for the whole step (attention_impl reuses pool->plan)
+    const hg_attn_opts ho = host_step_opts(v);
     s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan, true);
     if (s) return bail(s);
     if (T == 0) return HG_OK;

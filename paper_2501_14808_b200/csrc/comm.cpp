@@ -63,8 +63,6 @@ struct hg_comm {
 using namespace hg;
 
 namespace hg {
-hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
-                              unsigned long long epoch, void *stream, bool pdl = false);
 hg_status launch_out_proj(const uint16_t *o, const uint16_t *w, int M, int N, int K, int G, int rank, int rows_max,
                           uint16_t *const *dst, void *stream);
 hg_status launch_rs_reduce(const uint16_t *recv, uint16_t *y, int rows, int rows_max, int N, int G, void *stream);

@@ -71,6 +71,7 @@ struct TcItem {
     int32_t part;    // partial index (-1: rows written directly)
     int32_t pos0;    // mode 0: absolute position of token t0
     int32_t hl0;     // q-head-in-group of stacked row 0
+    int32_t cnew;    // first key position written by this call (c_i of the request; INT32_MAX: none)
 };
 
 // Device-side view of one attention call.
@@ -108,15 +109,24 @@ struct AttnParams {
     int32_t bar_rank, bar_world;
     unsigned long long bar_epoch;
     long long *trace;          // debug: per-event clock64 stamps of tcgen05 CTA 0 (NULL: off)
+    long long *sk_trace;       // debug: %globaltimer at each split-K CTA's start / end (NULL: off)
     // Fused step with the append running beside split-K (no tcgen05 items): split-K
     // reads the new tokens' K/V (positions [c_i, c_i + n_i)) from these inputs
     // instead of the cache the append is still writing (NULL: everything from the cache).
     const uint16_t *k_new, *v_new;
-    // ... and, in a sharded call, the append's entry barrier publishes bar_epoch here
-    // when it is through; split-K waits for it before its first peer-window store.
-    unsigned long long *bar_done;
+    // ... and, in a sharded call, split-K is a programmatic dependent of the
+    // peer-window entry barrier kernel: it waits for that grid (griddepcontrol.wait)
+    // before its first peer-window store and before it completes.
+    int32_t bar_pdl;
+    // Fused step on the tcgen05 route: the tcgen05 CTAs append this call's K/V
+    // (k_new / v_new, app_T tokens, split evenly over the grid) in their prologue
+    // and count themselves in app_cnt; a TMA producer waits for app_cnt >=
+    // app_target (every share written) before the first tile holding a new key.
+    // app_T = 0: the append ran as its own kernel before.
+    unsigned long long *app_cnt;
+    unsigned long long app_target;
+    int32_t app_T;
 };
-constexpr int kBarDoneSlot = 64;   // u64 slot of the peer-window header holding bar_done
 
 // Host-side plan (a.1 + a.4): built per call, staged to the device.
 struct Plan {
@@ -221,6 +231,8 @@ hg_status launch_rope_append(const uint16_t *k_new, const uint16_t *v_new, uint1
                              const int64_t *slot, const int32_t *pos, int T, int H_kv, int d, const RopeArgs &r,
                              void *stream);
 hg_status launch_splitk(const AttnParams &p, void *stream);
+hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
+                              unsigned long long epoch, void *stream, bool pdl = false);
 // pdl: launched as a programmatic dependent of the kernel before it in `stream`
 hg_status launch_combine(const AttnParams &p, void *stream, bool pdl = false);
 hg_status launch_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v, void *stream);

@@ -2,6 +2,7 @@
 // error reporting, batch validation (§8(b) rules), prefix groups, and the
 // per-call work plan consumed by the sm_100a kernels.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cmath>
 #include <cstdarg>
@@ -468,7 +469,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
                     const int nr = std::min(ipr, rows - r0);
                     const int j0 = r0 / G, j_last = (r0 + nr - 1) / G;
                     TcItem it{p->reqs[i].bt_off, g, 0, v.c[i] + j_last + 1, 0, p->reqs[i].cu_q + j0, nr, -1,
-                              v.c[i] + j0, r0 - j0 * G};
+                              v.c[i] + j0, r0 - j0 * G, v.c[i]};
                     kv_tok_read += it.k1;
                     if (np == 1) {
                         p->tc.push_back(it);
@@ -578,7 +579,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
                     const int nr = std::min(ipr, rows - r0);
                     const int m0 = r0 / G;
                     TcItem it{p->reqs[nd.rep].bt_off, g, nd.a * B, nd.e * B, 1, nd.first + m0, nr, nd.depth, 0,
-                              r0 - m0 * G};
+                              r0 - m0 * G, INT32_MAX};
                     kv_tok_read += (int64_t)(nd.e - nd.a) * B;
                     p->tc.push_back(it);
                     p->prefix_tiles++;

@@ -78,24 +78,6 @@ __device__ __forceinline__ void peer_barrier_body(unsigned long long *const *fla
     }
 }
 
-// The entry barrier is through (every thread of warp 0 returned from its peer's
-// wait): publish the epoch for kernels running beside the append (bar_done).
-__device__ __forceinline__ void publish_barrier_done(unsigned long long *done, unsigned long long epoch) {
-    __syncwarp();
-    if (done && threadIdx.x == 0)
-        asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(done), "l"(epoch) : "memory");
-}
-
-// Wait until the entry barrier of this call is through (before a peer-window store).
-__device__ __forceinline__ void wait_barrier_done(const unsigned long long *done, unsigned long long epoch) {
-    unsigned long long v;
-    for (;;) {
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(done) : "memory");
-        if (v >= epoch) break;
-        __nanosleep(128);
-    }
-}
-
 template <int PER>   // uint4 chunks of K (and of V) per thread
 __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict__ k_new,
                                                          const uint4 *__restrict__ v_new, uint4 *__restrict__ k_cache,
@@ -104,10 +86,8 @@ __global__ void __launch_bounds__(256) append_dev_kernel(const uint4 *__restrict
     const int t = blockIdx.x;
     // sharded fused step: CTA 0's first warp also runs the peer-window entry
     // barrier (the kernels after this one are the first to write peer windows)
-    if (p.bar_world > 0 && t == 0 && threadIdx.x < 32) {
+    if (p.bar_world > 0 && t == 0 && threadIdx.x < 32)
         peer_barrier_body(p.bar_flags, p.bar_mine, p.bar_rank, p.bar_world, p.bar_epoch, threadIdx.x);
-        publish_barrier_done(p.bar_done, p.bar_epoch);
-    }
     const int row_chunks = p.H_kv * chunks_per_row;   // uint4 chunks of one token's K (or V)
     const int64_t src0 = (int64_t)t * row_chunks;
     // the first batch of this token's K/V loads goes out before the descriptor
@@ -165,7 +145,6 @@ struct BarrierArgs {   // peer-window entry barrier carried by the append (world
     unsigned long long *mine;
     int rank, world;
     unsigned long long epoch;
-    unsigned long long *done;   // NULL, or where to publish the epoch once through
 };
 
 template <int PER, int NS>
@@ -175,10 +154,8 @@ __global__ void __launch_bounds__(256) append_param_kernel(const uint4 *__restri
                                                            const __grid_constant__ SlotParams<NS> sp, int H_kv,
                                                            int chunks_per_row, const BarrierArgs ba) {
     const int t = blockIdx.x;
-    if (ba.world > 0 && t == 0 && threadIdx.x < 32) {
+    if (ba.world > 0 && t == 0 && threadIdx.x < 32)
         peer_barrier_body(ba.flags, ba.mine, ba.rank, ba.world, ba.epoch, threadIdx.x);
-        publish_barrier_done(ba.done, ba.epoch);
-    }
     const int row_chunks = H_kv * chunks_per_row;
     const int64_t src0 = (int64_t)t * row_chunks;
     const int64_t s = sp.slot[t];
@@ -228,7 +205,6 @@ hg_status launch_append_param(const uint16_t *k_new, const uint16_t *v_new, uint
         ba.rank = bar->bar_rank;
         ba.world = bar->bar_world;
         ba.epoch = bar->bar_epoch;
-        ba.done = bar->bar_done;
     }
     if (T == 0) return HG_OK;
     if (T > kParamSlots) return fail(HG_E_INVALID, "append_param: T %d > %d", T, kParamSlots);
@@ -675,7 +651,9 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
             }
             const float lse2 = (L > 0.f) ? ref + __log2f(L) : -CUDART_INF_F;
             if (base < 0) {
-                if (p.bar_done) wait_barrier_done(p.bar_done, p.bar_epoch);   // peers' windows are free
+                // sharded call: the entry barrier kernel ahead of this grid (programmatic
+                // dependency) must be through before the first store into a peer's window
+                if (p.bar_pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
                 const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + part8 * PER;
 #pragma unroll
                 for (int e = 0; e < PER; e += 8) {
@@ -711,10 +689,38 @@ splitk_kernel(const AttnParams p) {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int g = blockIdx.y;   // KV head
     const int i0 = p.sk_off[blockIdx.x], i1 = p.sk_off[blockIdx.x + 1];
+    long long *tr = p.sk_trace ? p.sk_trace + 2 * ((int64_t)g * gridDim.x + blockIdx.x) : nullptr;
+    if (tr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(tr[0]));
     for (int i = i0; i < i1; ++i) {
         if (i > i0) __syncthreads();   // the previous item's merge has read its smem
         splitk_item<D>(p, p.sk[i], g, smem);
     }
+    if (tr) {
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(tr[1]));
+    }
+    // this grid completes only after the entry barrier ahead of it: the combine behind
+    // it (which waits for this grid) stores into peers' windows only after the barrier
+    if (p.bar_pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+// Launch with the programmatic-stream-serialization attribute (pdl = true): the
+// kernel may start before the previous kernel in the stream has finished; it
+// must execute griddepcontrol.wait before touching that kernel's results.
+template <typename... Args>
+static cudaError_t launch_maybe_pdl(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                    bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 template <int D>
@@ -725,8 +731,9 @@ static hg_status launch_splitk_d(const AttnParams &p, cudaStream_t st) {
         cudaFuncSetAttribute(splitk_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         attr = true;
     }
-    splitk_kernel<D><<<dim3(p.sk_ctas, p.H_kv), kSkWarps * 32, bytes, st>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_maybe_pdl(splitk_kernel<D>, dim3(p.sk_ctas, p.H_kv), dim3(kSkWarps * 32), (size_t)bytes, st,
+                                     p.bar_pdl != 0, p);
+    if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "split-K launch: %s", cudaGetErrorString(e));
 }
 
@@ -802,32 +809,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
     uint32_t pk[PER / 2];
 #pragma unroll
     for (int e = 0; e < PER; e += 2) pk[e / 2] = pack_bf16(acc[e], acc[e + 1]);
-    if (p.bar_done) wait_barrier_done(p.bar_done, p.bar_epoch);   // peers' windows are free
     for (int k = 0; k < p.n_out; ++k) {
 #pragma unroll
         for (int e = 0; e < PER / 2; ++e) reinterpret_cast<uint32_t *>(p.outs[k] + off)[e] = pk[e];
     }
     if (p.lse && lane == 0)
         p.lse[(int64_t)t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
-}
-
-// Launch with the programmatic-stream-serialization attribute (pdl = true): the
-// kernel may start before the previous kernel in the stream has finished; it
-// must execute griddepcontrol.wait before touching that kernel's results.
-template <typename... Args>
-static cudaError_t launch_maybe_pdl(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                                    bool pdl, Args... args) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 hg_status launch_combine(const AttnParams &p, void *stream, bool pdl) {
@@ -886,6 +873,9 @@ __global__ void peer_barrier_kernel(PeerFlags pf, unsigned long long *mine, int 
     // as a programmatic dependent of the attention's last kernel: resident early,
     // the barrier starts once that kernel's peer stores are complete
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    // as the entry barrier: the attention grid behind it may launch at once (it waits
+    // for this grid in griddepcontrol.wait before its first peer-window store)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     peer_barrier_body(pf.flags, mine, rank, world, epoch, threadIdx.x);
 }
 

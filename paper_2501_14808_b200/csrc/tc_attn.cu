@@ -234,6 +234,32 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
+    if (p.app_T > 0) {
+        // ---- fused append: this CTA's share of the call's new tokens -> paged cache ----
+        // (all 384 threads, 16-byte vectors; the slot of token t from the descriptors)
+        const int t0 = (int)((int64_t)p.app_T * blockIdx.x / gridDim.x);
+        const int t1 = (int)((int64_t)p.app_T * (blockIdx.x + 1) / gridDim.x);
+        const int cpr = D / 8, row = p.H_kv * cpr;   // uint4 chunks per head row / per token
+        const uint4 *kn = reinterpret_cast<const uint4 *>(p.k_new), *vn = reinterpret_cast<const uint4 *>(p.v_new);
+        uint4 *kc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.k_cache));
+        uint4 *vc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.v_cache));
+        for (int64_t idx = (int64_t)t0 * row + threadIdx.x; idx < (int64_t)t1 * row; idx += kTcThreads) {
+            const int t = (int)(idx / row), e = (int)(idx - (int64_t)t * row);
+            const TokDev tk = p.tok[t];
+            const ReqDev rq = p.reqs[tk.req];
+            const int pos = rq.c + (t - rq.cu_q);
+            const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
+            const int g = e / cpr, ch = e - g * cpr;
+            const int64_t dst = ((blk * p.H_kv + g) * kBlock + pos % kBlock) * cpr + ch;
+            kc[dst] = kn[idx];
+            vc[dst] = vn[idx];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {   // release: this share is in global memory
+            __threadfence();
+            atomicAdd(p.app_cnt, 1ull);
+        }
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -247,6 +273,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         // (separate threads so a V slot that is still busy never delays the next K load)
         if (lane == 0) {
             int64_t gn = 0;   // K (or V) tiles loaded by this CTA so far
+            bool appended = p.app_T == 0;   // every CTA's share of the fused append is in the cache
             for (int item = it_begin; item < it_end; ++item) {
                 const TcItem it = p.tc[item];
                 const int nkt = nkt_of(it);
@@ -254,6 +281,17 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 const int kb0 = it.k0 / kBlock;
                 const int kb_last = (it.k1 - 1) / kBlock;
                 for (int j = 0; j < nkt; ++j, ++gn) {
+                    if (!appended && it.k0 + (j + 1) * kTcKeys > it.cnew) {
+                        // the tile holds keys this call appends: wait for every CTA's share
+                        unsigned long long c;
+                        for (;;) {
+                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(c) : "l"(p.app_cnt) : "memory");
+                            if (c >= p.app_target) break;
+                            __nanosleep(64);
+                        }
+                        asm volatile("fence.proxy.async.global;\n" ::: "memory");   // before the TMA reads
+                        appended = true;
+                    }
                     int rows[8];
 #pragma unroll
                     for (int b = 0; b < 8; ++b) {

@@ -17,10 +17,15 @@ from synth.values import KIND_K, KIND_V, kv_values, q_values
 
 
 class Workload:
-    def __init__(self, spec, lay: Layout = None, device="cuda", populate=True, append_chunk_tokens=1 << 16):
+    def __init__(self, spec, lay: Layout = None, device="cuda", populate=True, append_chunk_tokens=1 << 16,
+                 gen_device=None):
+        """gen_device: where synth's generator runs (bit-identical on CPU and CUDA);
+        "cpu" makes the inputs with one host-to-device copy per tensor instead of
+        ~20 elementwise kernels each (smoke(): few launches besides the library's)."""
         self.spec = spec
         self.lay = lay or make_layout(spec)
         self.device = torch.device(device)
+        self.gen = torch.device(gen_device) if gen_device is not None else self.device
         N, H, d = self.lay.num_blocks, spec.H_kv, spec.d
         self.k_cache = torch.zeros((N, H, spec.B, d), dtype=torch.bfloat16, device=self.device)
         self.v_cache = torch.zeros((N, H, spec.B, d), dtype=torch.bfloat16, device=self.device)
@@ -29,7 +34,7 @@ class Workload:
         c = [r.c for r in spec.requests]
         n = [r.n for r in spec.requests]
         self.batch = hg.Batch(self.lay.block_table, c, n, [int(r.offline) for r in spec.requests], self.lay.shared)
-        self.q = q_values(spec, device=self.device)
+        self.q = q_values(spec, device=self.gen).to(self.device)
         self.k_new = self._kv_new(KIND_K)
         self.v_new = self._kv_new(KIND_V)
         T = spec.T
@@ -41,11 +46,11 @@ class Workload:
             self.populate()
 
     def _kv_new(self, kind):
-        parts = [kv_values(self.spec, i, r.c, r.c + r.n, kind, device=self.device)
+        parts = [kv_values(self.spec, i, r.c, r.c + r.n, kind, device=self.gen)
                  for i, r in enumerate(self.spec.requests)]
         if not parts:
             return torch.empty((0, self.spec.H_kv, self.spec.d), dtype=torch.bfloat16, device=self.device)
-        return torch.cat(parts)
+        return torch.cat(parts).to(self.device)
 
     def populate(self):
         """History appends: every request's first c_i tokens (group prefixes once)."""
@@ -59,10 +64,10 @@ class Workload:
                     tok += st.n[rows[end]]
                     end += 1
                 sel = rows[start:end]
-                ks = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_K, device=self.device)
-                                for k in sel])
-                vs = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_V, device=self.device)
-                                for k in sel])
+                ks = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_K, device=self.gen)
+                                for k in sel]).to(self.device)
+                vs = torch.cat([kv_values(spec, st.req[k], st.c[k], st.c[k] + st.n[k], KIND_V, device=self.gen)
+                                for k in sel]).to(self.device)
                 # rows list the blocks before their write position that are shared
                 shared = [st.shared[k] for k in sel]
                 b = hg.Batch(np.array([st.tables[k] for k in sel], np.int32), [st.c[k] for k in sel],
@@ -79,7 +84,7 @@ class Workload:
         more partial slots: 2x headroom; a too-small workspace is a loud HG_E_INVALID)."""
         if self.ws is None:
             need = hg.hg_hybrid_attention_workspace_size(self.pool, self.batch, self.spec.H_q)
-            self.ws = torch.empty(max(need, 1 << 20) * 2, dtype=torch.uint8, device=self.device)
+            self.ws = torch.empty(max(need * 2, need + (64 << 20)), dtype=torch.uint8, device=self.device)
         return self.ws
 
     def append(self, stream=None):

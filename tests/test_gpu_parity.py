@@ -502,13 +502,19 @@ def test_run_to_run_bitwise_and_fixed_split_head_sharding():
     assert torch.equal(sl.out.view(torch.int16), a[:, :half.H_q].contiguous().view(torch.int16))
 
 
-@pytest.mark.parametrize("name", ["toy_a", "c2_g8"])
-def test_fused_step_equals_append_then_attention(name):
+@pytest.mark.parametrize("name,route", [("toy_a", 0), ("c2_g8", 0), ("toy_a", 1), ("p1", 0), ("c1", 1)])
+def test_fused_step_equals_append_then_attention(name, route):
+    """The fused step -- HBM route: the append beside split-K, which reads the new
+    keys from the inputs; tcgen05 route: the append inside the tcgen05 kernel's
+    prologue -- leaves the same cache and output as hg_kv_append then
+    hg_hybrid_attention, bit for bit."""
+    import paper_2501_14808_b200 as hg
     from synth.configs import make_config
     spec = make_config(name, 1)
     a, b = make(spec), make(spec)
-    a.step()
-    b.step_unfused()
+    opts = hg.make_opts(route=route) if route else None
+    a.step(opts)
+    b.step_unfused(opts)
     torch.cuda.synchronize()
     assert torch.equal(a.out.view(torch.int16), b.out.view(torch.int16))
     assert torch.equal(a.k_cache.view(torch.int16), b.k_cache.view(torch.int16))

@@ -17,14 +17,14 @@ from synth.configs import make_config, shard_slice
 ap = argparse.ArgumentParser()
 ap.add_argument("config")
 ap.add_argument("--no-tc", action="store_true")
-ap.add_argument("--lpt", action="store_true")
+ap.add_argument("--route", type=int, default=0)
 ap.add_argument("--steps", type=int, default=3)
 a = ap.parse_args()
 name, _, g = a.config.partition("@")
 spec = make_config(name, 0)
 spec = shard_slice(spec, int(g)) if g else spec
 wl = Workload(spec)
-opts = hg.make_opts(disable_tc=a.no_tc, disable_stream_k=a.lpt)
+opts = hg.make_opts(disable_tc=a.no_tc, route=a.route)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(a.steps):
     flush.zero_()

@@ -52,6 +52,15 @@ def config_dict(spec, world):
             "l2": L2_FLUSH}
 
 
+_T0 = time.perf_counter()
+
+
+def progress(msg):
+    """Section timestamps on stderr (the JSON line alone goes to stdout): a stalled
+    section shows up in the log instead of as a silent timeout."""
+    print(f"[bench +{time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -253,6 +262,7 @@ def run_ours(args):
     if world > 1:
         return run_tp(args, spec, rank, world, dev, peaks, peak_kind)
 
+    progress(f"workload {WORKLOAD}")
     wl = Workload(spec, device=dev)
     stream = torch.cuda.current_stream(dev)
     flush = flush_buffer(dev)
@@ -265,6 +275,7 @@ def run_ours(args):
     # dominant kernel's roofline; an event between two kernels breaks that PDL
     # pairing, so this pass is a little slower).  Steps are issued back to back:
     # the host plans step k+1 while the GPU runs step k (the serving-engine overlap).
+    progress("warm-up done; timed steps")
     with ClockSampler(local) as clk:
         step_ms, _, host_s = timed_loop(lambda o: wl.step(o), args.steps, flush, stream, False)
     step_ms_ev, kev, _ = timed_loop(lambda o: wl.step(o), args.steps, flush, stream, True)
@@ -304,8 +315,10 @@ def run_ours(args):
     # whole-step roofline (all kernels): t_roof = max(bytes/BW, flops/TC)
     bt, fl = alg_bytes_total(spec), alg_flops(spec)
     t_roof = max(bt / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12))
+    progress("timed steps done; e2e")
     e2e = None if args.profile else measure_e2e(wl, spec, args, stream)
     split_calls = None if args.profile else measure_append_attention(wl, flush, stream)
+    progress("extra configs")
     extra = extra_configs(args, peaks, dev) if args.extra else None
     if extra:   # the tensor-bound (prefill-heavy) configs' rooflines, kept inside the roofline dict
         roofline["prefill_heavy"] = {k: v["roofline"] for k, v in extra.items() if k in ("p1", "p2")}
@@ -335,22 +348,29 @@ def run_ours(args):
     if extra:
         line["extra"] = extra
     if not args.profile and not args.no_predictor:
+        progress("predictor sweeps")
         pred = predictor_sweep(dev, iters=args.sweep_iters)
         model = pred.pop("_model")
         line["predictor"] = pred
         pred2 = predictor_sweep(dev, iters=args.sweep_iters, shape="llama2-7b")   # C4's second shape
         pred2.pop("_model")
         line["predictor_llama2_7b"] = pred2
+        progress("slo loops")
         line["slo_loop"] = slo_loop(dev, model)
         # the same loop with an online profiler refitting on its own observations
         line["slo_loop_online_refit"] = slo_loop(dev, model, refit_every=25)
+        progress("psm vs fcfs")
         line["psm_vs_fcfs"] = psm_vs_fcfs(dev)
     if args.extra:
+        progress("next4")
         line["next4"] = next4(dev, peaks)
         # the north_star's multi-GPU config (this line's workload): per-rank sharded step at G = 2/4/8
+        progress("shard projections")
         line["shard_projection_c3"] = shard_projection(spec, dev, ms, peaks)
         line["shard_projection_c1"] = shard_projection(make_config("c1", 0), dev, extra["c1"]["ms_per_step"], peaks)
+    progress("cpu baseline")
     line["cpu_baseline"] = None if args.profile else cpu_baseline(spec, wl)
+    progress("done")
     wl.close()
     print(json.dumps(line))
 
@@ -522,6 +542,7 @@ def extra_configs(args, peaks, dev):
     from synth.configs import make_config
     out = {}
     for name in ("c1", "c2", "p1", "p2"):
+        progress(f"extra {name}")
         spec = make_config(name, 0)
         wl = Workload(spec, device=dev)
         flush = flush_buffer(dev)

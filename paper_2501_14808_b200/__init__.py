@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libhygen.so")
+SO_PATH = os.environ.get("HG_SO_OVERRIDE") or os.path.join(_HERE, "libhygen.so")   # override: A/B variants
 
 HG_OK, HG_E_INVALID, HG_E_OOM, HG_E_SHARED_WRITE, HG_E_RANK_DEFICIENT, HG_E_CUDA, HG_E_NCCL, \
     HG_E_UNSUPPORTED = range(8)

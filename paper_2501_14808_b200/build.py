@@ -12,6 +12,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libhygen.so")
+# experiment variants (tools/gpurun A/B runs): HG_NVCC_DEFS="-DKNOB=..." HG_SO_OUT=build/var/x.so
+# builds a separate library; the binding loads it when HG_SO_OVERRIDE names it
+SO_OUT = os.environ.get("HG_SO_OUT")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -33,9 +36,10 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+    so = os.path.abspath(SO_OUT) if SO_OUT else SO
+    if not force and not SO_OUT and not needs_build():
         return SO
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" + ("_" + os.path.basename(so).replace(".", "_") if SO_OUT else ""))
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc")] + ARCH + \
@@ -59,10 +63,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(f"nvcc failed: {src}\n")
     if failed:
         raise RuntimeError("libhygen build failed")
-    tmp = SO + f".tmp{os.getpid()}"
+    os.makedirs(os.path.dirname(so), exist_ok=True)
+    tmp = so + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-ldl", "-lrt", "-lpthread"])
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

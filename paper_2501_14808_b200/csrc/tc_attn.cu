@@ -85,7 +85,16 @@ int tc_supported(int d) { return d == 128 || d == 64; }
 // ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-constexpr int kTcThreads = 384;  // WG0/WG1: softmax of Q tile 0/1; WG2: warp 8 TMA, warp 9 MMA, 10-11 idle
+constexpr int kTcThreads = 384;
+// Register split between the warpgroups (setmaxnreg; 2 x 128 x SOFTMAX + 128 x WG2 <= 384 x 168,
+// the launch allocation).  200 / 104: neither the softmax loop nor the MMA issuer spills.
+#ifndef HG_TC_REG_SOFTMAX
+#define HG_TC_REG_SOFTMAX 200
+#endif
+#ifndef HG_TC_REG_WG2
+#define HG_TC_REG_WG2 104
+#endif
+static_assert(2 * 128 * HG_TC_REG_SOFTMAX + 128 * HG_TC_REG_WG2 <= 384 * 168, "register split exceeds the launch allocation");  // WG0/WG1: softmax of Q tile 0/1; WG2: warp 8 TMA, warp 9 MMA, 10-11 idle
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values stay <= 2^8 between rescales
 
 // 2^x on the FMA/ALU pipes (offloads the MUFU unit): x = n + f, n = rint(x)
@@ -208,6 +217,11 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     // barrier phases come from running counters, so the pipelines never drain
     // between items.
     long long *tr = (blockIdx.x == 0) ? p.trace : nullptr;   // debug timeline of CTA 0's first item (NULL: off)
+    long long *trc = p.trace ? p.trace + 4096 + 4 * blockIdx.x : nullptr;   // per-CTA start / end (clock, ns)
+    if (trc && threadIdx.x == 0) {
+        trc[0] = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(trc[2]));
+    }
     const int it_begin = p.tc_off[blockIdx.x], it_end = p.tc_off[blockIdx.x + 1];
     auto nkt_of = [&](const TcItem &it) { return (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys; };
     auto ntiles_of = [&](const TcItem &it) { return it.nrows > kTcRows ? 2 : 1; };
@@ -239,20 +253,48 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         // (all 384 threads, 16-byte vectors; the slot of token t from the descriptors)
         const int t0 = (int)((int64_t)p.app_T * blockIdx.x / gridDim.x);
         const int t1 = (int)((int64_t)p.app_T * (blockIdx.x + 1) / gridDim.x);
-        const int cpr = D / 8, row = p.H_kv * cpr;   // uint4 chunks per head row / per token
-        const uint4 *kn = reinterpret_cast<const uint4 *>(p.k_new), *vn = reinterpret_cast<const uint4 *>(p.v_new);
+        constexpr int cpr = D / 8;                   // uint4 chunks per head row
+        const int row = p.H_kv * cpr;                // uint4 chunks per token (all KV heads)
+        const uint4 *kn = reinterpret_cast<const uint4 *>(p.k_new) + (int64_t)t0 * row;
+        const uint4 *vn = reinterpret_cast<const uint4 *>(p.v_new) + (int64_t)t0 * row;
         uint4 *kc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.k_cache));
         uint4 *vc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.v_cache));
-        for (int64_t idx = (int64_t)t0 * row + threadIdx.x; idx < (int64_t)t1 * row; idx += kTcThreads) {
-            const int t = (int)(idx / row), e = (int)(idx - (int64_t)t * row);
-            const TokDev tk = p.tok[t];
-            const ReqDev rq = p.reqs[tk.req];
+        // 1) each token's cache row base (the token -> request -> block id chain, once
+        //    per token) into smem; the K ring is unused until the producers start
+        int64_t *s_base = reinterpret_cast<int64_t *>(smem + L::oK);
+        const int ntok = t1 - t0;
+        for (int i = threadIdx.x; i < ntok; i += kTcThreads) {
+            const int t = t0 + i;
+            const ReqDev rq = p.reqs[p.tok[t].req];
             const int pos = rq.c + (t - rq.cu_q);
             const int64_t blk = p.bt_flat[rq.bt_off + pos / kBlock];
-            const int g = e / cpr, ch = e - g * cpr;
-            const int64_t dst = ((blk * p.H_kv + g) * kBlock + pos % kBlock) * cpr + ch;
-            kc[dst] = kn[idx];
-            vc[dst] = vn[idx];
+            s_base[i] = (blk * p.H_kv * kBlock + pos % kBlock) * cpr;   // + g * kBlock * cpr + chunk
+        }
+        __syncthreads();
+        // 2) the copy: 8 K and 8 V 16-byte loads in flight per thread before the stores
+        constexpr int U = 8;
+        const int64_t n = (int64_t)ntok * row;
+        for (int64_t b0 = threadIdx.x; b0 < n; b0 += (int64_t)kTcThreads * U) {
+            uint4 kv[U], vv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t idx = b0 + (int64_t)u * kTcThreads;
+                if (idx < n) {
+                    kv[u] = kn[idx];
+                    vv[u] = vn[idx];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t idx = b0 + (int64_t)u * kTcThreads;
+                if (idx < n) {
+                    const int i = (int)(idx / row), e = (int)(idx - (int64_t)i * row);
+                    const int g = e / cpr, ch = e % cpr;
+                    const int64_t dst = s_base[i] + (int64_t)g * kBlock * cpr + ch;
+                    kc[dst] = kv[u];
+                    vc[dst] = vv[u];
+                }
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {   // release: this share is in global memory
@@ -267,7 +309,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
 
     // register rebalance between warpgroups (setmaxnreg at the head of each role):
     // producers need few registers, a softmax thread holds a 128-column S row
-    if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(HG_TC_REG_WG2) : "memory");
     if (warp == 8 || warp == 10) {
         // ===================== TMA producers: warp 8 streams K, warp 10 streams V =====================
         // (separate threads so a V slot that is still busy never delays the next K load)
@@ -315,6 +357,9 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                         fb = bar(BAR_VFULL + st);
                         tm = &tmap_v;
                     }
+#ifdef HG_TC_NOLOAD   // A/B: after the rings' first fill, no K/V traffic (stale tiles; timing only)
+                    if (gn >= L::kKStages) { mbar_arrive(fb); continue; }
+#endif
                     mbar_expect_tx(fb, L::kKV);
 #pragma unroll
                     for (int b = 0; b < 8; ++b)
@@ -410,7 +455,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         }
     } else if (warp < 8) {
         // ===================== softmax / correction / epilogue (warps 0-7) =====================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(HG_TC_REG_SOFTMAX) : "memory");
         const int t = warp >> 2;             // Q tile of this warpgroup
         const int r = threadIdx.x & 127;     // row in the tile == TMEM lane
         const int rr = t * kTcRows + r;      // stacked row of the item
@@ -457,6 +502,11 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     mbar_wait(bar(BAR_SFULL + t), ss & 1);   // QK(t, j) and everything before it (PV(t, j-1)) done
                     if (trace && r == 0 && j < 64) tr[512 + 256 * t + 2 * j] = clock64();
                     tc_fence_after();
+#ifdef HG_TC_NOSOFTMAX   // A/B: no softmax work at all (the MMA + TMA pipeline alone; output wrong)
+                    mbar_arrive(bar(BAR_PHALF + t));
+                    mbar_arrive(bar(BAR_PFULL + t));
+                    continue;
+#endif
                     uint32_t sr[128];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) TMEM_LD32(tS + c * 32, (&sr[c * 32]));
@@ -610,6 +660,10 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     }
     tc_fence_before();
     __syncthreads();
+    if (trc && threadIdx.x == 0) {
+        trc[1] = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(trc[3]));
+    }
     if (warp == 9) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));

@@ -194,12 +194,17 @@ def test_ranks_same_gpu_peer_window(world, names, tmp_path):
     for p in ps:
         p.start()
     got = {}
-    for _ in ps:
-        rank, res, err = q.get(timeout=600)
-        assert err is None, f"rank {rank}:\n{err}"
-        got[rank] = res
-    for p in ps:
-        p.join(timeout=60)
+    try:
+        for _ in ps:
+            rank, res, err = q.get(timeout=600)
+            assert err is None, f"rank {rank}:\n{err}"
+            got[rank] = res
+    finally:   # a failed rank must not leave its peers spinning (pytest would wait on them at exit)
+        for p in ps:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+                p.join(timeout=10)
     for r in range(world):
         bad = [x for x in got[r] if not x[2]]
         assert not bad, (r, bad)

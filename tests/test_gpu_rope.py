@@ -42,11 +42,11 @@ def test_fuzz_rope(seed):
 
 
 @pytest.mark.parametrize("name", ["c1", "c1_long", "c2_nested"])
-def test_full_size_rope_sampled(name):
-    from test_gpu_parity import _sample
+def test_full_size_rope_whole_tensor(name):
+    """Full-size configs with the rope prologue: the whole output tensor against the oracle."""
     from synth.configs import make_config
     spec = make_config(name, 0).with_(rope=(5e5 if name == "c2_nested" else 1e4, 0))
-    wl = _run(spec, req_sel=_sample(spec, 4))
+    wl = _run(spec)
     wl.close()
 
 

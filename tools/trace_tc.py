@@ -25,3 +25,13 @@ print("softmax tile 0: S ready -> S loaded -> max/bump done -> first half exps d
 for j in range(0, 20):
     a = [t[512 + 2 * j]] + [t[2048 + 8 * j + k] for k in range(4)] + [t[512 + 2 * j + 1]]
     print(j, a, "deltas", [a[k + 1] - a[k] for k in range(5)])
+
+# per-CTA start / end (clock64, %globaltimer ns) of the whole grid
+c = tr.cpu().numpy()[4096:4096 + 4 * 148].reshape(-1, 4)
+c = c[c[:, 1] > 0]
+ns0 = c[:, 2].min()
+busy_ns = c[:, 3] - c[:, 2]
+mhz = (c[:, 1] - c[:, 0]) / np.maximum(busy_ns, 1) * 1e3
+print(f"grid: {len(c)} CTAs, makespan {(c[:, 3].max() - ns0) / 1e3:.1f} us, CTA busy min/median/max "
+      f"{busy_ns.min() / 1e3:.1f} / {np.median(busy_ns) / 1e3:.1f} / {busy_ns.max() / 1e3:.1f} us, "
+      f"start skew {(c[:, 2].max() - ns0) / 1e3:.1f} us, SM clock {np.median(mhz):.0f} MHz (min {mhz.min():.0f})")

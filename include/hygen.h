@@ -233,6 +233,9 @@ typedef struct {
     int32_t kernels;         /* kernels launched by the call */
     int64_t kv_bytes_unique; /* algorithmic KV bytes: 4*d*H_kv*U */
     int64_t kv_bytes_read;   /* KV bytes the plan streams from HBM */
+    int32_t append_mode;     /* fused step's append: 0 its own kernel (or none), 1 inside the
+                                tcgen05 kernel before its pipelines, 2 on the tcgen05 CTAs'
+                                idle warp in the background (hidden behind cached-prefix tiles) */
 } hg_plan_stats;
 HG_API hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *out);
 

@@ -60,7 +60,7 @@ class hg_attn_opts(ctypes.Structure):
 
 class hg_plan_stats(ctypes.Structure):
     _fields_ = [("tc_tiles", i32), ("prefix_tiles", i32), ("splitk_items", i32), ("combine_rows", i32),
-                ("kernels", i32), ("kv_bytes_unique", i64), ("kv_bytes_read", i64)]
+                ("kernels", i32), ("kv_bytes_unique", i64), ("kv_bytes_read", i64), ("append_mode", i32)]
 
 
 class hg_features(ctypes.Structure):

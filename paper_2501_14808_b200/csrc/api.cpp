@@ -562,6 +562,45 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (pipe && pipe->used)
             for (TokDev &tk : plan.tok) tk.wave = v.n[tk.req] > 1 ? 1 : 0;
     }
+    // tcgen05 route: the append runs inside the tcgen05 kernel, each CTA writing
+    // its share of the new tokens (<= ~256 KB of K+V per CTA), and a TMA producer
+    // waits only before the first tile holding new keys -- no append kernel and no
+    // launch in front of the tiles.  Not with the rope prologue or a peer-window
+    // entry barrier (those ride in the append kernel).
+    static const bool no_tc_append = getenv("HG_NO_TC_APPEND") != nullptr;   // A/B switch
+    static const bool no_bg_append = getenv("HG_NO_BG_APPEND") != nullptr;   // A/B switch
+    const int64_t tc_grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)plan.tc.size(), plan.tc_ctas));
+    const bool tc_append = fused && !ra.rot && !pipe && !plan.tc.empty() && !(outs && outs->bar_world > 0) &&
+                           !no_tc_append &&
+                           (int64_t)plan.T * pool->desc.num_kv_heads * pool->desc.head_dim * 4 <= tc_grid * (256 << 10);
+    // Where: in the prologue (all 384 threads, ~HBM rate, every pipeline waits for
+    // it) or in the background on each CTA's idle warp (~5 KB/us per CTA, hidden
+    // behind the cached-prefix tiles).  Each CTA's items are reordered so the one
+    // with the most cached-prefix tiles before its first new key comes first (the
+    // CTA's load is unchanged); background when, on every CTA, those tiles take
+    // longer than its share of the append.
+    bool app_bg = false;
+    if (tc_append && !no_bg_append && (int64_t)plan.tc_off.size() == tc_grid + 1) {
+        constexpr double kTileUs = 1.5, kBgBytesPerUs = 5.0e3, kSlackUs = 5.0;
+        auto lead_tiles = [](const TcItem &it) {
+            const int64_t nkt = (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys;
+            const int64_t before = it.cnew <= it.k0 ? 0 : (int64_t)(it.cnew - it.k0) / kTcKeys;
+            return std::min(nkt, before);
+        };
+        const double bg_us = 4.0 * plan.T * pool->desc.num_kv_heads * pool->desc.head_dim / tc_grid / kBgBytesPerUs;
+        app_bg = true;
+        for (int64_t b = 0; b < tc_grid && app_bg; ++b) {
+            TcItem *a = plan.tc.data() + plan.tc_off[b], *e = plan.tc.data() + plan.tc_off[b + 1];
+            std::stable_sort(a, e, [&](const TcItem &x, const TcItem &y) { return lead_tiles(x) > lead_tiles(y); });
+            double lead_us = 0;
+            for (TcItem *it = a; it < e; ++it) {
+                const int64_t nkt = (it->k1 - it->k0 + kTcKeys - 1) / kTcKeys, l = lead_tiles(*it);
+                lead_us += (double)l * kTileUs;
+                if (l < nkt) break;
+            }
+            app_bg = lead_us >= bg_us + kSlackUs;
+        }
+    }
     // one image of all descriptors -> one pinned H2D copy
     static thread_local std::vector<uint8_t> img;
     img.assign(plan.desc_bytes, 0);
@@ -579,16 +618,6 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     // the kernel parameters and runs on the side stream while the descriptors
     // upload, instead of after them (the tiles and split-K wait for both).
     static const bool no_param_append = getenv("HG_NO_PARAM_APPEND") != nullptr;   // A/B switch
-    // tcgen05 route: the append runs inside the tcgen05 kernel's prologue, each CTA
-    // writing its share of the new tokens (<= ~256 KB of K+V per CTA), and a TMA
-    // producer waits only before the first tile holding new keys -- no append
-    // kernel and no launch in front of the tiles.  Not with the rope prologue or
-    // a peer-window entry barrier (those ride in the append kernel).
-    static const bool no_tc_append = getenv("HG_NO_TC_APPEND") != nullptr;   // A/B switch
-    const int64_t tc_grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)plan.tc.size(), plan.tc_ctas));
-    const bool tc_append = fused && !ra.rot && !pipe && !plan.tc.empty() && !(outs && outs->bar_world > 0) &&
-                           !no_tc_append &&
-                           (int64_t)plan.T * pool->desc.num_kv_heads * pool->desc.head_dim * 4 <= tc_grid * (256 << 10);
     if (tc_append && !pool->app_cnt) {
         s = cuda_check(cudaMalloc(&pool->app_cnt, 256), "cudaMalloc(append counter)");
         if (!s) s = cuda_check(cudaMemset(pool->app_cnt, 0, 256), "memset(append counter)");
@@ -713,6 +742,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         p.k_new = (const uint16_t *)k_new;
         p.v_new = (const uint16_t *)v_new;
         p.app_T = plan.T;
+        p.app_bg = app_bg ? 1 : 0;
         p.app_cnt = pool->app_cnt;
         pool->app_total += (unsigned long long)tc_grid;
         p.app_target = pool->app_total;
@@ -766,6 +796,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         ls.kernels = kernels;
         ls.kv_bytes_unique = plan.kv_bytes_unique;
         ls.kv_bytes_read = plan.kv_bytes_read;
+        ls.append_mode = 0;   // two-wave step: the append kernels
         return HG_OK;
     }
     // The tcgen05 tiles (tensor-bound) and the split-K items (HBM-bound) are
@@ -844,6 +875,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     ls.kernels = kernels;
     ls.kv_bytes_unique = plan.kv_bytes_unique;
     ls.kv_bytes_read = plan.kv_bytes_read;
+    ls.append_mode = tc_append ? (app_bg ? 2 : 1) : 0;
     return HG_OK;
 }
 

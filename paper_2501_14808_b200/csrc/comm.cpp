@@ -223,8 +223,11 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
         s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream, o);
         if (s) return s;
         // exit barrier, resident behind the attention's last kernel (PDL)
-        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream, true);
-        if (s) return s;
+        static const bool no_exit = getenv("HG_TP_EXIT_SKIP") != nullptr;   // A/B (1 rank only): its cost
+        if (!(no_exit && G == 1)) {
+            s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream, true);
+            if (s) return s;
+        }
         uint8_t *data = comm->win + kWinHdr;
         if (out_gathered != data) {
             cudaError_t e = cudaMemcpyAsync(out_gathered, data, out_bytes, cudaMemcpyDeviceToDevice,

@@ -126,6 +126,10 @@ struct AttnParams {
     unsigned long long *app_cnt;
     unsigned long long app_target;
     int32_t app_T;
+    // app_bg = 1: the share is written by the CTA's idle warp 11 in the background
+    // while the pipelines run (the planner found every CTA's first new-key tile late
+    // enough to hide it); 0: by all 384 threads before the pipelines start.
+    int32_t app_bg;
 };
 
 // Host-side plan (a.1 + a.4): built per call, staged to the device.

@@ -248,7 +248,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    if (p.app_T > 0) {
+    if (p.app_T > 0 && !p.app_bg) {
         // ---- fused append: this CTA's share of the call's new tokens -> paged cache ----
         // (all 384 threads, 16-byte vectors; the slot of token t from the descriptors)
         const int t0 = (int)((int64_t)p.app_T * blockIdx.x / gridDim.x);
@@ -310,7 +310,50 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     // register rebalance between warpgroups (setmaxnreg at the head of each role):
     // producers need few registers, a softmax thread holds a 128-column S row
     if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(HG_TC_REG_WG2) : "memory");
-    if (warp == 8 || warp == 10) {
+    if (warp == 11 && p.app_T > 0 && p.app_bg) {
+        // ===================== background append (warp 11) =====================
+        // this CTA's share of the new tokens, token by token (the token -> request ->
+        // block chain once per token), 8 K and 8 V 16-byte loads in flight per lane;
+        // the TMA producers wait for every CTA's count before their first new-key tile
+        const int t0 = (int)((int64_t)p.app_T * blockIdx.x / gridDim.x);
+        const int t1 = (int)((int64_t)p.app_T * (blockIdx.x + 1) / gridDim.x);
+        constexpr int cpr = D / 8;
+        const int row = p.H_kv * cpr;
+        const uint4 *kn = reinterpret_cast<const uint4 *>(p.k_new), *vn = reinterpret_cast<const uint4 *>(p.v_new);
+        uint4 *kc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.k_cache));
+        uint4 *vc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.v_cache));
+        constexpr int U = 8;
+        for (int t = t0; t < t1; ++t) {
+            const ReqDev rq = p.reqs[p.tok[t].req];
+            const int pos = rq.c + (t - rq.cu_q);
+            const int64_t base = ((int64_t)p.bt_flat[rq.bt_off + pos / kBlock] * p.H_kv * kBlock + pos % kBlock) * cpr;
+            const int64_t src = (int64_t)t * row;
+            for (int e0 = lane; e0 < row; e0 += 32 * U) {
+                uint4 kv[U], vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + 32 * u;
+                    if (e < row) {
+                        kv[u] = kn[src + e];
+                        vv[u] = vn[src + e];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + 32 * u;
+                    if (e < row) {
+                        const int g = e / cpr, ch = e % cpr;
+                        const int64_t dst = base + (int64_t)g * kBlock * cpr + ch;
+                        kc[dst] = kv[u];
+                        vc[dst] = vv[u];
+                    }
+                }
+            }
+        }
+        __threadfence();   // every lane's stores, then one release count per CTA
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.app_cnt, 1ull);
+    } else if (warp == 8 || warp == 10) {
         // ===================== TMA producers: warp 8 streams K, warp 10 streams V =====================
         // (separate threads so a V slot that is still busy never delays the next K load)
         if (lane == 0) {

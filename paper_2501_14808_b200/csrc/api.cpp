@@ -630,6 +630,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     // starts at once beside the append instead of after it (the call still ends
     // after the append: st waits for it behind split-K).
     const bool sk_early = param_append && plan.tc.empty() && !plan.sk.empty();
+    static const bool no_app_count = getenv("HG_TP_APPEND_JOIN") != nullptr;   // A/B: stream join instead
     if (param_append) {
         s = ensure_side(pool);
         if (!s && !pool->ev_pre) s = cuda_check(cudaEventCreateWithFlags(&pool->ev_pre, cudaEventDisableTiming), "event");
@@ -655,6 +656,23 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             bar.bar_rank = outs->bar_rank;
             bar.bar_world = outs->bar_world;
             bar.bar_epoch = outs->bar_epoch;
+        }
+        if (outs && outs->bar_world > 0 && sk_early && !no_app_count) {
+            // sharded HBM route: no stream join for the append -- it counts its CTAs in a
+            // device counter and the caller's exit barrier kernel (a programmatic
+            // dependent of the combine) waits for the count instead, so no event wait
+            // sits between the last attention kernel and that barrier
+            if (!pool->app_cnt) {
+                s = cuda_check(cudaMalloc(&pool->app_cnt, 256), "cudaMalloc(append counter)");
+                if (!s) s = cuda_check(cudaMemset(pool->app_cnt, 0, 256), "memset(append counter)");
+                if (!s) s = cuda_check(cudaDeviceSynchronize(), "append counter init");
+                if (s) { if (pool->app_cnt) cudaFree(pool->app_cnt); pool->app_cnt = nullptr; return s; }
+                pool->app_total = 0;
+            }
+            bar.app_cnt = pool->app_cnt;
+            pool->app_total += (unsigned long long)plan.T;   // one CTA per token
+            outs->wait_cnt = pool->app_cnt;
+            outs->wait_target = pool->app_total;
         }
         if (!s) s = launch_append_param((const uint16_t *)k_new, (const uint16_t *)v_new,
                                         (uint16_t *)pool->desc.k_cache, (uint16_t *)pool->desc.v_cache,
@@ -863,7 +881,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         rec(5, st);
         ++kernels;
     }
-    if (sk_early) {   // the call ends after the append that ran beside split-K
+    if (sk_early && !(outs && outs->wait_cnt)) {   // the call ends after the append that ran beside split-K
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
         if (s) return s;
     }

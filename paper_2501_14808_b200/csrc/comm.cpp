@@ -222,12 +222,12 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
         }
         s = attention_planned(pool, batch, Hl, q_local, k_new, v_new, nullptr, &os, workspace, attn, stream, o);
         if (s) return s;
-        // exit barrier, resident behind the attention's last kernel (PDL)
-        static const bool no_exit = getenv("HG_TP_EXIT_SKIP") != nullptr;   // A/B (1 rank only): its cost
-        if (!(no_exit && G == 1)) {
-            s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream, true);
-            if (s) return s;
-        }
+        // exit barrier, resident behind the attention's last kernel (PDL); on the
+        // sharded HBM route it also waits for the append's device count (that append
+        // ran on a side stream without a stream join, so no event wait breaks the
+        // programmatic-dependent chain)
+        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream, true, os.wait_cnt, os.wait_target);
+        if (s) return s;
         uint8_t *data = comm->win + kWinHdr;
         if (out_gathered != data) {
             cudaError_t e = cudaMemcpyAsync(out_gathered, data, out_bytes, cudaMemcpyDeviceToDevice,

@@ -198,6 +198,10 @@ struct OutSpec {
     unsigned long long *bar_mine = nullptr;
     int bar_rank = 0, bar_world = 0;
     unsigned long long bar_epoch = 0;
+    // set by the call when its append ran on a side stream without a stream join
+    // (sharded HBM route): the caller's exit barrier waits for *wait_cnt >= wait_target
+    mutable const unsigned long long *wait_cnt = nullptr;
+    mutable unsigned long long wait_target = 0;
 };
 hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
                        void *ws, size_t ws_bytes, void *stream);
@@ -236,7 +240,8 @@ hg_status launch_rope_append(const uint16_t *k_new, const uint16_t *v_new, uint1
                              void *stream);
 hg_status launch_splitk(const AttnParams &p, void *stream);
 hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
-                              unsigned long long epoch, void *stream, bool pdl = false);
+                              unsigned long long epoch, void *stream, bool pdl = false,
+                              const unsigned long long *wait_cnt = nullptr, unsigned long long wait_target = 0);
 // pdl: launched as a programmatic dependent of the kernel before it in `stream`
 hg_status launch_combine(const AttnParams &p, void *stream, bool pdl = false);
 hg_status launch_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v, void *stream);

@@ -145,6 +145,7 @@ struct BarrierArgs {   // peer-window entry barrier carried by the append (world
     unsigned long long *mine;
     int rank, world;
     unsigned long long epoch;
+    unsigned long long *done;   // non-NULL: every CTA counts itself here after its stores
 };
 
 template <int PER, int NS>
@@ -181,6 +182,13 @@ __global__ void __launch_bounds__(256) append_param_kernel(const uint4 *__restri
             }
         }
     }
+    if (ba.done) {   // a later kernel on another stream waits for the count (no stream join)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(ba.done, 1ull);
+        }
+    }
 }
 
 template <int NS>
@@ -206,6 +214,7 @@ hg_status launch_append_param(const uint16_t *k_new, const uint16_t *v_new, uint
         ba.world = bar->bar_world;
         ba.epoch = bar->bar_epoch;
     }
+    if (bar) ba.done = bar->app_cnt;
     if (T == 0) return HG_OK;
     if (T > kParamSlots) return fail(HG_E_INVALID, "append_param: T %d > %d", T, kParamSlots);
     auto *kn = (const uint4 *)k_new, *vn = (const uint4 *)v_new;
@@ -869,10 +878,19 @@ struct PeerFlags {
 };
 
 __global__ void peer_barrier_kernel(PeerFlags pf, unsigned long long *mine, int rank, int world,
-                                    unsigned long long epoch) {
+                                    unsigned long long epoch, const unsigned long long *wait_cnt,
+                                    unsigned long long wait_target) {
     // as a programmatic dependent of the attention's last kernel: resident early,
     // the barrier starts once that kernel's peer stores are complete
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (wait_cnt) {   // the call's side-stream append has counted every CTA (long done by now)
+        unsigned long long c;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(c) : "l"(wait_cnt) : "memory");
+            if (c >= wait_target) break;
+            __nanosleep(64);
+        }
+    }
     // as the entry barrier: the attention grid behind it may launch at once (it waits
     // for this grid in griddepcontrol.wait before its first peer-window store)
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -880,11 +898,12 @@ __global__ void peer_barrier_kernel(PeerFlags pf, unsigned long long *mine, int 
 }
 
 hg_status launch_peer_barrier(unsigned long long *const *flags, unsigned long long *mine, int rank, int world,
-                              unsigned long long epoch, void *stream, bool pdl) {
+                              unsigned long long epoch, void *stream, bool pdl, const unsigned long long *wait_cnt,
+                              unsigned long long wait_target) {
     PeerFlags pf{};
     for (int k = 0; k < world; ++k) pf.flags[k] = flags[k];
     cudaError_t e = launch_maybe_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, (cudaStream_t)stream, pdl, pf, mine,
-                                     rank, world, epoch);
+                                     rank, world, epoch, wait_cnt, wait_target);
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? HG_OK : fail(HG_E_CUDA, "peer barrier launch: %s", cudaGetErrorString(e));
 }

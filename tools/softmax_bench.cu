@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256, 1) k(const float *in, uint32_t *out, floa
         uint32_t pk[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-            const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2, nref2);
+            const uint64_t x2 = (MODE & 128) ? f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1]))
+                                             : ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2, nref2);
             float a, b;
             const bool poly = (MODE & 8) ? ((0x49 >> (c & 7)) & 1) : ((MODE & 1) && ((0x88 >> (c & 7)) & 1));
             if (poly) {
@@ -71,8 +72,9 @@ __global__ void __launch_bounds__(256, 1) k(const float *in, uint32_t *out, floa
                 a = ex2(x0);
                 b = ex2(x1);
             }
-            ls2[c % NA] = fadd2(ls2[c % NA], f2pack(a, b));
-            pk[c] = pack2(a, b);
+            if (!(MODE & 32)) ls2[c % NA] = fadd2(ls2[c % NA], f2pack(a, b));
+            if (MODE & 64) pk[c] = __float_as_uint(a) ^ __float_as_uint(b);
+            else pk[c] = pack2(a, b);
         }
         float l = 0.f;
 #pragma unroll
@@ -112,6 +114,12 @@ int main() {
     cudaMalloc(&out, 148 * 1024 * 4);
     cudaMalloc(&ls, 148 * 1024 * 4);
     cudaMalloc(&cyc, 8);
+    run<32>("all MUFU, no max, no row sum", in, out, ls, cyc);
+    run<64>("all MUFU, no max, no bf16 pack", in, out, ls, cyc);
+    run<96>("all MUFU, no max, no sum, no pack", in, out, ls, cyc);
+    run<224>("MUFU only (no scale FFMA2, sum, pack)", in, out, ls, cyc);
+    run<33>("1/4 poly, no max, no row sum", in, out, ls, cyc);
+    run<35>("1/4 poly + max, no row sum", in, out, ls, cyc);
 #ifndef ONLY_HALF
     run<0>("all MUFU, no max", in, out, ls, cyc);
     run<1>("1/4 poly, no max", in, out, ls, cyc);

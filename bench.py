@@ -959,9 +959,27 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
     # each rank's slice is generated as its own (smaller-head) workload; values are synthetic
     wl = Workload(local, device=dev)
     same_gpu = os.environ.get("HG_BENCH_SAME_GPU") == "1"
-    uid = [hg.hg_comm_unique_id() if rank == 0 and not same_gpu else None]
+    # the timed path is the peer window (the epilogues store into every rank's window);
+    # the library's NCCL communicator is only its fallback for calls larger than the
+    # window, so a failing NCCL bootstrap degrades to a peer-only communicator
+    comm_kind = "nccl + peer window"
+    try:
+        uid = [hg.hg_comm_unique_id() if rank == 0 and not same_gpu else None]
+    except Exception:
+        uid = [None]
     dist.broadcast_object_list(uid, src=0)
-    comm = hg.Comm(uid[0], rank, world, dev.index)
+    try:
+        comm = hg.Comm(uid[0], rank, world, dev.index)
+    except hg.HgError as e:
+        print(f"[bench rank {rank}] NCCL communicator unavailable ({e}); peer-window only", file=sys.stderr)
+        comm = None
+    ok = torch.tensor([1 if comm is not None else 0], device="cpu" if same_gpu else dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() == 0 or uid[0] is None:
+        if comm is not None:
+            comm.close()
+        comm = hg.Comm(None, rank, world, dev.index)
+        comm_kind = "peer window only"
     # v2: a peer window per rank, mapped by every other rank (CUDA IPC over NVLink);
     # the attention epilogues store straight into all ranks' windows
     handles = [None] * world
@@ -1045,6 +1063,7 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
             "config": config_dict(spec, world),
             "roofline": roofline,
             "plan": st,
+            "communicator": comm_kind,
             "gpu_launches": (st["kernels"] + 1) * args.steps,  # + the exit barrier (the entry one rides in the append)
             "e2e": {"value": spec.T * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2 * world,

@@ -69,6 +69,9 @@ struct hg_kv_pool {
     // the host's running total of the shares launched (each call waits for its own)
     unsigned long long *app_cnt = nullptr;
     unsigned long long app_total = 0;
+    // ... and per request (background append): device counts and the host's targets
+    unsigned long long *app_req_cnt = nullptr;
+    std::vector<unsigned long long> app_req_total;
 };
 
 namespace hg {
@@ -225,6 +228,7 @@ extern "C" hg_status hg_kv_pool_destroy(hg_kv_pool *p) {
         cudaStreamDestroy(p->cp);
     }
     if (p->app_cnt) cudaFree(p->app_cnt);
+    if (p->app_req_cnt) cudaFree(p->app_req_cnt);
     delete p;
     return HG_OK;
 }
@@ -574,31 +578,71 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
                            !no_tc_append &&
                            (int64_t)plan.T * pool->desc.num_kv_heads * pool->desc.head_dim * 4 <= tc_grid * (256 << 10);
     // Where: in the prologue (all 384 threads, ~HBM rate, every pipeline waits for
-    // it) or in the background on each CTA's idle warp (~5 KB/us per CTA, hidden
-    // behind the cached-prefix tiles).  Each CTA's items are reordered so the one
-    // with the most cached-prefix tiles before its first new key comes first (the
-    // CTA's load is unchanged); background when, on every CTA, those tiles take
-    // longer than its share of the append.
+    // it) or in the background on each CTA's idle warp, request by request in the
+    // order the tiles need them (each request's tokens sliced over the grid, ~5 KB/us
+    // per CTA), a TMA producer waiting only for its own item's request.  Each CTA's
+    // items are reordered so the one with the most cached-prefix tiles before its first
+    // new key comes first (the CTA's load is unchanged); a request's need time is the
+    // earliest (item start + cached-prefix tiles) over the items reading its new keys.
+    // Background when every request is appended, at the grid's aggregate rate, before
+    // its need time.
     bool app_bg = false;
+    int32_t app_head = -1;
     if (tc_append && !no_bg_append && (int64_t)plan.tc_off.size() == tc_grid + 1) {
-        constexpr double kTileUs = 1.5, kBgBytesPerUs = 5.0e3, kSlackUs = 5.0;
+        constexpr double kTileUs = 1.5, kItemUs = 2.0, kBgBytesPerUs = 5.0e3, kSlackUs = 5.0;
         auto lead_tiles = [](const TcItem &it) {
             const int64_t nkt = (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys;
             const int64_t before = it.cnew <= it.k0 ? 0 : (int64_t)(it.cnew - it.k0) / kTcKeys;
             return std::min(nkt, before);
         };
-        const double bg_us = 4.0 * plan.T * pool->desc.num_kv_heads * pool->desc.head_dim / tc_grid / kBgBytesPerUs;
-        app_bg = true;
-        for (int64_t b = 0; b < tc_grid && app_bg; ++b) {
+        static thread_local std::vector<double> need;
+        need.assign((size_t)v.R, 1e30);   // decode rows: split-K reads their new keys from the inputs
+        for (int64_t b = 0; b < tc_grid; ++b) {
             TcItem *a = plan.tc.data() + plan.tc_off[b], *e = plan.tc.data() + plan.tc_off[b + 1];
             std::stable_sort(a, e, [&](const TcItem &x, const TcItem &y) { return lead_tiles(x) > lead_tiles(y); });
-            double lead_us = 0;
+            double at = 0;
             for (TcItem *it = a; it < e; ++it) {
-                const int64_t nkt = (it->k1 - it->k0 + kTcKeys - 1) / kTcKeys, l = lead_tiles(*it);
-                lead_us += (double)l * kTileUs;
-                if (l < nkt) break;
+                const int64_t nkt = (it->k1 - it->k0 + kTcKeys - 1) / kTcKeys;
+                if (it->mode == 0 && it->cnew < it->k1) {
+                    const int r = plan.tok[it->t0].req;
+                    need[r] = std::min(need[r], at + (double)lead_tiles(*it) * kTileUs);
+                }
+                at += (double)nkt * kTileUs + kItemUs;
             }
-            app_bg = lead_us >= bg_us + kSlackUs;
+        }
+        static thread_local std::vector<int32_t> order;
+        order.resize((size_t)v.R);
+        for (int i = 0; i < v.R; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return need[x] < need[y]; });
+        const double bytes_per_tok = 4.0 * pool->desc.num_kv_heads * pool->desc.head_dim;   // K + V
+        double done_us = 0;
+        app_bg = true;
+        for (int32_t r : order) {
+            done_us += (double)v.n[r] * bytes_per_tok / (kBgBytesPerUs * (double)tc_grid);
+            if (need[r] < 1e29 && done_us + kSlackUs > need[r]) {
+                app_bg = false;
+                break;
+            }
+        }
+        if (app_bg) {
+            if ((int64_t)pool->app_req_total.size() < v.R) {   // grow the per-request counters
+                if (pool->app_req_cnt) cudaFree(pool->app_req_cnt);
+                pool->app_req_cnt = nullptr;
+                const size_t cap = std::max<size_t>(256, (size_t)v.R * 2);
+                s = cuda_check(cudaMalloc(&pool->app_req_cnt, cap * 8), "cudaMalloc(request counters)");
+                if (!s) s = cuda_check(cudaMemset(pool->app_req_cnt, 0, cap * 8), "memset(request counters)");
+                if (!s) s = cuda_check(cudaDeviceSynchronize(), "request counters init");
+                if (s) { if (pool->app_req_cnt) cudaFree(pool->app_req_cnt); pool->app_req_cnt = nullptr;
+                         pool->app_req_total.clear(); return s; }
+                pool->app_req_total.assign(cap, 0ull);
+            }
+            for (int k = 0; k < v.R; ++k) {
+                const int32_t r = order[k];
+                plan.reqs[r].app_next = k + 1 < v.R ? order[k + 1] : -1;
+                pool->app_req_total[r] += (unsigned long long)tc_grid;   // one count per CTA
+                plan.reqs[r].app_tgt = pool->app_req_total[r];
+            }
+            app_head = v.R > 0 ? order[0] : -1;
         }
     }
     // one image of all descriptors -> one pinned H2D copy
@@ -761,6 +805,8 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         p.v_new = (const uint16_t *)v_new;
         p.app_T = plan.T;
         p.app_bg = app_bg ? 1 : 0;
+        p.app_head = app_head;
+        p.app_req_cnt = pool->app_req_cnt;
         p.app_cnt = pool->app_cnt;
         pool->app_total += (unsigned long long)tc_grid;
         p.app_target = pool->app_total;

@@ -23,6 +23,12 @@ struct ReqDev {
     int32_t n;       // new tokens n_i
     int32_t cu_q;    // first batch row of the request
     int32_t bt_off;  // offset of the request's block ids in bt_flat
+    // background append of a fused tcgen05 step (AttnParams.app_bg): the next request
+    // in need order (-1: last), and the count app_req_cnt[i] reaches once every
+    // CTA has written its slice of this request's new tokens
+    int32_t app_next = -1;
+    int32_t pad_ = 0;
+    unsigned long long app_tgt = 0;
 };
 
 // Split-K item (sm_100a mma.sync path, kernels.cu), launched once per KV head g
@@ -126,10 +132,14 @@ struct AttnParams {
     unsigned long long *app_cnt;
     unsigned long long app_target;
     int32_t app_T;
-    // app_bg = 1: the share is written by the CTA's idle warp 11 in the background
-    // while the pipelines run (the planner found every CTA's first new-key tile late
-    // enough to hide it); 0: by all 384 threads before the pipelines start.
+    // app_bg = 1: written in the background by each CTA's idle warp 11, request by
+    // request in need order (the list from app_head through ReqDev.app_next, each
+    // request's tokens sliced over the grid, app_req_cnt[i] counting the slices
+    // done); a TMA producer waits for its item's request only.  0: all 384 threads
+    // append the CTA's share before the pipelines start (global count app_cnt).
     int32_t app_bg;
+    int32_t app_head;
+    unsigned long long *app_req_cnt;
 };
 
 // Host-side plan (a.1 + a.4): built per call, staged to the device.

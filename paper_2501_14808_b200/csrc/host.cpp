@@ -270,7 +270,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->prefix_sk = 0;
     int64_t T = 0, nbt = 0;
     for (int i = 0; i < v.R; ++i) {
-        p->reqs[i] = ReqDev{v.c[i], v.n[i], (int32_t)T, (int32_t)nbt};
+        p->reqs[i] = ReqDev{v.c[i], v.n[i], (int32_t)T, (int32_t)nbt, -1, 0, 0ull};
         T += v.n[i];
         nbt += ceil_div((int64_t)v.c[i] + v.n[i], B);
     }

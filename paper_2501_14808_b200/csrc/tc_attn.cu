@@ -312,47 +312,50 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(HG_TC_REG_WG2) : "memory");
     if (warp == 11 && p.app_T > 0 && p.app_bg) {
         // ===================== background append (warp 11) =====================
-        // this CTA's share of the new tokens, token by token (the token -> request ->
-        // block chain once per token), 8 K and 8 V 16-byte loads in flight per lane;
-        // the TMA producers wait for every CTA's count before their first new-key tile
-        const int t0 = (int)((int64_t)p.app_T * blockIdx.x / gridDim.x);
-        const int t1 = (int)((int64_t)p.app_T * (blockIdx.x + 1) / gridDim.x);
+        // request by request in need order, this CTA's slice of each request's new
+        // tokens (the block chain once per token), 8 K and 8 V 16-byte loads in flight
+        // per lane; one count per (request, CTA) when the slice is in the cache
         constexpr int cpr = D / 8;
         const int row = p.H_kv * cpr;
         const uint4 *kn = reinterpret_cast<const uint4 *>(p.k_new), *vn = reinterpret_cast<const uint4 *>(p.v_new);
         uint4 *kc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.k_cache));
         uint4 *vc = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(p.v_cache));
         constexpr int U = 8;
-        for (int t = t0; t < t1; ++t) {
-            const ReqDev rq = p.reqs[p.tok[t].req];
-            const int pos = rq.c + (t - rq.cu_q);
-            const int64_t base = ((int64_t)p.bt_flat[rq.bt_off + pos / kBlock] * p.H_kv * kBlock + pos % kBlock) * cpr;
-            const int64_t src = (int64_t)t * row;
-            for (int e0 = lane; e0 < row; e0 += 32 * U) {
-                uint4 kv[U], vv[U];
+        for (int r = p.app_head; r >= 0;) {
+            const ReqDev rq = p.reqs[r];
+            const int a0 = rq.cu_q + (int)((int64_t)rq.n * blockIdx.x / gridDim.x);
+            const int a1 = rq.cu_q + (int)((int64_t)rq.n * (blockIdx.x + 1) / gridDim.x);
+            for (int t = a0; t < a1; ++t) {
+                const int pos = rq.c + (t - rq.cu_q);
+                const int64_t base = ((int64_t)p.bt_flat[rq.bt_off + pos / kBlock] * p.H_kv * kBlock + pos % kBlock) * cpr;
+                const int64_t src = (int64_t)t * row;
+                for (int e0 = lane; e0 < row; e0 += 32 * U) {
+                    uint4 kv[U], vv[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + 32 * u;
-                    if (e < row) {
-                        kv[u] = kn[src + e];
-                        vv[u] = vn[src + e];
+                    for (int u = 0; u < U; ++u) {
+                        const int e = e0 + 32 * u;
+                        if (e < row) {
+                            kv[u] = kn[src + e];
+                            vv[u] = vn[src + e];
+                        }
                     }
-                }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + 32 * u;
-                    if (e < row) {
-                        const int g = e / cpr, ch = e % cpr;
-                        const int64_t dst = base + (int64_t)g * kBlock * cpr + ch;
-                        kc[dst] = kv[u];
-                        vc[dst] = vv[u];
+                    for (int u = 0; u < U; ++u) {
+                        const int e = e0 + 32 * u;
+                        if (e < row) {
+                            const int g = e / cpr, ch = e % cpr;
+                            const int64_t dst = base + (int64_t)g * kBlock * cpr + ch;
+                            kc[dst] = kv[u];
+                            vc[dst] = vv[u];
+                        }
                     }
                 }
             }
+            __threadfence();   // every lane's stores, then one release count per (request, CTA)
+            __syncwarp();
+            if (lane == 0) atomicAdd(p.app_req_cnt + r, 1ull);
+            r = rq.app_next;
         }
-        __threadfence();   // every lane's stores, then one release count per CTA
-        __syncwarp();
-        if (lane == 0) atomicAdd(p.app_cnt, 1ull);
     } else if (warp == 8 || warp == 10) {
         // ===================== TMA producers: warp 8 streams K, warp 10 streams V =====================
         // (separate threads so a V slot that is still busy never delays the next K load)
@@ -361,6 +364,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             bool appended = p.app_T == 0;   // every CTA's share of the fused append is in the cache
             for (int item = it_begin; item < it_end; ++item) {
                 const TcItem it = p.tc[item];
+                if (p.app_bg) appended = p.app_T == 0;   // background mode: waited per item's request
                 const int nkt = nkt_of(it);
                 const int32_t *bt = p.bt_flat + it.bt_off;
                 const int kb0 = it.k0 / kBlock;
@@ -368,10 +372,19 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 for (int j = 0; j < nkt; ++j, ++gn) {
                     if (!appended && it.k0 + (j + 1) * kTcKeys > it.cnew) {
                         // the tile holds keys this call appends: wait for every CTA's share
+                        // prologue mode: every CTA's share (global count); background mode:
+                        // every slice of this item's request (a prefill item's rows are one request)
+                        const unsigned long long *cnt = p.app_cnt;
+                        unsigned long long tgt = p.app_target;
+                        if (p.app_bg) {
+                            const int rq = p.tok[it.t0].req;
+                            cnt = p.app_req_cnt + rq;
+                            tgt = p.reqs[rq].app_tgt;
+                        }
                         unsigned long long c;
                         for (;;) {
-                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(c) : "l"(p.app_cnt) : "memory");
-                            if (c >= p.app_target) break;
+                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(c) : "l"(cnt) : "memory");
+                            if (c >= tgt) break;
                             __nanosleep(64);
                         }
                         asm volatile("fence.proxy.async.global;\n" ::: "memory");   // before the TMA reads

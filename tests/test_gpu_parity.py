@@ -505,11 +505,11 @@ def test_run_to_run_bitwise_and_fixed_split_head_sharding():
 @pytest.mark.parametrize("name,route", [("toy_a", 0), ("c2_g8", 0), ("toy_a", 1), ("p1", 0), ("c1", 1), ("p2", 0)])
 def test_fused_step_equals_append_then_attention(name, route):
     """The fused step -- HBM route: the append beside split-K, which reads the new
-    keys from the inputs; tcgen05 route: the append inside the tcgen05 kernel, in
-    its prologue (p1: some CTAs need new keys early) or on each CTA's idle warp in
-    the background (p2: 48 cached-prefix tiles before the first new key) --
-    leaves the same cache and output as hg_kv_append then hg_hybrid_attention,
-    bit for bit."""
+    keys from the inputs; tcgen05 route: the append inside the tcgen05 kernel, on
+    each CTA's idle warp in the background, request by request in the order the
+    tiles need them (p1, p2: the planner finds every request appended before its
+    first new-key tile), else in the prologue (toy_a) -- leaves the same cache and
+    output as hg_kv_append then hg_hybrid_attention, bit for bit."""
     import paper_2501_14808_b200 as hg
     from synth.configs import make_config
     spec = make_config(name, 1)
@@ -520,7 +520,7 @@ def test_fused_step_equals_append_then_attention(name, route):
     b.step_unfused(opts)
     torch.cuda.synchronize()
     if name in ("p1", "p2"):
-        assert mode == {"p1": 1, "p2": 2}[name], mode
+        assert mode == 2, mode
     assert torch.equal(a.out.view(torch.int16), b.out.view(torch.int16))
     assert torch.equal(a.k_cache.view(torch.int16), b.k_cache.view(torch.int16))
     assert torch.equal(a.v_cache.view(torch.int16), b.v_cache.view(torch.int16))

@@ -414,7 +414,8 @@ struct SkSmem {
     static constexpr int kStage = 2 * kTile;                 // K + V
     static constexpr int kWarp = kSkStages * kStage;
     static constexpr int kQ = kSkRows * D * 2;
-    static constexpr int kMerge = kSkWarps * (kSkRows * D + 2 * kSkRows) * 4;
+    static constexpr int kMS = D + 4;                         // merge row stride (floats): rotates rows by 4 banks
+    static constexpr int kMerge = kSkWarps * (kSkRows * kMS + 2 * kSkRows) * 4;
     static constexpr int kMain = kSkWarps * kWarp;
     static constexpr int kBytes = kQ + (kMain > kMerge ? kMain : kMerge);
 };
@@ -603,17 +604,18 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
     l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
     l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
     __syncthreads();  // all warps done with their KV stages
-    float *mo = reinterpret_cast<float *>(sKV);                     // [warp][16][D]
-    float *mml = mo + kSkWarps * kSkRows * D;                       // [warp][16][2]
+    // [warp][16][MS] (row stride D + 4 floats: the fragment stores' 8 rows and the
+    // merge's 4 rows per quarter-warp land on distinct banks), then [warp][16][2]
+    constexpr int MS = SkSmem<D>::kMS;
+    float *mo = reinterpret_cast<float *>(sKV);
+    float *mml = mo + kSkWarps * kSkRows * MS;
     {
-        float *ow = mo + warp * kSkRows * D;
+        float *ow = mo + warp * kSkRows * MS;
         const int cc = 2 * (lane & 3);
 #pragma unroll
         for (int nt = 0; nt < NNT; ++nt) {
-            ow[ra * D + nt * 8 + cc] = o[nt][0];
-            ow[ra * D + nt * 8 + cc + 1] = o[nt][1];
-            ow[rb * D + nt * 8 + cc] = o[nt][2];
-            ow[rb * D + nt * 8 + cc + 1] = o[nt][3];
+            *reinterpret_cast<float2 *>(ow + ra * MS + nt * 8 + cc) = make_float2(o[nt][0], o[nt][1]);
+            *reinterpret_cast<float2 *>(ow + rb * MS + nt * 8 + cc) = make_float2(o[nt][2], o[nt][3]);
         }
         if ((lane & 3) == 0) {
             mml[(warp * kSkRows + ra) * 2 + 0] = m_a;
@@ -623,7 +625,8 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
         }
     }
     __syncthreads();
-    // 128 threads: thread -> (row r = tid / 8, dim chunk of D/8 elements)
+    // 128 threads: thread -> (row r = tid / 8, columns 4 part8 + 32 k + [0, 4) for k < D/32:
+    // a quarter-warp reads one row's 128 contiguous bytes per k, conflict-free)
     {
         const int r = threadIdx.x >> 3;
         const int part8 = threadIdx.x & 7;
@@ -654,32 +657,37 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
 #pragma unroll
             for (int w = 0; w < kSkWarps; ++w) {
                 const float fw = f[w] * inv;
-                const float *src = mo + (w * kSkRows + r) * D + part8 * PER;
+                const float *src = mo + (w * kSkRows + r) * MS + part8 * 4;
 #pragma unroll
-                for (int e = 0; e < PER; ++e) acc[e] += fw * src[e];
+                for (int k = 0; k < PER / 4; ++k) {
+                    const float4 v = *reinterpret_cast<const float4 *>(src + 32 * k);
+                    acc[4 * k] += fw * v.x;
+                    acc[4 * k + 1] += fw * v.y;
+                    acc[4 * k + 2] += fw * v.z;
+                    acc[4 * k + 3] += fw * v.w;
+                }
             }
             const float lse2 = (L > 0.f) ? ref + __log2f(L) : -CUDART_INF_F;
             if (base < 0) {
                 // sharded call: the entry barrier kernel ahead of this grid (programmatic
                 // dependency) must be through before the first store into a peer's window
                 if (p.bar_pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-                const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + part8 * PER;
+                const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + part8 * 4;
 #pragma unroll
-                for (int e = 0; e < PER; e += 8) {
-                    uint4 v;
-                    v.x = pack_bf16(acc[e + 0], acc[e + 1]);
-                    v.y = pack_bf16(acc[e + 2], acc[e + 3]);
-                    v.z = pack_bf16(acc[e + 4], acc[e + 5]);
-                    v.w = pack_bf16(acc[e + 6], acc[e + 7]);
-                    for (int k = 0; k < p.n_out; ++k) *reinterpret_cast<uint4 *>(p.outs[k] + off + e) = v;
+                for (int k = 0; k < PER / 4; ++k) {
+                    uint2 v;
+                    v.x = pack_bf16(acc[4 * k + 0], acc[4 * k + 1]);
+                    v.y = pack_bf16(acc[4 * k + 2], acc[4 * k + 3]);
+                    for (int o2 = 0; o2 < p.n_out; ++o2) *reinterpret_cast<uint2 *>(p.outs[o2] + off + 32 * k) = v;
                 }
                 if (p.lse && part8 == 0) p.lse[(int64_t)t * p.H_q + h] = lse2 * 0.69314718055994531f;
             } else {
                 const int64_t slot = base + (int64_t)it.part * G + (x % G);
-                float *dst = p.part_o + slot * D + part8 * PER;
+                float *dst = p.part_o + slot * D + part8 * 4;
 #pragma unroll
-                for (int e = 0; e < PER; e += 4)
-                    *reinterpret_cast<float4 *>(dst + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+                for (int k = 0; k < PER / 4; ++k)
+                    *reinterpret_cast<float4 *>(dst + 32 * k) =
+                        make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
                 if (part8 == 0) p.part_lse[slot] = lse2;
             }
         }

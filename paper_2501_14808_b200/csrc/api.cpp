@@ -694,7 +694,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         s = cuda_check(cudaEventRecord(pool->ev_pre, st), "order record");   // after the caller's earlier work
         if (!s) s = cuda_check(cudaStreamWaitEvent(pool->side, pool->ev_pre, 0), "order wait");
         AttnParams bar{};   // a sharded call's peer-window entry barrier rides in this kernel
-        if (outs && outs->bar_world > 0 && !sk_early) {   // (beside split-K: its own kernel, see below)
+        if (outs && outs->bar_world > 0 && !sk_early) {   // (beside split-K: see below)
             for (int k = 0; k < outs->bar_world; ++k) bar.bar_flags[k] = outs->bar_flags[k];
             bar.bar_mine = outs->bar_mine;
             bar.bar_rank = outs->bar_rank;
@@ -741,6 +741,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (s) return s;
     }
     uint8_t *w = (uint8_t *)ws;
+    static const bool no_sk_merge = getenv("HG_NO_SK_MERGE") != nullptr;   // A/B switch: combine kernel
     AttnParams p{};
     p.k_cache = (const uint16_t *)pool->desc.k_cache;
     p.v_cache = (const uint16_t *)pool->desc.v_cache;
@@ -774,6 +775,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.tc_off = (const int32_t *)(dsc + plan.off_tcoff);
     p.sk_off = (const int32_t *)(dsc + plan.off_skoff);
     p.sk_ctas = (int32_t)plan.sk_off.size() - 1;
+    p.sk_cnt = (plan.sk_merge && !no_sk_merge) ? (unsigned int *)(dsc + plan.off_cnt) : nullptr;
     p.part_o = (float *)(w + plan.off_part_o);
     p.part_lse = (float *)(w + plan.off_part_lse);
     p.H_q = H_q;
@@ -790,7 +792,12 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     if (sk_early) {
         p.k_new = (const uint16_t *)k_new;
         p.v_new = (const uint16_t *)v_new;
-        if (outs && outs->bar_world > 0) {
+        // sharded: the entry barrier in split-K's first CTA (HG_TP_ENTRY_KERNEL: a 1-warp
+        // kernel ahead of split-K, its programmatic primary -- A/B)
+        static const bool entry_kernel = getenv("HG_TP_ENTRY_KERNEL") != nullptr;
+        if (outs && outs->bar_world > 0 && !entry_kernel) {
+            p.entry_word = (unsigned int *)(dsc + plan.off_exit) + 2;
+        } else if (outs && outs->bar_world > 0) {
             // sharded: the peer-window entry barrier as a 1-warp kernel right ahead of
             // split-K, which is its programmatic dependent (launched at once, waiting
             // for the barrier only before its first peer-window store)
@@ -910,6 +917,18 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         ++kernels;
         return HG_OK;
     };
+    // sharded HBM route with split-K last (its partials merged in the kernel): the exit
+    // barrier runs in split-K's last CTA (HG_TP_EXIT_KERNEL: its own kernel, A/B)
+    static const bool exit_kernel = getenv("HG_TP_EXIT_KERNEL") != nullptr;
+    const bool fold_exit = outs && outs->exit_epoch && (p.bar_pdl || p.entry_word) && !p.n_tc && p.n_sk &&
+                           (!p.n_comb || p.sk_cnt) && !exit_kernel;
+    if (fold_exit) {
+        p.exit_epoch = outs->exit_epoch;
+        p.exit_ticket = (unsigned int *)(dsc + plan.off_exit);
+        p.exit_wait_cnt = outs->wait_cnt;
+        p.exit_wait_target = outs->wait_target;
+        outs->exit_folded = true;
+    }
     if ((s = do_tc())) return s;   // first: its CTAs are placed before split-K fills the SMs
     if ((s = do_sk())) return s;
     if (overlap) {
@@ -918,7 +937,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_join, 0), "join wait");
         if (s) return s;
     }
-    if (p.n_comb) {
+    if (p.n_comb && !p.sk_cnt) {
         rec(4, st);
         // right behind split-K on the same stream: a programmatic dependent launch
         // (resident early, waits for split-K's completion in griddepcontrol.wait)

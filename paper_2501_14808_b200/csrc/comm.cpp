@@ -216,6 +216,7 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
             os.bar_rank = comm->rank;
             os.bar_world = G;
             os.bar_epoch = ++comm->epoch;
+            os.exit_epoch = ++comm->epoch;   // the call may run the exit barrier in its last kernel
         } else {
             s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream);
             if (s) return s;
@@ -226,8 +227,11 @@ static hg_status tp_call(hg_kv_pool *pool, hg_comm *comm, const hg_batch *batch,
         // sharded HBM route it also waits for the append's device count (that append
         // ran on a side stream without a stream join, so no event wait breaks the
         // programmatic-dependent chain)
-        s = launch_peer_barrier(fl, mine, comm->rank, G, ++comm->epoch, stream, true, os.wait_cnt, os.wait_target);
-        if (s) return s;
+        if (!os.exit_folded) {
+            const unsigned long long ep = os.exit_epoch ? os.exit_epoch : ++comm->epoch;
+            s = launch_peer_barrier(fl, mine, comm->rank, G, ep, stream, true, os.wait_cnt, os.wait_target);
+            if (s) return s;
+        }
         uint8_t *data = comm->win + kWinHdr;
         if (out_gathered != data) {
             cudaError_t e = cudaMemcpyAsync(out_gathered, data, out_bytes, cudaMemcpyDeviceToDevice,

@@ -140,6 +140,22 @@ struct AttnParams {
     int32_t app_bg;
     int32_t app_head;
     unsigned long long *app_req_cnt;
+    // In-kernel merge (no tcgen05 items, so every partial comes from split-K):
+    // arrival counters [T][H_kv], zero in every call's descriptor image; the split-K
+    // CTA completing a token's partials merges its rows and no combine kernel runs.
+    // NULL: partials are merged by combine_kernel.
+    unsigned int *sk_cnt;
+    // Sharded HBM route with split-K as the call's last kernel: the peer-window exit
+    // barrier runs in split-K's last CTA (exit_ticket counts finished CTAs, zero in
+    // the descriptor image) instead of a kernel of its own; it waits for the side-
+    // stream append's count first.  exit_epoch = 0: no folded barrier.
+    // sharded HBM route: split-K's first CTA runs the entry barrier (bar_* fields);
+    // entry_word[0] its ticket, [1] set once through (desc image, zero each call; NULL: none)
+    unsigned int *entry_word;
+    unsigned long long exit_epoch;
+    unsigned int *exit_ticket;
+    const unsigned long long *exit_wait_cnt;
+    unsigned long long exit_wait_target;
 };
 
 // Host-side plan (a.1 + a.4): built per call, staged to the device.
@@ -163,9 +179,10 @@ struct Plan {
     int64_t kv_bytes_unique = 0;
     int64_t kv_bytes_read = 0;
     int32_t tc_ctas = 0;        // persistent tcgen05 grid chosen by the planner
+    bool sk_merge = false;      // partials merged inside split-K (AttnParams.sk_cnt)
     // device layout (byte offsets inside the workspace)
     size_t off_reqs = 0, off_bt = 0, off_sk = 0, off_tc = 0, off_rows = 0, off_cbase = 0,
-           off_comb = 0, off_tcoff = 0, off_skoff = 0, off_qrot = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
+           off_comb = 0, off_tcoff = 0, off_skoff = 0, off_cnt = 0, off_exit = 0, off_qrot = 0, desc_bytes = 0, off_part_o = 0, off_part_lse = 0, total_bytes = 0;
 };
 
 // ---- host helpers (host.cpp) ------------------------------------------------
@@ -212,6 +229,10 @@ struct OutSpec {
     // (sharded HBM route): the caller's exit barrier waits for *wait_cnt >= wait_target
     mutable const unsigned long long *wait_cnt = nullptr;
     mutable unsigned long long wait_target = 0;
+    // exit barrier epoch the call may fold into its last kernel (0: the caller launches
+    // the exit barrier); the call sets exit_folded when it did
+    unsigned long long exit_epoch = 0;
+    mutable bool exit_folded = false;
 };
 hg_status attention_to(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q, const OutSpec &outs,
                        void *ws, size_t ws_bytes, void *stream);

@@ -522,8 +522,8 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             // pieces than 4 waves' worth mean fewer partials to write and merge (c1
             // 0.451 -> 0.443 ms, its G = 8 shard 0.107 -> 0.099 ms; c2 / c3 within
             // 0.5 %); small batches keep the 256-key floor.  HG_SK_WAVES: A/B knob.
-            static const int waves = getenv("HG_SK_WAVES") ? std::max(1, atoi(getenv("HG_SK_WAVES"))) : 1;
-            const int64_t target = (int64_t)o.num_sms * 3 * waves;
+            static const double waves = getenv("HG_SK_WAVES") ? std::max(0.25, atof(getenv("HG_SK_WAVES"))) : 1.0;
+            const int64_t target = (int64_t)std::llround(o.num_sms * 3 * waves);
             int64_t ct = (total_keys + target - 1) / std::max<int64_t>(target, 1);
             ct = std::max<int64_t>(ct, 256);
             chunk_tok = (int)((ct + B - 1) / B * B);
@@ -611,6 +611,11 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->off_comb = off;  off = align_up(off + sizeof(int32_t) * p->comb.size(), 16);
     p->off_tcoff = off; off = align_up(off + sizeof(int32_t) * p->tc_off.size(), 16);
     p->off_skoff = off; off = align_up(off + sizeof(int32_t) * p->sk_off.size(), 16);
+    // no tcgen05 items: split-K merges the partials itself (arrival counters, zero in
+    // the uploaded image) and no combine kernel runs
+    p->sk_merge = p->tc.empty() && !p->comb.empty();
+    p->off_cnt = off;   off = align_up(off + (p->sk_merge ? sizeof(uint32_t) * (size_t)T * H_kv : 0), 16);
+    p->off_exit = off;  off = align_up(off + 16, 16);   // split-K's entry / exit tickets (folded barriers)
     p->desc_bytes = off;   // the descriptor image lives in a library-owned device slot (api.cpp stage_desc)
     off = 0;               // the caller's workspace: partials and the rotated-Q copy only
     p->off_part_o = off;   off = align_up(off + sizeof(float) * (size_t)p->n_slots * d, 256);

@@ -420,6 +420,87 @@ struct SkSmem {
     static constexpr int kBytes = kQ + (kMain > kMerge ? kMain : kMerge);
 };
 
+// Sharded step: split-K's first store into a peer window waits until this call's
+// entry barrier is through -- either the barrier kernel ahead of it (programmatic
+// dependency, bar_pdl) or the barrier run by split-K's own first CTA (entry_word).
+__device__ __forceinline__ void wait_entry(const AttnParams &p) {
+    if (p.bar_pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (p.entry_word) {
+        unsigned int c;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(c) : "l"(p.entry_word + 1) : "memory");
+            if (c) break;
+            __nanosleep(128);
+        }
+    }
+}
+
+// a.7 merge of one row's partials: O = sum_s 2^{lse_s - LSE} o_s, LSE = log2 sum_s 2^{lse_s}
+// One merged row (token t, KV head g, q-head-in-group hl) by one warp.  Shared by
+// the combine kernel and split-K's in-kernel merge (AttnParams.sk_cnt), so the two
+// give bit-identical rows.  Partials are read through L2 (ld.global.cg): inside
+// split-K they were written by other SMs during this grid.
+template <int D>
+__device__ __forceinline__ void combine_row(const AttnParams &p, const int t, const int g, const int hl,
+                                            const int lane) {
+    const int G = p.G_q;
+    const TokDev tk = p.tok[t];
+    const int64_t base = tk.base + (int64_t)g * tk.nparts * G;
+    // the parts' LSEs are loaded once, lane s holding parts s, s + 32, ...; max and
+    // sum by warp shuffles (no chain of dependent loads per part)
+    float lv[2];
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int sidx = lane + 32 * k;
+        lv[k] = sidx < tk.nparts ? __ldcg(p.part_lse + base + (int64_t)sidx * G + hl) : -CUDART_INF_F;
+        M = fmaxf(M, lv[k]);
+    }
+    for (int sidx = lane + 64; sidx < tk.nparts; sidx += 32) M = fmaxf(M, __ldcg(p.part_lse + base + (int64_t)sidx * G + hl));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float ref = (M == -CUDART_INF_F) ? 0.f : M;
+    float wl[2], L = 0.f;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        wl[k] = fast_exp2(lv[k] - ref);   // 0 for missing / empty parts
+        L += wl[k];
+    }
+    for (int sidx = lane + 64; sidx < tk.nparts; sidx += 32)
+        L += fast_exp2(__ldcg(p.part_lse + base + (int64_t)sidx * G + hl) - ref);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    constexpr int PER = D / 32;
+    float acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+#pragma unroll 4
+    for (int sidx = 0; sidx < tk.nparts; ++sidx) {
+        const int64_t slot = base + (int64_t)sidx * G + hl;
+        const float w = (sidx < 64 ? __shfl_sync(0xffffffffu, wl[sidx >> 5], sidx & 31)
+                                   : fast_exp2(__ldcg(p.part_lse + slot) - ref)) * inv;
+        const float *src = p.part_o + slot * D + lane * PER;
+#pragma unroll
+        for (int e = 0; e < PER; e += 2) {
+            float2 v = __ldcg(reinterpret_cast<const float2 *>(src + e));
+            acc[e] += w * v.x;
+            acc[e + 1] += w * v.y;
+        }
+    }
+    const int h = g * G + hl;
+    const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + lane * PER;
+    uint32_t pk[PER / 2];
+#pragma unroll
+    for (int e = 0; e < PER; e += 2) pk[e / 2] = pack_bf16(acc[e], acc[e + 1]);
+    for (int k = 0; k < p.n_out; ++k) {
+#pragma unroll
+        for (int e = 0; e < PER / 2; ++e) reinterpret_cast<uint32_t *>(p.outs[k] + off)[e] = pk[e];
+    }
+    if (p.lse && lane == 0)
+        p.lse[(int64_t)t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
+}
+
 // One split-K item (a piece of one row chunk's keys for KV head g) by the whole CTA.
 template <int D>
 __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it, const int g, uint8_t *smem) {
@@ -671,7 +752,7 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
             if (base < 0) {
                 // sharded call: the entry barrier kernel ahead of this grid (programmatic
                 // dependency) must be through before the first store into a peer's window
-                if (p.bar_pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+                wait_entry(p);
                 const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + part8 * 4;
 #pragma unroll
                 for (int k = 0; k < PER / 4; ++k) {
@@ -692,6 +773,41 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
             }
         }
     }
+    // ---- in-kernel merge (no combine kernel; every partial comes from this grid) ----
+    // Each token this item wrote partials for counts one arrival per (token, KV head);
+    // the CTA bringing the count to nparts x (head chunks) merges the token's G rows.
+    // Release: every writer fences, then the CTA barrier, then the counting atomics
+    // (the threadFenceReduction pattern); acquire: a fence after the winning atomic,
+    // partials read through L2.
+    if (p.sk_cnt && it.part >= 0) {
+        __shared__ uint32_t s_win;
+        __threadfence();
+        if (threadIdx.x == 0) s_win = 0;
+        __syncthreads();
+        const int u0 = it.hl0 / G, u1 = (it.hl0 + nrows - 1) / G;   // local token range of the rows
+        const int nu = u1 - u0 + 1;                                // <= 16
+        if ((int)threadIdx.x < nu) {
+            const int u = u0 + threadIdx.x;
+            const int t = it.mode ? p.tc_tok[it.j0 + u] : rq.cu_q + it.j0 + u;
+            const int need = p.tok[t].nparts * (G > kSkRows ? (G + kSkRows - 1) / kSkRows : 1);
+            if (atomicAdd(p.sk_cnt + (int64_t)t * p.H_kv + g, 1u) == (unsigned)need - 1) atomicOr(&s_win, 1u << threadIdx.x);
+        }
+        __syncthreads();
+        uint32_t win = s_win;
+        if (win) {
+            __threadfence();
+            wait_entry(p);   // peer-window stores follow
+            // rows (u, hl) of the winning tokens, one warp each
+            const int nw = __popc(win);
+            for (int k = warp; k < nw * G; k += kSkWarps) {
+                uint32_t m = win;
+                for (int z = k / G; z > 0; --z) m &= m - 1;
+                const int u = u0 + __ffs(m) - 1;
+                const int t = it.mode ? p.tc_tok[it.j0 + u] : rq.cu_q + it.j0 + u;
+                combine_row<D>(p, t, g, k % G, lane);
+            }
+        }
+    }
 }
 
 // Persistent split-K grid: CTA (b, g) runs the items [sk_off[b], sk_off[b+1]) for
@@ -706,6 +822,21 @@ splitk_kernel(const AttnParams p) {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int g = blockIdx.y;   // KV head
     const int i0 = p.sk_off[blockIdx.x], i1 = p.sk_off[blockIdx.x + 1];
+    if (p.entry_word && threadIdx.x < 32) {
+        // folded entry barrier: the first CTA to start (so one that is resident) runs the
+        // peer-window flag barrier and publishes its passage; every CTA waits for that
+        // only before its first peer-window store (wait_entry)
+        unsigned int first = 0;
+        if (threadIdx.x == 0) first = atomicAdd(p.entry_word, 1u) == 0;
+        if (__shfl_sync(0xffffffffu, first, 0)) {
+            peer_barrier_body(p.bar_flags, p.bar_mine, p.bar_rank, p.bar_world, p.bar_epoch, threadIdx.x);
+            __syncwarp();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], 1;\n" ::"l"(p.entry_word + 1) : "memory");
+            }
+        }
+    }
     long long *tr = p.sk_trace ? p.sk_trace + 2 * ((int64_t)g * gridDim.x + blockIdx.x) : nullptr;
     if (tr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(tr[0]));
     for (int i = i0; i < i1; ++i) {
@@ -714,11 +845,45 @@ splitk_kernel(const AttnParams p) {
     }
     if (tr) {
         __syncthreads();
-        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(tr[1]));
+        if (threadIdx.x == 0) {
+            asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(tr[1]));
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+            p.sk_trace[2 * (int64_t)gridDim.x * gridDim.y + (int64_t)g * gridDim.x + blockIdx.x] = smid;
+        }
     }
     // this grid completes only after the entry barrier ahead of it: the combine behind
     // it (which waits for this grid) stores into peers' windows only after the barrier
-    if (p.bar_pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (p.bar_pdl || p.entry_word) {
+        if (threadIdx.x == 0) wait_entry(p);
+        __syncthreads();
+    }
+    if (p.exit_epoch) {
+        // folded exit barrier: every CTA releases its stores at GPU scope and takes a
+        // ticket; the last one (acquire) waits for the side-stream append's count, then
+        // runs the flag barrier, whose system-scope release is cumulative over every
+        // store it has observed
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(p.exit_ticket, 1u) == gridDim.x * gridDim.y - 1;
+        }
+        __syncthreads();
+        if (s_last && threadIdx.x < 32) {
+            __threadfence();
+            if (p.exit_wait_cnt && threadIdx.x == 0) {
+                unsigned long long c;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(c) : "l"(p.exit_wait_cnt) : "memory");
+                    if (c >= p.exit_wait_target) break;
+                    __nanosleep(64);
+                }
+            }
+            __syncwarp();
+            peer_barrier_body(p.bar_flags, p.bar_mine, p.bar_rank, p.bar_world, p.exit_epoch, threadIdx.x);
+        }
+    }
 }
 
 // Launch with the programmatic-stream-serialization attribute (pdl = true): the
@@ -777,61 +942,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const AttnParams p) {
     if (wid >= (int64_t)p.n_comb * p.H_kv * G) return;
     const int t = p.comb[wid / (p.H_kv * G)];
     const int rem = (int)(wid % (p.H_kv * G));
-    const int g = rem / G, hl = rem % G;
-    const TokDev tk = p.tok[t];
-    const int64_t base = tk.base + (int64_t)g * tk.nparts * G;
-    // the parts' LSEs are loaded once, lane s holding parts s, s + 32, ...; max and
-    // sum by warp shuffles (no chain of dependent loads per part)
-    float lv[2];
-    float M = -CUDART_INF_F;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int sidx = lane + 32 * k;
-        lv[k] = sidx < tk.nparts ? p.part_lse[base + (int64_t)sidx * G + hl] : -CUDART_INF_F;
-        M = fmaxf(M, lv[k]);
-    }
-    for (int sidx = lane + 64; sidx < tk.nparts; sidx += 32) M = fmaxf(M, p.part_lse[base + (int64_t)sidx * G + hl]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const float ref = (M == -CUDART_INF_F) ? 0.f : M;
-    float wl[2], L = 0.f;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        wl[k] = fast_exp2(lv[k] - ref);   // 0 for missing / empty parts
-        L += wl[k];
-    }
-    for (int sidx = lane + 64; sidx < tk.nparts; sidx += 32) L += fast_exp2(p.part_lse[base + (int64_t)sidx * G + hl] - ref);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    constexpr int PER = D / 32;
-    float acc[PER];
-#pragma unroll
-    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-#pragma unroll 4
-    for (int sidx = 0; sidx < tk.nparts; ++sidx) {
-        const int64_t slot = base + (int64_t)sidx * G + hl;
-        const float w = (sidx < 64 ? __shfl_sync(0xffffffffu, wl[sidx >> 5], sidx & 31)
-                                   : fast_exp2(p.part_lse[slot] - ref)) * inv;
-        const float *src = p.part_o + slot * D + lane * PER;
-#pragma unroll
-        for (int e = 0; e < PER; e += 2) {
-            float2 v = *reinterpret_cast<const float2 *>(src + e);
-            acc[e] += w * v.x;
-            acc[e + 1] += w * v.y;
-        }
-    }
-    const int h = g * G + hl;
-    const int64_t off = (int64_t)t * p.out_ld + (int64_t)h * D + lane * PER;
-    uint32_t pk[PER / 2];
-#pragma unroll
-    for (int e = 0; e < PER; e += 2) pk[e / 2] = pack_bf16(acc[e], acc[e + 1]);
-    for (int k = 0; k < p.n_out; ++k) {
-#pragma unroll
-        for (int e = 0; e < PER / 2; ++e) reinterpret_cast<uint32_t *>(p.outs[k] + off)[e] = pk[e];
-    }
-    if (p.lse && lane == 0)
-        p.lse[(int64_t)t * p.H_q + h] = (L > 0.f ? ref + __log2f(L) : -CUDART_INF_F) * 0.69314718055994531f;
+    combine_row<D>(p, t, rem / G, rem % G, lane);
 }
 
 hg_status launch_combine(const AttnParams &p, void *stream, bool pdl) {

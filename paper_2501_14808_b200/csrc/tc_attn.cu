@@ -17,10 +17,10 @@
 // KV head is a [16][64] box per 64-column half (2 KB), eight blocks per tile,
 // K in a 3-deep ring and V in a 2-deep ring, shared by both Q tiles.  Warp
 // roles (384 threads): warps 0-3 / 4-7 softmax + epilogue of Q tile 0 / 1
-// (thread <-> TMEM lane <-> row, setmaxnreg 224), warp 8 the K TMA producer,
+// (thread <-> TMEM lane <-> row, setmaxnreg 200), warp 8 the K TMA producer,
 // warp 10 the V TMA producer, warp 9 MMA issuer + TMEM allocator (all 512
-// columns), warp 11 idle (warps 8-11 drop to 56 registers).
-// Synchronisation is mbarrier-only.
+// columns), warp 11 the fused step's background append (else idle); warps
+// 8-11 drop to 104 registers.  Synchronisation is mbarrier-only.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>

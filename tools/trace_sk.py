@@ -32,7 +32,7 @@ for rep in range(4):
     torch.cuda.synchronize()
 st = hg.hg_last_plan_stats(wl.pool)
 t = tr.cpu().numpy()
-n = int((t != 0).sum() // 2)
+n = int(st["splitk_items"])   # CTAs (the SM ids follow the start / end pairs)
 s, e = t[0:2 * n:2], t[1:2 * n:2]
 t0 = s.min()
 s, e = (s - t0) / 1e3, (e - t0) / 1e3
@@ -43,3 +43,34 @@ active = [int(((s <= x) & (e > x)).sum()) for x in edges]
 print("time(us) active CTAs")
 for x, a in zip(edges, active):
     print(f"{x:7.1f} {a:5d} " + "#" * (a // 8))
+if os.environ.get("HG_TRACE_TAIL"):
+    # CTA b runs LPT item b (one item per CTA): who ends last, and how long the
+    # first wave's items take as a function of their LPT rank
+    order = np.argsort(e)[::-1][:24]
+    print("last-ending CTAs: lpt_rank start end dur")
+    for b in order:
+        print(f"  {b:5d} {s[b]:7.1f} {e[b]:7.1f} {e[b] - s[b]:6.1f}")
+    for lo, hi in [(0, 50), (50, 150), (150, 300), (300, 444), (444, 600), (600, n - 40), (n - 40, n)]:
+        if hi > lo:
+            d = e[lo:hi] - s[lo:hi]
+            print(f"  rank [{lo},{hi}): start {np.median(s[lo:hi]):6.1f} end med {np.median(e[lo:hi]):6.1f} "
+                  f"max {e[lo:hi].max():6.1f} dur med {np.median(d):6.1f} min {d.min():6.1f} max {d.max():6.1f}")
+    # SM of each CTA (written after the start / end pairs): do the slow first-wave CTAs
+    # share SMs (or GPCs)?
+    sm = t[2 * n:3 * n].astype(np.int64)
+    d = e - s
+    first = np.arange(n) < min(444, n)
+    big = first & (np.arange(n) < 300)
+    if big.any():
+        db = d[big]
+        slow = big & (d > np.percentile(db, 90))
+        fast = big & (d < np.percentile(db, 10))
+        print("  slowest 10% of ranks [0,300): SMs", sorted(sm[slow].tolist()))
+        print("  fastest 10% of ranks [0,300): SMs", sorted(sm[fast].tolist()))
+        per_sm = {}
+        for b in np.flatnonzero(big):
+            per_sm.setdefault(int(sm[b]), []).append(d[b])
+        avg = np.array([np.mean(per_sm.get(k, [np.nan])) for k in range(148)])
+        print("  mean big-item duration by SM id (rows of 16 SMs):")
+        for r0 in range(0, 148, 16):
+            print("   " + " ".join(f"{x:5.1f}" for x in avg[r0:r0 + 16]))

@@ -97,7 +97,10 @@ static hg_status sticky_check() {
 }
 
 // Copy `bytes` of host data to `dst` on `stream` through a pinned staging buffer.
-static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+// Copy `bytes` to device memory `dst` on `st` through the next pinned staging slot;
+// `fill` writes the bytes into the slot (so an image can be assembled in place).
+template <typename Fill>
+static hg_status stage_h2d_fill(hg_kv_pool *pool, void *dst, size_t bytes, cudaStream_t st, const Fill &fill) {
     if (bytes == 0) return HG_OK;
     auto &s = pool->ring[pool->ring_pos];
     pool->ring_pos = (pool->ring_pos + 1) % hg_kv_pool::kRing;
@@ -117,7 +120,7 @@ static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t 
         hg_status r = cuda_check(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming), "event create");
         if (r) return r;
     }
-    memcpy(s.host, src, bytes);
+    fill((uint8_t *)s.host);
     hg_status r = cuda_check(cudaMemcpyAsync(dst, s.host, bytes, cudaMemcpyHostToDevice, st), "H2D descriptors");
     if (r) return r;
     r = cuda_check(cudaEventRecord(s.ev, st), "event record");
@@ -126,11 +129,16 @@ static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t 
     return HG_OK;
 }
 
+static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    return stage_h2d_fill(pool, dst, bytes, st, [&](uint8_t *h) { memcpy(h, src, bytes); });
+}
+
 // Upload a call's descriptor image into the next device slot on the copy stream
 // and make `st` wait for it.  The copy waits (on the GPU) only for the kernels
 // of the call that used the slot before; the caller records `done` after its
 // last kernel (DescDone).
-static hg_status stage_desc(hg_kv_pool *pool, const void *img, size_t bytes, cudaStream_t st, void **dev,
+template <typename Fill>
+static hg_status stage_desc(hg_kv_pool *pool, const Fill &fill, size_t bytes, cudaStream_t st, void **dev,
                             hg_kv_pool::DSlot **slot) {
     hg_status s = HG_OK;
     if (!pool->cp) s = cuda_check(cudaStreamCreateWithFlags(&pool->cp, cudaStreamNonBlocking), "copy stream");
@@ -154,7 +162,7 @@ static hg_status stage_desc(hg_kv_pool *pool, const void *img, size_t bytes, cud
         d.cap = cap;
     }
     if (d.used) s = cuda_check(cudaStreamWaitEvent(pool->cp, d.done, 0), "descriptor slot wait");
-    if (!s) s = stage_h2d(pool, d.dev, img, bytes, pool->cp);
+    if (!s) s = stage_h2d_fill(pool, d.dev, bytes, pool->cp, fill);   // the image is assembled in the pinned slot
     if (!s) s = cuda_check(cudaEventRecord(d.ready, pool->cp), "descriptor ready record");
     if (!s) s = cuda_check(cudaStreamWaitEvent(st, d.ready, 0), "descriptor ready wait");
     if (s) return s;
@@ -472,6 +480,8 @@ struct StepPipe {
                                                 // launch (so that launch is not delayed by the host)
     bool planned = false;                       // pool->plan already holds this batch's validated plan
     bool used = false;                          // out: the call was split into waves
+    uint16_t *zc_out = nullptr;                 // device-visible pinned host O: split-K and the combine
+                                                // store their final rows there (zero-copy result)
 };
 static PlanOpts plan_opts(const hg_kv_pool *pool, const hg_attn_opts *o) {
     PlanOpts po;
@@ -565,6 +575,10 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         }
         if (pipe && pipe->used)
             for (TokDev &tk : plan.tok) tk.wave = v.n[tk.req] > 1 ? 1 : 0;
+        // zero-copy result only where every row is written either by split-K / the
+        // combine (to the host) or by the tcgen05 kernel of the two-wave step (its rows
+        // are copied back on their own): not when one launch mixes both into one copy
+        if (pipe && pipe->zc_out && !pipe->used && !plan.tc.empty()) pipe->zc_out = nullptr;
     }
     // tcgen05 route: the append runs inside the tcgen05 kernel, each CTA writing
     // its share of the new tokens (<= ~256 KB of K+V per CTA), and a TMA producer
@@ -645,19 +659,23 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             app_head = v.R > 0 ? order[0] : -1;
         }
     }
-    // one image of all descriptors -> one pinned H2D copy
-    static thread_local std::vector<uint8_t> img;
-    img.assign(plan.desc_bytes, 0);
-    auto put = [&](size_t off, const void *src, size_t n) { if (n) memcpy(img.data() + off, src, n); };
-    put(plan.off_reqs, plan.reqs.data(), sizeof(ReqDev) * plan.reqs.size());
-    put(plan.off_bt, plan.bt_flat.data(), sizeof(int32_t) * plan.bt_flat.size());
-    put(plan.off_sk, plan.sk.data(), sizeof(SkItem) * plan.sk.size());
-    put(plan.off_tc, plan.tc.data(), sizeof(TcItem) * plan.tc.size());
-    put(plan.off_rows, plan.tc_tok.data(), sizeof(int32_t) * plan.tc_tok.size());
-    put(plan.off_cbase, plan.tok.data(), sizeof(TokDev) * plan.tok.size());
-    put(plan.off_comb, plan.comb.data(), sizeof(int32_t) * plan.comb.size());
-    put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
-    put(plan.off_skoff, plan.sk_off.data(), sizeof(int32_t) * plan.sk_off.size());
+    // one image of all descriptors -> one pinned H2D copy, assembled in the staging slot
+    // (alignment gaps are never read; the in-kernel counters at off_cnt.. are zeroed)
+    auto build_img = [&](uint8_t *img) {
+        auto put = [&](size_t off, const void *src, size_t n) { if (n) memcpy(img + off, src, n); };
+        put(plan.off_reqs, plan.reqs.data(), sizeof(ReqDev) * plan.reqs.size());
+        for (int i = 0; i < v.R; ++i)   // block tables: straight from the caller's rows
+            put(plan.off_bt + sizeof(int32_t) * (size_t)plan.reqs[i].bt_off, v.bt + (int64_t)i * v.W,
+                sizeof(int32_t) * (size_t)((v.c[i] + v.n[i] + pool->desc.block_size - 1) / pool->desc.block_size));
+        put(plan.off_sk, plan.sk.data(), sizeof(SkItem) * plan.sk.size());
+        put(plan.off_tc, plan.tc.data(), sizeof(TcItem) * plan.tc.size());
+        put(plan.off_rows, plan.tc_tok.data(), sizeof(int32_t) * plan.tc_tok.size());
+        put(plan.off_cbase, plan.tok.data(), sizeof(TokDev) * plan.tok.size());
+        put(plan.off_comb, plan.comb.data(), sizeof(int32_t) * plan.comb.size());
+        put(plan.off_tcoff, plan.tc_off.data(), sizeof(int32_t) * plan.tc_off.size());
+        put(plan.off_skoff, plan.sk_off.data(), sizeof(int32_t) * plan.sk_off.size());
+        memset(img + plan.off_cnt, 0, plan.desc_bytes - plan.off_cnt);
+    };
     // Fused step (no rope, no host-step waves): the append takes its slots from
     // the kernel parameters and runs on the side stream while the descriptors
     // upload, instead of after them (the tiles and split-K wait for both).
@@ -728,7 +746,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     void *dbase = nullptr;
     DescDone desc_done;
     desc_done.st = st;
-    s = stage_desc(pool, img.data(), plan.desc_bytes, st, &dbase, &desc_done.slot);
+    s = stage_desc(pool, build_img, plan.desc_bytes, st, &dbase, &desc_done.slot);
     if (s) return s;
     if (param_append && !sk_early) {
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
@@ -818,6 +836,14 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         pool->app_total += (unsigned long long)tc_grid;
         p.app_target = pool->app_total;
     }
+    // host step with a device-visible pinned output: the rows split-K and the combine
+    // finish go straight into host memory from the kernels (their PCIe writes overlap
+    // the attention); the tcgen05 kernel keeps writing the device copy
+    auto sk_params = [&]() {
+        AttnParams q = p;
+        if (pipe && pipe->zc_out) q.outs[0] = pipe->zc_out;
+        return q;
+    };
     int kernels = 0;
     auto rec = [&](int k, cudaStream_t on) {
         if (o && o->events[k]) cudaEventRecord((cudaEvent_t)o->events[k], on);
@@ -831,7 +857,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (!s) s = launch_append_dev(p, (const uint16_t *)k_new, (const uint16_t *)v_new, plan.T, st, 0);
         if (s) return s;
         rec(2, st);
-        s = launch_splitk(p, st);
+        s = launch_splitk(sk_params(), st);
         if (s) return s;
         rec(3, st);
         // wave 1 on the pipe's stream: prefill rows' append, then the tcgen05 tiles
@@ -854,7 +880,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         int kernels = 4;
         if (p.n_comb) {
             rec(4, st);
-            s = launch_combine(p, st);
+            s = launch_combine(sk_params(), st);
             if (s) return s;
             rec(5, st);
             ++kernels;
@@ -911,7 +937,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             if (r) return r;
         }
         rec(2, sk_stream);
-        hg_status r = launch_splitk(p, sk_stream);
+        hg_status r = launch_splitk(sk_params(), sk_stream);
         if (r) return r;
         rec(3, sk_stream);
         ++kernels;
@@ -941,7 +967,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         rec(4, st);
         // right behind split-K on the same stream: a programmatic dependent launch
         // (resident early, waits for split-K's completion in griddepcontrol.wait)
-        s = launch_combine(p, st, sk_early);
+        s = launch_combine(sk_params(), st, sk_early);
         if (s) return s;
         rec(5, st);
         ++kernels;
@@ -1081,6 +1107,13 @@ static hg_attn_opts host_step_opts(const BatchView &v) {
     return ho;
 }
 
+static bool device_visible_host(const void *p) {
+    cudaPointerAttributes pa{};
+    const bool ok = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer;
+    cudaGetLastError();
+    return ok;
+}
+
 extern "C" hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
                                                         int32_t H_q, size_t *bytes) {
     if (!pool || !bytes) return fail(HG_E_INVALID, "NULL argument");
@@ -1188,6 +1221,8 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
         return e;
     };
     // one validated plan for the whole step (attention_impl reuses pool->plan)
+    static const bool no_zc = getenv("HG_E2E_NO_ZC") != nullptr;   // A/B: copy every row back
+    const bool pinned_out = !no_zc && device_visible_host(out_host);
     const hg_attn_opts ho = host_step_opts(v);
     s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan, true);
     if (s) return bail(s);
@@ -1197,7 +1232,22 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     if (!workspace || workspace_bytes < need)
         return bail(fail(HG_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need));
     uint8_t *ws_attn = w + in_bytes;
+    // Zero-copy result: when out_host is pinned, device-visible host memory, the rows
+    // written by split-K / the combine (every row on the HBM route, the decode rows on
+    // the tcgen05 route) are stored there by the kernels, and only the tcgen05 kernel's
+    // rows are copied back -- unless a prefill chunk is cut into key ranges (its rows
+    // then come from the combine after the tcgen05 copy-back was planned)
+    uint16_t *zc = nullptr;
+    if (pinned_out) {
+        cudaPointerAttributes pa{};
+        bool cut = false;
+        for (size_t k = 0; !cut && k < pool->plan.tok.size(); ++k)
+            cut = v.n[pool->plan.tok[k].req] > 1 && pool->plan.tok[k].nparts > 1 && !pool->plan.tc.empty();
+        if (!cut && cudaPointerGetAttributes(&pa, out_host) == cudaSuccess) zc = (uint16_t *)pa.devicePointer;
+        cudaGetLastError();
+    }
     StepPipe pipe;
+    pipe.zc_out = zc;
     pipe.in0 = pool->ev_in0;
     pipe.in1 = pool->ev_in1;
     pipe.side = pool->side_hi;
@@ -1228,11 +1278,11 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     } else if (pipe.used) {
         s = d2h(runs[1], pipe.side);
         if (!s) s = cuda_check(cudaEventRecord(pool->ev_d2h, pipe.side), "d2h record");
-        if (!s) s = d2h(runs[0], st);
+        if (!s && !pipe.zc_out) s = d2h(runs[0], st);   // zero-copy: split-K / the combine wrote them
         if (!s) s = cuda_check(cudaStreamWaitEvent(st, pool->ev_d2h, 0), "d2h wait");
-    } else {
+    } else if (!pipe.zc_out) {
         s = cuda_check(cudaMemcpyAsync(out_host, o_d, T * qrow, cudaMemcpyDeviceToHost, st), "D2H out");
-    }
+    }   // else zero-copy: every row came from split-K / the combine
     if (s) return s;
     const auto t_d2 = now();
     s = cuda_check(cudaStreamSynchronize(st), "stream sync");

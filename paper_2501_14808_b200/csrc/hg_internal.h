@@ -162,7 +162,7 @@ struct AttnParams {
 struct Plan {
     int R = 0, T = 0, W = 0;
     std::vector<ReqDev> reqs;
-    std::vector<int32_t> bt_flat;
+    int64_t n_bt = 0;                // flattened block ids (request i's at ReqDev.bt_off)
     std::vector<SkItem> sk;
     std::vector<TcItem> tc;
     std::vector<int32_t> tc_tok;

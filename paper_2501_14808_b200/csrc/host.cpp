@@ -105,9 +105,11 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
     int ng = 0, shared_write = -1;
     sc.n_shared = 0;
     uint64_t *bp = sc.bm_priv.data();
-    // pass A: shapes, id ranges; shared prefixes must form a trie (NEXT-3,
-    // DESIGN.md R23): a block shared by several rows sits at the same column in
-    // each, after the same id (hence after identical sequences, by induction).
+    // One pass over the block table (it is read once: ~300 KB for a C3-sized batch):
+    // shapes and id ranges; shared prefixes must form a trie (NEXT-3, R23):
+    // a block shared by several rows sits at the same column in each, after the same
+    // id (hence after identical sequences, by induction); every id is used by one
+    // row's private columns or by shared prefixes, never both (bitmap of ids taken).
     for (int i = 0; i < v.R; ++i) {
         const int64_t c = v.c[i], n = v.n[i], s = v.s[i];
         if (n < 1 || c < 0 || s < 0)
@@ -118,29 +120,47 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
         if (s > nb) return fail(HG_E_INVALID, "request %d: shared blocks %lld > blocks %d", i, (long long)s, nb);
         if (append && c < s * B && shared_write < 0) shared_write = i;
         const int32_t *row = v.bt + (int64_t)i * v.W;
-        int32_t lo = INT32_MAX, hi = INT32_MIN;
-        for (int col = 0; col < nb; ++col) {
-            lo = std::min(lo, row[col]);
-            hi = std::max(hi, row[col]);
-        }
-        if (nb > 0 && (lo < 0 || hi >= num_blocks))
-            return fail(HG_E_INVALID, "request %d: block id outside [0, %d)", i, num_blocks);
         for (int col = 0; col < s; ++col) {
             const int32_t b = row[col], parent = col ? row[col - 1] : -1;
+            if ((uint32_t)b >= (uint32_t)num_blocks)
+                return fail(HG_E_INVALID, "request %d: block id outside [0, %d)", i, num_blocks);
             const uint64_t t = sc.stamp[b];
             if ((t & ~0xFFFFFFFFull) == ep) {
                 if ((int)(t & 0xFFFFFFFFu) != col || sc.par[b] != parent)
                     return fail(HG_E_INVALID, "request %d shares block %d but not an identical prefix before it",
                                 i, b);
             } else {
+                if (bm_test(bp, (uint32_t)b))
+                    return fail(HG_E_INVALID, "block %d of request %d is also used by another row or prefix", b, i);
                 sc.stamp[b] = ep | (uint32_t)col;
                 sc.par[b] = parent;
                 sc.gid[b] = -1;
                 sc.cnt[b] = 0;
                 sc.node[b] = -1;
-                bm_set(bp, (uint32_t)b);  // shared ids are "taken" for pass C
+                bm_set(bp, (uint32_t)b);
                 ++sc.n_shared;
             }
+        }
+        // private columns: range check and test-and-set, branch-free per id
+        uint32_t bad = 0;
+        uint64_t seen = 0;
+        for (int col = (int)s; col < nb; ++col) {
+            const uint32_t b = (uint32_t)row[col];
+            bad |= (uint32_t)(b >= (uint32_t)num_blocks);
+            const uint32_t bb = b < (uint32_t)num_blocks ? b : 0u;
+            uint64_t &w = bp[bb >> 6];
+            const uint64_t bit = 1ull << (bb & 63);
+            seen |= w & bit;
+            w |= bit;
+        }
+        if (bad) return fail(HG_E_INVALID, "request %d: block id outside [0, %d)", i, num_blocks);
+        if (seen) {
+            for (int col = (int)s; col < nb; ++col)   // name the offending id (error path only)
+                for (int k = (int)s; k < col; ++k)
+                    if (row[k] == row[col])
+                        return fail(HG_E_INVALID, "block %d of request %d is also used by another row or prefix",
+                                    row[col], i);
+            return fail(HG_E_INVALID, "a private block of request %d is also used by another row or prefix", i);
         }
         if (s > 0) {   // prefix group = identical whole shared sequence = same last shared block
             int32_t &g = sc.gid[row[s - 1]];
@@ -149,17 +169,6 @@ hg_status validate(const BatchView &v, int B, int num_blocks, int num_q_heads, i
                 sc.owners.push_back(i);
             }
             sc.group[i] = g;
-        }
-    }
-    // pass C: private blocks are used exactly once and never inside any shared prefix
-    for (int i = 0; i < v.R; ++i) {
-        const int32_t *row = v.bt + (int64_t)i * v.W;
-        const int nb = ceil_div((int64_t)v.c[i] + v.n[i], B);
-        for (int col = v.s[i]; col < nb; ++col) {
-            const uint32_t b = (uint32_t)row[col];
-            if (bm_test(bp, b))
-                return fail(HG_E_INVALID, "block %d of request %d is also used by another row or prefix", b, i);
-            bm_set(bp, b);
         }
     }
     if (shared_write >= 0)
@@ -275,11 +284,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         nbt += ceil_div((int64_t)v.c[i] + v.n[i], B);
     }
     p->T = (int)T;
-    p->bt_flat.resize((size_t)nbt);
-    for (int i = 0; i < v.R; ++i) {
-        const int nb = ceil_div((int64_t)v.c[i] + v.n[i], B);
-        memcpy(p->bt_flat.data() + p->reqs[i].bt_off, v.bt + (int64_t)i * v.W, sizeof(int32_t) * (size_t)nb);
-    }
+    p->n_bt = nbt;   // the block ids themselves go straight from the batch into the descriptor image
     p->tok.resize((size_t)T);
     for (int i = 0; i < v.R; ++i)
         for (int j = 0; j < v.n[i]; ++j) p->tok[(size_t)p->reqs[i].cu_q + j] = TokDev{-1, 1, i, 0};
@@ -603,7 +608,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     // ---- workspace layout ----------------------------------------------------
     size_t off = 0;
     p->off_reqs = off;  off = align_up(off + sizeof(ReqDev) * p->reqs.size(), 16);
-    p->off_bt = off;    off = align_up(off + sizeof(int32_t) * p->bt_flat.size(), 16);
+    p->off_bt = off;    off = align_up(off + sizeof(int32_t) * (size_t)p->n_bt, 16);
     p->off_sk = off;    off = align_up(off + sizeof(SkItem) * p->sk.size(), 16);
     p->off_tc = off;    off = align_up(off + sizeof(TcItem) * p->tc.size(), 16);
     p->off_rows = off;  off = align_up(off + sizeof(int32_t) * p->tc_tok.size(), 16);

@@ -339,6 +339,30 @@ def test_e2e_host_step_matches_device_path(name):
         compare(spec, wl, check_lse=False, tag=" (host step)")
 
 
+@pytest.mark.parametrize("name", ["toy_a", "c2", "c3"])
+def test_e2e_host_step_pageable_output(name):
+    """With a pinned out_host the kernels store split-K's / the combine's rows into it
+    directly (zero-copy result, the test above); a pageable out_host takes the copy
+    path -- each equal to the device path on the same plan, bit for bit."""
+    import paper_2501_14808_b200 as hg
+    spec = _e2e_spec(name)
+    wl = make(spec)
+    torch.cuda.synchronize()
+    qh, kh, vh = (x.cpu().pin_memory() for x in (wl.q, wl.k_new, wl.v_new))
+    ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
+                     device="cuda")
+    mixed = any(r.n > 1 for r in spec.requests) and any(r.n == 1 for r in spec.requests)
+    for pinned in (False, True):
+        oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16)
+        oh = oh.pin_memory() if pinned else oh
+        hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
+        # a mixed batch on the tcgen05 route (its tiles consume the second input wave);
+        # the appended values are the same every call, so the cache needs no reset
+        wl.step(hg.make_opts(route=1) if mixed else None)
+        torch.cuda.synchronize()
+        assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), pinned
+
+
 def test_e2e_host_step_errors_leave_outputs_untouched():
     """hg_hybrid_step_host starts the decode rows' copies before validating; an
     invalid batch must still return its status with out_host and the pool untouched."""

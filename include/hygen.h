@@ -160,7 +160,11 @@ typedef struct {
                                    next to the decode pass, else the tcgen05 route; 1: tcgen05 route
                                    (prefill chunks and shared-prefix nodes on tcgen05 tiles); 2: HBM
                                    route (everything on the split-K kernel, prefix nodes as stacked-row
-                                   split-K items; same as disable_tc for the prefill rows) */
+                                   split-K items; same as disable_tc for the prefill rows); 3: prefill
+                                   chunks on tcgen05 tiles, shared-prefix nodes as stacked-row split-K
+                                   items (G_q <= 16; above, on tiles as in route 1) -- no tile writes
+                                   partials, so split-K merges every partial itself (the host step's
+                                   route for mixed batches) */
 } hg_attn_opts;
 
 /* Bytes of device workspace hg_hybrid_attention needs for this batch. */

@@ -267,7 +267,7 @@ def make_opts(split_tokens=0, disable_prefix_pass=False, disable_tc=False, num_s
     rope: hg_rope applied in the hg_hybrid_step prologue (kept alive by the returned struct)."""
     o = hg_attn_opts(split_tokens, int(disable_prefix_pass), int(disable_tc), num_sms)
     o.disable_prefill_split = int(disable_prefill_split)
-    o.route = int(route)   # 0 automatic, 1 tcgen05 route, 2 HBM route
+    o.route = int(route)   # 0 automatic, 1 tcgen05 route, 2 HBM route, 3 tcgen05 prefill + split-K prefix nodes
     if rope is not None:
         o._rope_ref = rope
         o.rope = ctypes.pointer(rope)

@@ -878,7 +878,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (!s) s = cuda_check(cudaStreamWaitEvent(st, pipe->tc_done, 0), "tc wait");
         if (s) return s;
         int kernels = 4;
-        if (p.n_comb) {
+        if (p.n_comb && !p.sk_cnt) {   // (sk_cnt: split-K merged every partial itself)
             rec(4, st);
             s = launch_combine(sk_params(), st);
             if (s) return s;
@@ -1095,15 +1095,17 @@ extern "C" hg_status hg_last_plan_stats(const hg_kv_pool *pool, hg_plan_stats *o
 static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 // The host step's plan options: with both prefill chunks and decode rows, the
-// tcgen05 route (its prefill tiles consume the second input wave on their own
+// prefill chunks on tcgen05 tiles (they consume the second input wave on their own
 // stream while split-K runs on the first, which hides most of the PCIe upload;
 // the HBM route would put both waves' rows into one split-K launch behind the
-// whole upload).
+// whole upload) and shared-prefix nodes on split-K (route 3), so split-K merges
+// every decode row's partials itself and its final rows leave as it runs.
 static hg_attn_opts host_step_opts(const BatchView &v) {
     bool has_pre = false, has_dec = false;
     for (int i = 0; i < v.R; ++i) (v.n[i] > 1 ? has_pre : has_dec) = true;
     hg_attn_opts ho{};
-    ho.route = has_pre && has_dec ? 1 : 0;
+    static const bool nodes_tc = getenv("HG_E2E_NODES_TC") != nullptr;   // A/B: prefix nodes on tcgen05 (route 1)
+    ho.route = has_pre && has_dec ? (nodes_tc ? 1 : 3) : 0;
     return ho;
 }
 

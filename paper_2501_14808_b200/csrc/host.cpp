@@ -353,7 +353,11 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         // prefill rows on mma.sync split-K items at ~300 TFLOP/s vs the decode pass at ~6.5 TB/s
         tc_on = !(dec_bytes > 0 && pre_flops / 300e12 < 0.5 * dec_bytes / 6.5e12);
     }
-    if (!tc_on && !sc.nodes.empty()) {
+    // route 3: prefill chunks on tcgen05 tiles, shared-prefix nodes as stacked-row
+    // split-K items (G_q <= 16) -- so no tcgen05 item writes partials and split-K
+    // merges every partial itself (no combine kernel after it)
+    const bool nodes_tc = tc_on && !(o.route == 3 && G <= kSkRows);
+    if (!nodes_tc && !sc.nodes.empty()) {
         // HBM route: a node pays for its extra partials (every member row gets merged)
         // only when the members would re-read a large share of the KV bytes: a prefix
         // re-read by its members mostly hits L2.  Measured: c2_nested (re-reads 40 %
@@ -363,7 +367,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         for (int i = 0; i < v.R; ++i) uniq += (double)v.c[i] + v.n[i] - (double)v.s[i] * B;
         uniq += (double)sc.n_shared * B;
         for (const Scratch::Node &nd : sc.nodes) reread += (double)(nd.nm - 1) * (nd.e - nd.a) * B;
-        if (G > kSkRows || (o.route == 0 && reread <= 0.25 * uniq)) {
+        if (G > kSkRows || ((o.route == 0 || o.route == 3) && reread <= 0.25 * uniq)) {
             std::fill(sc.pre_end.begin(), sc.pre_end.end(), 0);
             std::fill(sc.npre.begin(), sc.npre.end(), 0);
             sc.nodes.clear();
@@ -376,7 +380,8 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         int64_t n256 = 0;
         for (int i = 0; i < v.R; ++i)
             if (v.n[i] > 1) n256 += (int64_t)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows);
-        for (const Scratch::Node &nd : sc.nodes) n256 += (int64_t)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows);
+        if (nodes_tc)
+            for (const Scratch::Node &nd : sc.nodes) n256 += (int64_t)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows);
         if (n256 >= o.num_sms) ipr = 2 * kTcRows;
         // Long prefill items on an unbalanced grid (a small chunk at a long prompt:
         // one item = one CTA walking thousands of keys while the other SMs run out
@@ -416,7 +421,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
                     total_us += (double)H_kv * ceil_div((int64_t)v.n[i] * G, 2 * kTcRows) *
                                 ceil_div((int64_t)v.c[i] + v.n[i], kTcKeys) * kTileUs;
             for (const Scratch::Node &nd : sc.nodes)
-                total_us += (double)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows) *
+                if (nodes_tc) total_us += (double)H_kv * ceil_div((int64_t)nd.nm * G, 2 * kTcRows) *
                             ceil_div((int64_t)(nd.e - nd.a) * B, kTcKeys) * kTileUs;
             const double target_us = std::max({sk_us, total_us / o.num_sms, 8 * kTileUs});
             bool any = false;
@@ -569,7 +574,7 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
         }
         for (const Scratch::Node &nd : sc.nodes) {
             const int rows = nd.nm * G;
-            if (!tc_on) {   // HBM route: 16-row split-K items over the node's keys (16 / G_q members each)
+            if (!nodes_tc) {   // HBM route / route 3: 16-row split-K items over the node's keys (16 / G_q members each)
                 const int mpi = kSkRows / G;
                 for (int m0 = 0; m0 < nd.nm; m0 += mpi) {
                     const int nmm = std::min(mpi, nd.nm - m0);
@@ -616,9 +621,9 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
     p->off_comb = off;  off = align_up(off + sizeof(int32_t) * p->comb.size(), 16);
     p->off_tcoff = off; off = align_up(off + sizeof(int32_t) * p->tc_off.size(), 16);
     p->off_skoff = off; off = align_up(off + sizeof(int32_t) * p->sk_off.size(), 16);
-    // no tcgen05 items: split-K merges the partials itself (arrival counters, zero in
-    // the uploaded image) and no combine kernel runs
-    p->sk_merge = p->tc.empty() && !p->comb.empty();
+    // no tcgen05 item writes partials: split-K merges them itself (arrival counters,
+    // zero in the uploaded image) and no combine kernel runs
+    p->sk_merge = !p->comb.empty() && std::none_of(p->tc.begin(), p->tc.end(), [](const TcItem &it) { return it.part >= 0; });
     p->off_cnt = off;   off = align_up(off + (p->sk_merge ? sizeof(uint32_t) * (size_t)T * H_kv : 0), 16);
     p->off_exit = off;  off = align_up(off + 16, 16);   // split-K's entry / exit tickets (folded barriers)
     p->desc_bytes = off;   // the descriptor image lives in a library-owned device slot (api.cpp stage_desc)

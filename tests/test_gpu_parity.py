@@ -136,7 +136,7 @@ def test_fuzz(seed):
     compare(spec, wl)
 
 
-@pytest.mark.parametrize("variant", ["default", "no_tc", "split64", "no_prefix", "tc_route", "hbm_route"])
+@pytest.mark.parametrize("variant", ["default", "no_tc", "split64", "no_prefix", "tc_route", "hbm_route", "route3"])
 @pytest.mark.parametrize("seed", range(8))
 def test_plan_variants(variant, seed):
     import paper_2501_14808_b200 as hg
@@ -144,7 +144,7 @@ def test_plan_variants(variant, seed):
     spec = make_fuzz(100 + seed)
     opts = {"default": None, "no_tc": hg.make_opts(disable_tc=True), "split64": hg.make_opts(split_tokens=64),
             "no_prefix": hg.make_opts(disable_prefix_pass=True), "tc_route": hg.make_opts(route=1),
-            "hbm_route": hg.make_opts(route=2)}[variant]
+            "hbm_route": hg.make_opts(route=2), "route3": hg.make_opts(route=3)}[variant]
     wl = make(spec)
     wl.append()
     wl.attention(opts)
@@ -324,13 +324,14 @@ def test_e2e_host_step_matches_device_path(name):
     oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16).pin_memory()
     ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
                      device="cuda")
-    # with both prefill chunks and decode rows the host step takes the tcgen05 route
-    # (its prefill tiles consume the second input wave): the same plan on the device path
+    # with both prefill chunks and decode rows the host step puts the prefill chunks on
+    # tcgen05 tiles (they consume the second input wave) and shared prefixes on split-K
+    # (route 3): the same plan on the device path
     mixed = any(r.n > 1 for r in spec.requests) and any(r.n == 1 for r in spec.requests)
     for rep in range(2):   # second call: events and streams reused
         hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
         k_after, v_after = wl.k_cache.clone(), wl.v_cache.clone()
-        wl.step(hg.make_opts(route=1) if mixed else None)
+        wl.step(hg.make_opts(route=3) if mixed else None)
         torch.cuda.synchronize()
         assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), rep
         assert torch.equal(k_after, wl.k_cache) and torch.equal(v_after, wl.v_cache), rep
@@ -356,9 +357,9 @@ def test_e2e_host_step_pageable_output(name):
         oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16)
         oh = oh.pin_memory() if pinned else oh
         hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)
-        # a mixed batch on the tcgen05 route (its tiles consume the second input wave);
-        # the appended values are the same every call, so the cache needs no reset
-        wl.step(hg.make_opts(route=1) if mixed else None)
+        # a mixed batch: the host step's route 3 (its tiles consume the second input
+        # wave); the appended values are the same every call, so the cache needs no reset
+        wl.step(hg.make_opts(route=3) if mixed else None)
         torch.cuda.synchronize()
         assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), pinned
 
@@ -383,7 +384,7 @@ def test_e2e_host_step_errors_leave_outputs_untouched():
     torch.cuda.synchronize()
     assert torch.all(oh == 7.0) and torch.equal(k_before, wl.k_cache)
     hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, oh, ws)   # and the next valid call works
-    wl.step(hg.make_opts(route=1))   # toy_a is mixed: the host step's tcgen05 route
+    wl.step(hg.make_opts(route=3))   # toy_a is mixed: the host step's route 3
     torch.cuda.synchronize()
     assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16))
 
@@ -574,7 +575,7 @@ def test_nested_fuzz(seed):
     assert hg_stats(wl)["kv_bytes_unique"] == _unique_kv_bytes(spec, wl.lay)
 
 
-@pytest.mark.parametrize("variant", ["no_tc", "no_prefix", "split64", "tc_route", "hbm_route"])
+@pytest.mark.parametrize("variant", ["no_tc", "no_prefix", "split64", "tc_route", "hbm_route", "route3"])
 @pytest.mark.parametrize("seed", range(6))
 def test_nested_plan_variants(variant, seed):
     import paper_2501_14808_b200 as hg
@@ -582,7 +583,7 @@ def test_nested_plan_variants(variant, seed):
     spec = make_fuzz_nested(100 + seed)
     opts = {"no_tc": hg.make_opts(disable_tc=True), "split64": hg.make_opts(split_tokens=64),
             "no_prefix": hg.make_opts(disable_prefix_pass=True), "tc_route": hg.make_opts(route=1),
-            "hbm_route": hg.make_opts(route=2)}[variant]
+            "hbm_route": hg.make_opts(route=2), "route3": hg.make_opts(route=3)}[variant]
     wl = make(spec)
     wl.append()
     wl.attention(opts)

@@ -85,6 +85,40 @@ def test_window_world1(zero_copy):
     comm.close()
 
 
+def test_window_world1_sharded_hbm_step_two_launches():
+    """The sharded HBM-route step (decode-dominated batch with split-K partials and a
+    shared-prefix group): two launches -- the append beside split-K, which runs the entry
+    barrier in its first CTA, merges its own partials and runs the exit barrier in its
+    last CTA -- equal to the plain fused step bit for bit, call after call (epochs)."""
+    _cuda()
+    import paper_2501_14808_b200 as hg
+    from paper_2501_14808_b200.harness import Workload
+    from synth.configs import BatchSpec, Request
+    spec = BatchSpec("hbm_tp", 8, 1, 128, 16, 3,
+                     [Request(0, 40, False)] +
+                     [Request(1500 + 211 * k, 1, True, group=0, prefix_tokens=1024) for k in range(6)] +
+                     [Request(900 + 377 * k, 1, False) for k in range(10)])
+    wl = Workload(spec)
+    wl.step()
+    torch.cuda.synchronize()
+    ref = wl.out.clone()
+    st = hg.hg_last_plan_stats(wl.pool)
+    assert st["tc_tiles"] == 0 and st["combine_rows"] > 0, st   # HBM route, partials merged
+    comm = hg.Comm(None, 0, 1, torch.cuda.current_device())
+    comm.hg_comm_window_open([comm.hg_comm_window_create(spec.T * spec.H_q * spec.d * 2)])
+    ws = torch.empty(hg.hg_hybrid_attention_tp_workspace_size(wl.pool, comm, wl.batch, spec.H_q),
+                     dtype=torch.uint8, device="cuda")
+    win = comm.window((spec.T, spec.H_q, spec.d))
+    for zero_copy in (True, False, True):
+        out = win if zero_copy else torch.empty_like(wl.out)
+        out.fill_(0)
+        hg.hg_hybrid_step_tp(wl.pool, comm, wl.batch, spec.H_q, wl.q, wl.k_new, wl.v_new, out, ws)
+        torch.cuda.synchronize()
+        assert hg.hg_last_plan_stats(wl.pool)["kernels"] == 2   # append + split-K (no combine kernel)
+        assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    comm.close()
+
+
 def test_peer_only_comm_without_window_rejects_world2():
     _cuda()
     import paper_2501_14808_b200 as hg

@@ -142,7 +142,9 @@ typedef struct {
     int32_t num_sms;            /* 0: device SM count */
     void *events[6];            /* profiling: cudaEvent_t (or NULL) recorded on the stream right before /
                                    after the tcgen05 kernel [0,1], the split-K kernel [2,3] and the
-                                   combine kernel [4,5] (bench.py's per-kernel roofline timing) */
+                                   combine kernel [4,5] (bench.py's per-kernel roofline timing); when
+                                   split-K merges the partials itself, [4,5] are both recorded where the
+                                   combine would run (after every attention kernel) */
     void *debug_trace;          /* NULL, or device int64[4096]: clock64 stamps of tcgen05 CTA 0's pipeline
                                    events (kernel development aid; see tc_attn.cu) */
     const hg_rope *rope;        /* hg_hybrid_step only (NULL: none): q and k_new are pre-rotary; the

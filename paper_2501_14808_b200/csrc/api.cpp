@@ -797,6 +797,8 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     p.part_o = (float *)(w + plan.off_part_o);
     p.part_lse = (float *)(w + plan.off_part_lse);
     p.H_q = H_q;
+    p.T = plan.T;
+    p.n_slots = plan.n_slots;
     p.H_kv = pool->desc.num_kv_heads;
     p.G_q = H_q / p.H_kv;
     p.d = pool->desc.head_dim;
@@ -884,6 +886,9 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
             if (s) return s;
             rec(5, st);
             ++kernels;
+        } else if (p.n_comb) {   // merged in split-K: the combine events mark the kernels' joint end
+            rec(4, st);
+            rec(5, st);
         }
         hg_plan_stats &ls = pool->last;
         ls.tc_tiles = p.n_tc;
@@ -971,6 +976,9 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
         if (s) return s;
         rec(5, st);
         ++kernels;
+    } else if (p.n_comb) {   // merged in split-K: the combine events mark the kernels' joint end
+        rec(4, st);
+        rec(5, st);
     }
     if (sk_early && !(outs && outs->wait_cnt)) {   // the call ends after the append that ran beside split-K
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");

@@ -8,6 +8,23 @@
 
 #include "hygen.h"
 
+// Device-side invariant checks (index ranges, arrival counts): compiled in only for the
+// checking build (HG_NVCC_DEFS=-DHG_CHECKS, tools/gpurun/r2_checks.sh) -- a failed check
+// prints its condition and traps (sticky HG_E_CUDA), so parity tests fail on it.
+#ifdef HG_CHECKS
+#define HG_DCHECK(c)                                                                           \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("HG_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);                   \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define HG_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace hg {
 
 constexpr int kBlock = 16;        // KV block size B handled by the kernels
@@ -103,6 +120,8 @@ struct AttnParams {
     float *part_o;             // [slots][d] normalised partial outputs
     float *part_lse;           // [slots] log2-domain LSE of each partial (-inf: empty)
     int32_t H_q, H_kv, G_q, d;
+    int32_t T;                 // batch tokens (rows of q / O)
+    int64_t n_slots;           // partial slots in part_o / part_lse
     int32_t n_sk, n_tc, n_comb;
     int32_t tc_ctas;           // persistent tcgen05 grid (<= n_tc)
     const int32_t *tc_off;     // [tc_ctas + 1]: CTA b processes tc items [tc_off[b], tc_off[b+1])

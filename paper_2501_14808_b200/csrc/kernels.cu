@@ -446,6 +446,8 @@ __device__ __forceinline__ void combine_row(const AttnParams &p, const int t, co
     const int G = p.G_q;
     const TokDev tk = p.tok[t];
     const int64_t base = tk.base + (int64_t)g * tk.nparts * G;
+    HG_DCHECK(t >= 0 && t < p.T && tk.nparts >= 1 && tk.base >= 0 && g < p.H_kv && hl < G);
+    HG_DCHECK(base + (int64_t)(tk.nparts - 1) * G + hl < p.n_slots);
     // the parts' LSEs are loaded once, lane s holding parts s, s + 32, ...; max and
     // sum by warp shuffles (no chain of dependent loads per part)
     float lv[2];
@@ -522,6 +524,7 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
             const int x = it.hl0 + r;
             const int t = it.mode ? p.tc_tok[it.j0 + x / G] : rq.cu_q + it.j0 + x / G;
             const int h = g * G + x % G;
+            HG_DCHECK(t >= 0 && t < p.T && h < p.H_q);
             val = *reinterpret_cast<const uint4 *>(p.q + ((int64_t)t * p.H_q + h) * D + ch * 8);
         }
         *reinterpret_cast<uint4 *>(sQ + swz<D>(r, ch)) = val;
@@ -764,6 +767,7 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
                 if (p.lse && part8 == 0) p.lse[(int64_t)t * p.H_q + h] = lse2 * 0.69314718055994531f;
             } else {
                 const int64_t slot = base + (int64_t)it.part * G + (x % G);
+                HG_DCHECK(slot >= 0 && slot < p.n_slots && it.part < p.tok[t].nparts);
                 float *dst = p.part_o + slot * D + part8 * 4;
 #pragma unroll
                 for (int k = 0; k < PER / 4; ++k)
@@ -790,7 +794,9 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
             const int u = u0 + threadIdx.x;
             const int t = it.mode ? p.tc_tok[it.j0 + u] : rq.cu_q + it.j0 + u;
             const int need = p.tok[t].nparts * (G > kSkRows ? (G + kSkRows - 1) / kSkRows : 1);
-            if (atomicAdd(p.sk_cnt + (int64_t)t * p.H_kv + g, 1u) == (unsigned)need - 1) atomicOr(&s_win, 1u << threadIdx.x);
+            const unsigned old = atomicAdd(p.sk_cnt + (int64_t)t * p.H_kv + g, 1u);
+            HG_DCHECK(old < (unsigned)need);   // no more arrivals than the token has parts
+            if (old == (unsigned)need - 1) atomicOr(&s_win, 1u << threadIdx.x);
         }
         __syncthreads();
         uint32_t win = s_win;
@@ -867,7 +873,9 @@ splitk_kernel(const AttnParams p) {
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
-            s_last = atomicAdd(p.exit_ticket, 1u) == gridDim.x * gridDim.y - 1;
+            const unsigned tk = atomicAdd(p.exit_ticket, 1u);
+            HG_DCHECK(tk < gridDim.x * gridDim.y);
+            s_last = tk == gridDim.x * gridDim.y - 1;
         }
         __syncthreads();
         if (s_last && threadIdx.x < 32) {

@@ -540,6 +540,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             // Q row -> smem, K-major 128B swizzle: half h, row r at h*16K + r*128, chunk c at (c ^ (r&7))*16.
             // The previous item's QKs are complete: this warpgroup waited its ODONE.
             if (t < ntiles) {
+                HG_DCHECK(!valid || (row.t >= 0 && row.t < p.T && row.h < p.H_q));
                 const uint4 *src = reinterpret_cast<const uint4 *>(p.q + ((int64_t)row.t * p.H_q + row.h) * D);
                 const uint32_t qb = sQ + t * L::kQ + r * 128;
 #pragma unroll
@@ -691,6 +692,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                         }
                     } else {
                         const int64_t slot = base + (int64_t)it.part * G + (row.h % G);
+                        HG_DCHECK(slot >= 0 && slot < p.n_slots);
                         float4 *dst = reinterpret_cast<float4 *>(p.part_o + slot * D + c * 32);
 #pragma unroll
                         for (int e = 0; e < 8; ++e)

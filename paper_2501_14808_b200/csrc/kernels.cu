@@ -252,6 +252,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
 }
+// 16 bytes, or 16 zero bytes when !valid (src-size 0: nothing is read from src)
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -516,19 +520,6 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
     uint8_t *sQ = smem;
     uint8_t *sKV = smem + SkSmem<D>::kQ;
 
-    // ---- Q tile (16 rows, zero padded) -> smem (swizzled) --------------------
-    for (int idx = threadIdx.x; idx < kSkRows * NCH; idx += blockDim.x) {
-        const int r = idx / NCH, ch = idx % NCH;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (r < nrows) {
-            const int x = it.hl0 + r;
-            const int t = it.mode ? p.tc_tok[it.j0 + x / G] : rq.cu_q + it.j0 + x / G;
-            const int h = g * G + x % G;
-            HG_DCHECK(t >= 0 && t < p.T && h < p.H_q);
-            val = *reinterpret_cast<const uint4 *>(p.q + ((int64_t)t * p.H_q + h) * D + ch * 8);
-        }
-        *reinterpret_cast<uint4 *>(sQ + swz<D>(r, ch)) = val;
-    }
     // per-row causal limit (exclusive), rows this lane owns: r0 = lane/4, r1 = r0 + 8
     const int ra = lane >> 2, rb = ra + 8;
     auto row_lim = [&](int r) -> int {
@@ -581,11 +572,29 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
             cp_async16(dv + swz<D>(r, ch), gv + r * D + ch * 8);
         }
     };
+    // ---- Q tile (16 rows, zero padded) -> smem (swizzled), asynchronously: its
+    // loads are in flight together with the first K/V blocks' (one cp.async group
+    // ahead of the prologue's), so an item's start-up pays one memory latency
+    const uint32_t sQ_w = smem_u32(sQ);
+    for (int idx = threadIdx.x; idx < kSkRows * NCH; idx += blockDim.x) {
+        const int r = idx / NCH, ch = idx % NCH;
+        const uint16_t *src = p.q;
+        if (r < nrows) {
+            const int x = it.hl0 + r;
+            const int t = it.mode ? p.tc_tok[it.j0 + x / G] : rq.cu_q + it.j0 + x / G;
+            const int h = g * G + x % G;
+            HG_DCHECK(t >= 0 && t < p.T && h < p.H_q);
+            src = p.q + ((int64_t)t * p.H_q + h) * D + ch * 8;
+        }
+        cp_async16_zfill(sQ_w + swz<D>(r, ch), src, r < nrows);
+    }
+    cp_async_commit();
 #pragma unroll
     for (int b = 0; b < kSkStages - 1; ++b) {   // prologue: blocks 0 .. S-2 in flight
         if (b < nblk_w) issue(b, b);
         cp_async_commit();
     }
+    cp_async_wait<kSkStages - 1>();   // the Q group (the prologue's blocks may still be in flight)
     __syncthreads();  // Q tile visible
 
     // Q A-fragments (all warps hold the same 16 x D tile)

@@ -1064,7 +1064,9 @@ def run_tp(args, spec, rank, world, dev, peaks, peak_kind):
             "roofline": roofline,
             "plan": st,
             "communicator": comm_kind,
-            "gpu_launches": (st["kernels"] + 1) * args.steps,  # + the exit barrier (the entry one rides in the append)
+            # the plan's kernels (append + split-K on the HBM route, whose first / last CTA run
+            # the entry / exit barriers); the tcgen05 route adds the exit barrier kernel
+            "gpu_launches": (st["kernels"] + (1 if st["tc_tiles"] else 0)) * args.steps,
             "e2e": {"value": spec.T * args.steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2 * world,
                     "d2h_bytes_per_step": spec.T * spec.H_q * spec.d * 2, "ms_per_step": e2e_s / args.steps * 1e3,

@@ -533,7 +533,10 @@ hg_status build_plan(const BatchView &v, int H_q, int H_kv, int d, const PlanOpt
             // 0.451 -> 0.443 ms, its G = 8 shard 0.107 -> 0.099 ms; c2 / c3 within
             // 0.5 %); small batches keep the 256-key floor.  HG_SK_WAVES: A/B knob.
             static const double waves = getenv("HG_SK_WAVES") ? std::max(0.25, atof(getenv("HG_SK_WAVES"))) : 1.0;
-            const int64_t target = (int64_t)std::llround(o.num_sms * 3 * waves);
+            // split-K CTAs resident per SM (3 at the kernel's launch bounds); HG_SK_CTAS_PER_SM:
+            // A/B knob for builds with a deeper ring (HG_SK_STAGES)
+            static const int per_sm = getenv("HG_SK_CTAS_PER_SM") ? std::max(1, atoi(getenv("HG_SK_CTAS_PER_SM"))) : 3;
+            const int64_t target = (int64_t)std::llround(o.num_sms * per_sm * waves);
             int64_t ct = (total_keys + target - 1) / std::max<int64_t>(target, 1);
             ct = std::max<int64_t>(ct, 256);
             chunk_tok = (int)((ct + B - 1) / B * B);

@@ -828,7 +828,10 @@ __device__ __forceinline__ void splitk_item(const AttnParams &p, const SkItem it
 // Persistent split-K grid: CTA (b, g) runs the items [sk_off[b], sk_off[b+1]) for
 // KV head g (stream-K plans give every CTA the same number of KV blocks).
 template <int D>
-__global__ void __launch_bounds__(kSkWarps * 32, 3)   // 3 CTAs per SM: <= 170 registers
+#ifndef HG_SK_MIN_CTAS
+#define HG_SK_MIN_CTAS 3
+#endif
+__global__ void __launch_bounds__(kSkWarps * 32, HG_SK_MIN_CTAS)   // 3 CTAs per SM: <= 170 registers
 splitk_kernel(const AttnParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     // the combine kernel behind this one (programmatic dependent launch) may be

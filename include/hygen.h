@@ -221,6 +221,25 @@ HG_API hg_status hg_hybrid_step(hg_kv_pool *pool, const hg_batch *batch, int32_t
 HG_API hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
                               const void *q_host, const void *k_new_host, const void *v_new_host,
                               void *out_host, void *workspace, size_t workspace_bytes, void *stream);
+/* Pipelined use of the host step (a serving loop planning the next batch while the
+ * GPU runs the current one):
+ *   hg_hybrid_step_host_plan validates and plans `batch` for the NEXT host step into a
+ *   second plan slot of the pool (pure host work; same errors as the step's
+ *   validation; overwrites any earlier plan-ahead).
+ *   hg_hybrid_step_host_async is hg_hybrid_step_host without the final synchronise:
+ *   it returns once everything is queued on `stream`; out_host is valid, and the
+ *   host input buffers may be reused, only after `stream` completes.  When the
+ *   pool holds a plan-ahead for this same `batch` pointer and num_q_heads it is used
+ *   instead of planning again -- the caller must not change the batch's arrays in
+ *   between (nothing checks their contents).  Either way the plan-ahead is consumed.
+ * A loop: plan(b0); for k: async(b_k); plan(b_{k+1}); synchronise(stream); ... keeps
+ * each step's input upload after the previous step's result (the data dependency of
+ * autoregressive decoding) and takes the validation and planning off the GPU's
+ * critical path. */
+HG_API hg_status hg_hybrid_step_host_plan(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads);
+HG_API hg_status hg_hybrid_step_host_async(hg_kv_pool *pool, const hg_batch *batch, int32_t num_q_heads,
+                                           const void *q_host, const void *k_new_host, const void *v_new_host,
+                                           void *out_host, void *workspace, size_t workspace_bytes, void *stream);
 HG_API hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, const hg_batch *batch,
                                              int32_t num_q_heads, size_t *bytes);
 

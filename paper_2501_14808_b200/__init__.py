@@ -90,6 +90,8 @@ _SIGS = {
     "hg_hybrid_attention": ([P, P, i32, P, P, P, P, ctypes.c_size_t, P], i32),
     "hg_hybrid_attention_ex": ([P, P, i32, P, P, P, P, ctypes.c_size_t, P, P], i32),
     "hg_hybrid_step_host": ([P, P, i32, P, P, P, P, P, ctypes.c_size_t, P], i32),
+    "hg_hybrid_step_host_async": ([P, P, i32, P, P, P, P, P, ctypes.c_size_t, P], i32),
+    "hg_hybrid_step_host_plan": ([P, P, i32], i32),
     "hg_hybrid_step": ([P, P, i32, P, P, P, P, P, P, ctypes.c_size_t, P, P], i32),
     "hg_hybrid_step_host_workspace_size": ([P, P, i32, P], i32),
     "hg_batch_indices": ([P, P, P, P, P, P], i32),
@@ -312,6 +314,20 @@ def hg_hybrid_step_host(pool: KVPool, batch: Batch, num_q_heads: int, q_host, k_
     _check(lib().hg_hybrid_step_host(pool.h, batch.ref(), num_q_heads, _ptr(q_host), _ptr(k_host), _ptr(v_host),
                                      _ptr(out_host), _ptr(workspace), workspace.numel() * workspace.element_size(),
                                      _stream_ptr(stream)))
+
+
+def hg_hybrid_step_host_async(pool: KVPool, batch: Batch, num_q_heads: int, q_host, k_host, v_host, out_host,
+                              workspace, stream=None) -> None:
+    """The host step without its final synchronise (out_host valid once `stream` completes);
+    uses the pool's plan-ahead for this batch if hg_hybrid_step_host_plan made one."""
+    _check(lib().hg_hybrid_step_host_async(pool.h, batch.ref(), num_q_heads, _ptr(q_host), _ptr(k_host),
+                                           _ptr(v_host), _ptr(out_host), _ptr(workspace),
+                                           workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+
+
+def hg_hybrid_step_host_plan(pool: KVPool, batch: Batch, num_q_heads: int) -> None:
+    """Validate and plan `batch` for the next host step (host work only)."""
+    _check(lib().hg_hybrid_step_host_plan(pool.h, batch.ref(), num_q_heads))
 
 
 def hg_batch_indices(pool: KVPool, batch: Batch):

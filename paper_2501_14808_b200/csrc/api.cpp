@@ -42,6 +42,11 @@ struct hg_kv_pool {
     bool tmap_ok = false;
     hg_plan_stats last{};
     Plan plan;  // reused storage
+    // host step planned ahead (hg_hybrid_step_host_plan): the plan, for which batch
+    Plan plan_ahead;
+    bool ahead_ok = false;
+    const hg_batch *ahead_batch = nullptr;
+    int32_t ahead_Hq = 0;
     // side stream: the split-K kernel runs beside the tcgen05 kernel (fork/join by events)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1148,9 +1153,43 @@ extern "C" hg_status hg_hybrid_step_host_workspace_size(const hg_kv_pool *pool, 
 // it runs and feed the tcgen05 tiles on a high-priority stream; their O goes
 // back to the host as soon as those tiles finish, the decode rows' after the
 // combine.  Runs of consecutive requests of one wave are copied as one range.
+static hg_status step_host_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q_host,
+                                const void *k_new_host, const void *v_new_host, void *out_host, void *workspace,
+                                size_t workspace_bytes, void *stream, bool sync);
+
 extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q,
                                          const void *q_host, const void *k_new_host, const void *v_new_host,
                                          void *out_host, void *workspace, size_t workspace_bytes, void *stream) {
+    return step_host_impl(pool, batch, H_q, q_host, k_new_host, v_new_host, out_host, workspace, workspace_bytes,
+                          stream, true);
+}
+
+extern "C" hg_status hg_hybrid_step_host_async(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q,
+                                               const void *q_host, const void *k_new_host, const void *v_new_host,
+                                               void *out_host, void *workspace, size_t workspace_bytes,
+                                               void *stream) {
+    return step_host_impl(pool, batch, H_q, q_host, k_new_host, v_new_host, out_host, workspace, workspace_bytes,
+                          stream, false);
+}
+
+extern "C" hg_status hg_hybrid_step_host_plan(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q) {
+    if (!pool || !batch) return fail(HG_E_INVALID, "NULL argument");
+    pool->ahead_ok = false;
+    BatchView v;
+    hg_status s = view_batch(batch, &v);
+    if (s) return s;
+    const hg_attn_opts ho = host_step_opts(v);
+    s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan_ahead, true);
+    if (s) return s;
+    pool->ahead_ok = true;
+    pool->ahead_batch = batch;
+    pool->ahead_Hq = H_q;
+    return HG_OK;
+}
+
+static hg_status step_host_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q, const void *q_host,
+                                const void *k_new_host, const void *v_new_host, void *out_host, void *workspace,
+                                size_t workspace_bytes, void *stream, bool sync) {
     static const bool trace = getenv("HG_E2E_TRACE") != nullptr;   // host-side phase times (stderr)
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
@@ -1234,7 +1273,12 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     static const bool no_zc = getenv("HG_E2E_NO_ZC") != nullptr;   // A/B: copy every row back
     const bool pinned_out = !no_zc && device_visible_host(out_host);
     const hg_attn_opts ho = host_step_opts(v);
-    s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan, true);
+    if (pool->ahead_ok && pool->ahead_batch == batch && pool->ahead_Hq == H_q) {
+        std::swap(pool->plan, pool->plan_ahead);   // planned while the previous step ran
+    } else {
+        s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan, true);
+    }
+    pool->ahead_ok = false;
     if (s) return bail(s);
     if (T == 0) return HG_OK;
     const size_t attn = pool->plan.total_bytes;
@@ -1295,6 +1339,7 @@ extern "C" hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch
     }   // else zero-copy: every row came from split-K / the combine
     if (s) return s;
     const auto t_d2 = now();
+    if (!sync) return HG_OK;   // hg_hybrid_step_host_async: the caller synchronises `stream`
     s = cuda_check(cudaStreamSynchronize(st), "stream sync");
     if (trace)
         fprintf(stderr, "hg_hybrid_step_host: prep %.1f us, attention + input copies enqueue %.1f, d2h %.1f, sync %.1f\n",

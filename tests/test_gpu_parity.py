@@ -364,6 +364,37 @@ def test_e2e_host_step_pageable_output(name):
         assert torch.equal(oh.view(torch.int16), wl.out.cpu().view(torch.int16)), pinned
 
 
+@pytest.mark.parametrize("name", ["toy_a", "c3"])
+def test_e2e_host_step_plan_ahead_async(name):
+    """The pipelined host step: hg_hybrid_step_host_plan for the next batch while the
+    current one runs, hg_hybrid_step_host_async (no final synchronise) -- the same bits
+    as the synchronous call; a plan made for another batch object is not used (that
+    call plans its own), and an invalid batch fails at plan time."""
+    import paper_2501_14808_b200 as hg
+    spec = _e2e_spec(name)
+    wl = make(spec)
+    torch.cuda.synchronize()
+    qh, kh, vh = (x.cpu().pin_memory() for x in (wl.q, wl.k_new, wl.v_new))
+    ws = torch.empty(hg.hg_hybrid_step_host_workspace_size(wl.pool, wl.batch, spec.H_q), dtype=torch.uint8,
+                     device="cuda")
+    ref = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16).pin_memory()
+    hg.hg_hybrid_step_host(wl.pool, wl.batch, spec.H_q, qh, kh, vh, ref, ws)
+    other = hg.Batch(wl.lay.block_table, [r.c for r in spec.requests], [r.n for r in spec.requests],
+                     [int(r.offline) for r in spec.requests], wl.lay.shared)   # same content, another object
+    hg.hg_hybrid_step_host_plan(wl.pool, wl.batch, spec.H_q)
+    for k in range(4):
+        oh = torch.full(wl.out.shape, 7.0, dtype=torch.bfloat16).pin_memory()
+        b = other if k == 2 else wl.batch   # k = 2: the plan-ahead is for wl.batch, not this object
+        hg.hg_hybrid_step_host_async(wl.pool, b, spec.H_q, qh, kh, vh, oh, ws)
+        hg.hg_hybrid_step_host_plan(wl.pool, wl.batch, spec.H_q)   # the next step's plan, beside the GPU
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(oh.view(torch.int16), ref.view(torch.int16)), k
+    bad = hg.Batch(wl.lay.block_table, [r.c for r in spec.requests], [r.n for r in spec.requests], None,
+                   [1] + [0] * (len(spec.requests) - 1))
+    if name == "toy_a":   # r0 appends into a block it would share: rejected when planned
+        assert hg.status_of(hg.hg_hybrid_step_host_plan, wl.pool, bad, spec.H_q) != hg.HG_OK
+
+
 def test_e2e_host_step_errors_leave_outputs_untouched():
     """hg_hybrid_step_host starts the decode rows' copies before validating; an
     invalid batch must still return its status with out_host and the pool untouched."""

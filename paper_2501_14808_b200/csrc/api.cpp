@@ -143,11 +143,15 @@ static hg_status stage_h2d(hg_kv_pool *pool, void *dst, const void *src, size_t 
 // of the call that used the slot before; the caller records `done` after its
 // last kernel (DescDone).
 template <typename Fill>
+// `cp`: the copy stream (NULL: the pool's own).  The host step passes its input copy
+// stream, so the descriptors go up in order with the input waves: on a separate stream
+// the copy engine may run a later wave's megabytes first and hold the kernels back.
 static hg_status stage_desc(hg_kv_pool *pool, const Fill &fill, size_t bytes, cudaStream_t st, void **dev,
-                            hg_kv_pool::DSlot **slot) {
+                            hg_kv_pool::DSlot **slot, cudaStream_t cp = nullptr) {
     hg_status s = HG_OK;
     if (!pool->cp) s = cuda_check(cudaStreamCreateWithFlags(&pool->cp, cudaStreamNonBlocking), "copy stream");
     if (s) return s;
+    if (!cp) cp = pool->cp;
     hg_kv_pool::DSlot &d = pool->dring[pool->dpos];
     pool->dpos = (pool->dpos + 1) % hg_kv_pool::kDRing;
     for (cudaEvent_t *e : {&d.ready, &d.done})
@@ -166,9 +170,9 @@ static hg_status stage_desc(hg_kv_pool *pool, const Fill &fill, size_t bytes, cu
         if (s) { d.dev = nullptr; return s; }
         d.cap = cap;
     }
-    if (d.used) s = cuda_check(cudaStreamWaitEvent(pool->cp, d.done, 0), "descriptor slot wait");
-    if (!s) s = stage_h2d_fill(pool, d.dev, bytes, pool->cp, fill);   // the image is assembled in the pinned slot
-    if (!s) s = cuda_check(cudaEventRecord(d.ready, pool->cp), "descriptor ready record");
+    if (d.used) s = cuda_check(cudaStreamWaitEvent(cp, d.done, 0), "descriptor slot wait");
+    if (!s) s = stage_h2d_fill(pool, d.dev, bytes, cp, fill);   // the image is assembled in the pinned slot
+    if (!s) s = cuda_check(cudaEventRecord(d.ready, cp), "descriptor ready record");
     if (!s) s = cuda_check(cudaStreamWaitEvent(st, d.ready, 0), "descriptor ready wait");
     if (s) return s;
     *dev = d.dev;
@@ -485,6 +489,7 @@ struct StepPipe {
                                                 // launch (so that launch is not delayed by the host)
     bool planned = false;                       // pool->plan already holds this batch's validated plan
     bool used = false;                          // out: the call was split into waves
+    cudaStream_t copy = nullptr;                // stream of the input copies (the descriptors follow them)
     uint16_t *zc_out = nullptr;                 // device-visible pinned host O: split-K and the combine
                                                 // store their final rows there (zero-copy result)
 };
@@ -751,7 +756,7 @@ static hg_status attention_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     void *dbase = nullptr;
     DescDone desc_done;
     desc_done.st = st;
-    s = stage_desc(pool, build_img, plan.desc_bytes, st, &dbase, &desc_done.slot);
+    s = stage_desc(pool, build_img, plan.desc_bytes, st, &dbase, &desc_done.slot, pipe ? pipe->copy : nullptr);
     if (s) return s;
     if (param_append && !sk_early) {
         s = cuda_check(cudaStreamWaitEvent(st, pool->ev_app, 0), "append wait");
@@ -1302,6 +1307,7 @@ static hg_status step_host_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     }
     StepPipe pipe;
     pipe.zc_out = zc;
+    pipe.copy = pool->h2d;
     pipe.in0 = pool->ev_in0;
     pipe.in1 = pool->ev_in1;
     pipe.side = pool->side_hi;

@@ -229,9 +229,10 @@ HG_API hg_status hg_hybrid_step_host(hg_kv_pool *pool, const hg_batch *batch, in
  *   hg_hybrid_step_host_async is hg_hybrid_step_host without the final synchronise:
  *   it returns once everything is queued on `stream`; out_host is valid, and the
  *   host input buffers may be reused, only after `stream` completes.  When the
- *   pool holds a plan-ahead for this same `batch` pointer and num_q_heads it is used
- *   instead of planning again -- the caller must not change the batch's arrays in
- *   between (nothing checks their contents).  Either way the plan-ahead is consumed.
+ *   pool holds a plan-ahead for this same `batch` pointer, num_q_heads, shape and
+ *   per-request lengths it is used instead of planning again -- the caller must not
+ *   change the block-table contents in between (only their address is compared).
+ *   Either way the plan-ahead is consumed.
  * A loop: plan(b0); for k: async(b_k); plan(b_{k+1}); synchronise(stream); ... keeps
  * each step's input upload after the previous step's result (the data dependency of
  * autoregressive decoding) and takes the validation and planning off the GPU's

@@ -47,6 +47,7 @@ struct hg_kv_pool {
     bool ahead_ok = false;
     const hg_batch *ahead_batch = nullptr;
     int32_t ahead_Hq = 0;
+    uint64_t ahead_fp = 0;
     // side stream: the split-K kernel runs beside the tcgen05 kernel (fork/join by events)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1177,6 +1178,19 @@ extern "C" hg_status hg_hybrid_step_host_async(hg_kv_pool *pool, const hg_batch 
                           stream, false);
 }
 
+// Cheap identity of a batch for the plan-ahead: its pointers, shape and per-request
+// lengths (not the block-table contents -- the caller keeps those unchanged).
+static uint64_t batch_fingerprint(const BatchView &v, const hg_batch *b) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t x) { h = (h ^ x) * 1099511628211ull; };
+    mix((uint64_t)(uintptr_t)b);
+    mix((uint64_t)(uintptr_t)v.bt);
+    mix((uint64_t)v.R);
+    mix((uint64_t)v.W);
+    for (int i = 0; i < v.R; ++i) mix(((uint64_t)(uint32_t)v.c[i] << 32) ^ ((uint64_t)(uint32_t)v.n[i] << 8) ^ (uint32_t)v.s[i]);
+    return h;
+}
+
 extern "C" hg_status hg_hybrid_step_host_plan(hg_kv_pool *pool, const hg_batch *batch, int32_t H_q) {
     if (!pool || !batch) return fail(HG_E_INVALID, "NULL argument");
     pool->ahead_ok = false;
@@ -1189,6 +1203,7 @@ extern "C" hg_status hg_hybrid_step_host_plan(hg_kv_pool *pool, const hg_batch *
     pool->ahead_ok = true;
     pool->ahead_batch = batch;
     pool->ahead_Hq = H_q;
+    pool->ahead_fp = batch_fingerprint(v, batch);
     return HG_OK;
 }
 
@@ -1278,7 +1293,8 @@ static hg_status step_host_impl(hg_kv_pool *pool, const hg_batch *batch, int32_t
     static const bool no_zc = getenv("HG_E2E_NO_ZC") != nullptr;   // A/B: copy every row back
     const bool pinned_out = !no_zc && device_visible_host(out_host);
     const hg_attn_opts ho = host_step_opts(v);
-    if (pool->ahead_ok && pool->ahead_batch == batch && pool->ahead_Hq == H_q) {
+    if (pool->ahead_ok && pool->ahead_batch == batch && pool->ahead_Hq == H_q &&
+        pool->ahead_fp == batch_fingerprint(v, batch)) {
         std::swap(pool->plan, pool->plan_ahead);   // planned while the previous step ran
     } else {
         s = plan_call(pool, batch, H_q, &ho, &v, &pool->plan, true);

@@ -333,3 +333,18 @@ def test_fit_80k_samples_fast():
     assert time.perf_counter() - t0 < 0.1   # SPEC.md:246 (paper: ~15 ms)
     m2 = hg.hg_predictor_fit([hg.features_from_array(x) for x in X[:1000]], y[:1000], OP.MASK_GRADED)
     assert m.n_samples == 80_000 and m2.n_samples == 1000
+
+
+def test_host_step_plan_ahead_validates_on_the_host():
+    """hg_hybrid_step_host_plan is host work only (validation + plan into the pool's
+    second plan slot): a valid batch plans, an invalid one returns the step's error."""
+    p = pool(64, H_kv=2, d=64)
+    bt = np.arange(3 * 4, dtype=np.int32).reshape(3, 4)
+    ok = hg.Batch(bt, [0, 32, 20], [16, 1, 1])
+    assert hg.status_of(hg.hg_hybrid_step_host_plan, p, ok, 4) == hg.HG_OK
+    dup = bt.copy()
+    dup[2, 0] = dup[1, 0]   # a private block used by two rows
+    assert hg.status_of(hg.hg_hybrid_step_host_plan, p, hg.Batch(dup, [0, 32, 20], [16, 1, 1]), 4) == hg.HG_E_INVALID
+    shared_write = hg.Batch(bt, [0, 32, 20], [16, 1, 1], None, [1, 0, 0])   # r0 appends into its shared block
+    assert hg.status_of(hg.hg_hybrid_step_host_plan, p, shared_write, 4) == hg.HG_E_SHARED_WRITE
+    assert hg.status_of(hg.hg_hybrid_step_host_plan, p, ok, 3) == hg.HG_E_INVALID   # 3 q heads on 2 KV heads

@@ -225,6 +225,17 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
     const int it_begin = p.tc_off[blockIdx.x], it_end = p.tc_off[blockIdx.x + 1];
     auto nkt_of = [&](const TcItem &it) { return (it.k1 - it.k0 + kTcKeys - 1) / kTcKeys; };
     auto ntiles_of = [&](const TcItem &it) { return it.nrows > kTcRows ? 2 : 1; };
+    // KV tiles Q tile t of a prefill item needs: up to the causal limit of its last
+    // row (tile 0 of a 256-row item stops one tile before tile 1 -- its last tile
+    // would be fully masked).  The last Q tile needs them all; prefix nodes too.
+    auto nkt_tile = [&](const TcItem &it, int t) {
+        const int nkt = nkt_of(it);
+        if (it.mode != 0 || t == ntiles_of(it) - 1) return nkt;
+        const int x_last = it.hl0 + min(kTcRows * (t + 1), it.nrows) - 1;
+        const int lim = min(it.k1, it.pos0 + x_last / p.G_q + 1);
+        const int n = (lim - it.k0 + kTcKeys - 1) / kTcKeys;
+        return n < 1 ? 1 : (n > nkt ? nkt : n);
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < L::kKStages; ++i) {
@@ -442,6 +453,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         for (int item = it_begin; item < it_end; ++item, ++n_item) {
             const TcItem it = p.tc[item];
             const int nkt = nkt_of(it), ntiles = ntiles_of(it);
+            const int nkt0 = nkt_tile(it, 0);   // tile 0's steps (tile 1, if any, takes all nkt)
             const bool trace = tr && item == it_begin;
             auto issue_qk = [&](int t, int64_t kt, bool last_tile) {
                 const uint32_t tS = tmem + 256 * t;
@@ -470,11 +482,13 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             for (int j = 0; j < nkt; ++j, ++gk, ++gv) {
                 const int s = (int)(gv & 1);
                 const uint64_t dv = dV0 + (uint64_t)((s * L::kKV) >> 4);
+                bool kfull_next = false;   // K(j + 1) waited for (before the first QK of step j + 1)
                 for (int t = 0; t < ntiles; ++t) {
+                    if (t == 0 && j >= nkt0) continue;   // tile 0 is past its causal range
                     // PV in two halves: keys 0-63 as soon as the softmax has written them
                     mbar_wait(bar(BAR_PHALF + t), ps[t] & 1);
                     if (trace && j < 64 && lane == 0) tr[8 * j + 2 * t] = clock64();
-                    if (t == 0) mbar_wait(bar(BAR_VFULL + s), (gv >> 1) & 1);
+                    if (t == 0 || j >= nkt0) mbar_wait(bar(BAR_VFULL + s), (gv >> 1) & 1);   // first tile of the step
                     tc_fence_after();
                     const uint32_t tS = tmem + 256 * t, tO = tS + 128;
 #pragma unroll
@@ -494,10 +508,11 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                         __syncwarp();
                     }
                     ++ps[t];
-                    if (j + 1 < nkt) {
-                        if (t == 0) {
+                    if (j + 1 < (t == 0 ? nkt0 : nkt)) {
+                        if (!kfull_next) {
                             mbar_wait(bar(BAR_KFULL + (gk + 1) % L::kKStages), ((gk + 1) / L::kKStages) & 1);
                             tc_fence_after();
+                            kfull_next = true;
                         }
                         issue_qk(t, gk + 1, t == ntiles - 1);   // in order after PV(t, j): S/P of tile t is free
                     }
@@ -522,7 +537,8 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
         int n_item = 0;
         for (int item = it_begin; item < it_end; ++item, ++n_item) {
             const TcItem it = p.tc[item];
-            const int nkt = nkt_of(it), ntiles = ntiles_of(it);
+            const int ntiles = ntiles_of(it);
+            const int nkt = t < ntiles ? nkt_tile(it, t) : 0;   // this Q tile's KV steps
             const bool trace = tr && item == it_begin;
             const bool valid = rr < it.nrows;
             struct { int t, h, lim; } row{0, 0, 0};

@@ -2,7 +2,7 @@
 attention of a prefill-heavy config, L2 flushed; median over reps of the makespan
 and the spread of CTA end times (the planner's assign_tc decides it).
 
-python tools/trace_tc_grid.py p1 p2      (HG_NO_TC_CUTS / HG_TC_ITEM_COST: planner A/B)
+python tools/trace_tc_grid.py p1 p2
 """
 import os
 import sys
@@ -16,7 +16,7 @@ import paper_2501_14808_b200 as hg
 from paper_2501_14808_b200.harness import Workload
 from synth.configs import make_config
 
-tag = f"cuts={'off' if os.environ.get('HG_NO_TC_CUTS') else 'on'} item_cost={os.environ.get('HG_TC_ITEM_COST', '4')}"
+tag = os.path.basename(os.environ.get("HG_SO_OVERRIDE", "default"))
 flush = torch.zeros(512 << 20, dtype=torch.uint8, device="cuda")
 for name in sys.argv[1:]:
     wl = Workload(make_config(name, 0))

@@ -179,7 +179,9 @@ struct TcSmem {
 };
 
 enum { BAR_KFULL = 0, BAR_KEMPTY = 3, BAR_VFULL = 6, BAR_VEMPTY = 8, BAR_SFULL = 10, BAR_PFULL = 12, BAR_ODONE = 14,
-       BAR_QREADY = 15, BAR_PHALF = 16, BAR_OFREE = 18, BAR_N = 19 };
+       BAR_QREADY = 15, BAR_PHALF = 16, BAR_OFREE = 18, BAR_ODONE1 = 19, BAR_N = 20 };
+// O of Q tile t final: BAR_ODONE (t = 0; committed right after tile 0's last PV, so its
+// epilogue overlaps tile 1's last step) / BAR_ODONE1 (t = 1; at the item's end)
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -250,6 +252,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             mbar_init(bar(BAR_PHALF + i), 128);
         }
         mbar_init(bar(BAR_ODONE), 1);
+        mbar_init(bar(BAR_ODONE1), 1);
         mbar_init(bar(BAR_QREADY), 256);
         mbar_init(bar(BAR_OFREE), 256);
         asm volatile("st.shared.u32 [%0], 0;\n" ::"r"(s_zero) : "memory");
@@ -508,6 +511,8 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                         __syncwarp();
                     }
                     ++ps[t];
+                    if (t == 0 && j == nkt0 - 1 && elect_one()) umma_commit(bar(BAR_ODONE));   // tile 0's O final
+                    __syncwarp();
                     if (j + 1 < (t == 0 ? nkt0 : nkt)) {
                         if (!kfull_next) {
                             mbar_wait(bar(BAR_KFULL + (gk + 1) % L::kKStages), ((gk + 1) / L::kKStages) & 1);
@@ -521,7 +526,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                 if (elect_one()) umma_commit(bar(BAR_VEMPTY + s));   // every PV read V(j)
                 __syncwarp();
             }
-            if (elect_one()) umma_commit(bar(BAR_ODONE));
+            if (elect_one()) umma_commit(bar(BAR_ODONE1));   // tile 1's O (and every MMA of the item) final
             __syncwarp();
         }
     } else if (warp < 8) {
@@ -671,7 +676,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
                     if (trace && r == 0 && j < 64) tr[512 + 256 * t + 2 * j + 1] = clock64();
                 }
                 // ---- epilogue ----
-                mbar_wait(bar(BAR_ODONE), n_item & 1);
+                mbar_wait(bar(t == 0 ? BAR_ODONE : BAR_ODONE1), n_item & 1);
                 tc_fence_after();
                 const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
                 const float lse2 = l_sum > 0.f ? m_used + __log2f(l_sum) : -CUDART_INF_F;
@@ -727,7 +732,7 @@ tc_attn_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmap_k,
             } else {
                 // an unused Q tile holds no O; stay in step with the item (QREADY / OFREE
                 // phases must not mix arrivals of different items)
-                mbar_wait(bar(BAR_ODONE), n_item & 1);
+                mbar_wait(bar(t == 0 ? BAR_ODONE : BAR_ODONE1), n_item & 1);
                 mbar_arrive(bar(BAR_OFREE));
             }
         }

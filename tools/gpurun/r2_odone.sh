@@ -1,0 +1,14 @@
+# tcgen05: tile 0's O released right after its last PV (its epilogue overlaps tile 1's last
+# step): guarded smoke, parity, p1 / p2 A/B against the previous kernel (var/libhygen_prev.so)
+mkdir -p gpurun_out/r2_odone
+O=gpurun_out/r2_odone
+timeout -s KILL 180 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "test_toy" > $O/smoke_tests.log 2>&1
+echo rc=$? >> $O/smoke_tests.log
+if grep -q "rc=0" $O/smoke_tests.log; then
+  timeout -s KILL 1500 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider > $O/tests.log 2>&1
+  echo rc=$? >> $O/tests.log
+  for r in 1 2; do
+    timeout -s KILL 300 python tools/exp_tc.py p1 p2 >> $O/tc.log 2>&1
+    HG_SO_OVERRIDE=$PWD/paper_2501_14808_b200/var/libhygen_prev.so timeout -s KILL 300 python tools/exp_tc.py p1 p2 >> $O/tc.log 2>&1
+  done
+fi
